@@ -1,0 +1,374 @@
+"""TensorACO-B200 benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c3] [--construct sorted|dense]
+
+A "step" is one full ACO iteration of the hot path (bench.py:199-206 of the
+reference): construct m tours -> lengths -> stable elite sort -> index-mapped
+deposit + evaporation -> P and the selection table for the next iteration.
+The default workload is BASELINE.json's metric config: synthetic uniform
+Euclidean n=2392 cities, m=4096 ants (k=409), AdaIR, on 1 GPU.  Under
+torchrun the ants are sharded over the ranks (weak in the colony sense: the
+whole colony is fixed and split).
+
+--impl reference times the reference algorithm (oracle/reference_port, the
+numpy restatement pinned against the reference's golden vectors) on the host
+cores: one sampled-and-extrapolated iteration per step, one independent colony
+per core (the reference is single-threaded numpy).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (n, m, selection)  — BASELINE.json configs
+    "c1": (51, 64, "ir"),
+    "c2": (1000, 1024, "adair"),
+    "c3": (2392, 4096, "adair"),
+    "c3ir": (2392, 4096, "ir"),
+    "c4": (10000, 8192, "ir"),
+    "c5_256": (5000, 256, "ir"),
+    "c5_4096": (5000, 4096, "ir"),
+    "c5_65536": (5000, 65536, "ir"),
+}
+METRIC = "ACO iterations/sec at n=2392, m=4096 (city-selections/sec = m*(n-1)*it/s)"
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK = 6650.0  # GB/s, /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def _peaks() -> tuple[float, str]:
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except (OSError, KeyError, ValueError):
+        return HBM_FALLBACK, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows: list[list[str]] = []
+        self._stop = threading.Event()
+        self._thread = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                for line in out.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:  # noqa: BLE001 - sampling is best effort
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._thread = threading.Thread(target=self._run, daemon=True)
+        self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread is not None:
+            self._thread.join(timeout=10)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+# ---------------------------------------------------------------------------
+def _dist_init(gpus: int):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, world, local
+
+
+def _max_over_ranks(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def _barrier(world: int) -> None:
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args) -> dict | None:
+    import torch
+
+    rank, world, local = _dist_init(args.gpus)
+    import paper_2404_04895_b200 as taco
+    from paper_2404_04895_b200 import _device, _lib
+
+    n, m, selection = CONFIGS[args.config]
+    k = max(1, m // 10)
+    period = args.warmup + args.steps
+    coords = np.random.default_rng(0).uniform(0.0, 2000.0, (n, 2))
+    inst = taco.euclidean_instance(coords)
+    params = taco.AcoParams(m=m, k=k, selection=selection, seed=0,
+                            gamma_schedule=taco.GammaSchedule(1.5, 1.0, period))
+    dev = _device.device()
+
+    # ---- e2e: solve from host buffers through the public API ---------------
+    # timed: host instance -> Solver (H2D of dist + eta), then K x step()
+    # each returning the best tour + length to the host (D2H)
+    e2e_inst = inst
+    warm = taco.Solver(e2e_inst, params, construct=args.construct)
+    for _ in range(args.warmup):
+        warm.step()
+    del warm
+    _device._INSTANCES.clear()
+    torch.cuda.synchronize()
+    _barrier(world)
+    t0 = time.perf_counter()
+    e2e_solver = taco.Solver(e2e_inst, params, construct=args.construct)
+    for _ in range(args.steps):
+        best_tour, best_len = e2e_solver.step()
+    torch.cuda.synchronize()
+    e2e_s = _max_over_ranks(time.perf_counter() - t0, world)
+    del e2e_solver
+
+    # ---- device-timed value ------------------------------------------------
+    solver = taco.Solver(inst, params, construct=args.construct)
+    for _ in range(args.warmup):
+        solver.step_async()
+    solver.check()
+    torch.cuda.synchronize()
+    timers = {"construct": [], "update": []}
+    scan = torch.zeros(1, dtype=torch.int64, device=dev)
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
+    _barrier(world)
+    torch.cuda.synchronize()
+    start.record()
+    for _ in range(args.steps):
+        solver.step_async(timers=timers, scan_count=scan if args.construct == "sorted" else None)
+    end.record()
+    torch.cuda.synchronize()
+    if sampler:
+        sampler.__exit__()
+    solver.check()
+    _barrier(world)
+    elapsed_ms = _max_over_ranks(start.elapsed_time(end), world)
+    ms_per_step = elapsed_ms / args.steps
+    t_construct = float(np.mean([a.elapsed_time(b) for a, b in timers["construct"]]))
+    t_update = float(np.mean([a.elapsed_time(b) for a, b in timers["update"]]))
+    windows = int(scan.item()) / args.steps
+
+    # ---- L2-flushed variant: 256 MB scrub before every iteration ----------
+    scrub = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
+    flushed = []
+    for _ in range(min(args.steps, 10)):
+        scrub.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        solver.step_async()
+        b.record()
+        torch.cuda.synchronize()
+        flushed.append(a.elapsed_time(b))
+    flushed_ms = _max_over_ranks(float(np.mean(flushed)), world)
+
+    # ---- the north-star full-row streaming kernel on the same state -------
+    dense_ms = None
+    if args.construct == "sorted" and n <= 20480:
+        pmat = torch.from_numpy(solver.probability().p).to(dev)
+        dt = _device.SelectionTables(n, dev, dense=True, sorted_=False)
+        g = taco.colony.construction_gamma(params, solver.iteration)
+        _device.selection_table_from_p(pmat, 1.0 / g, dt)
+        tours = torch.zeros((solver.shard.count, n), dtype=torch.int32, device=dev)
+        st = _device.new_status(dev)
+        reps = []
+        for r in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            _device.construct(n, solver.shard.count, solver.shard.offset, _lib.CONSTRUCT_DENSE, dt, 0,
+                              solver.iteration, tours, st)
+            b.record()
+            torch.cuda.synchronize()
+            reps.append(a.elapsed_time(b))
+        dense_ms = float(np.median(reps))
+        del dt, tours
+
+    if rank != 0:
+        return None
+
+    it_per_s = 1000.0 / ms_per_step
+    peak, peak_kind = _peaks()
+    m_local = solver.shard.count
+    # algorithmic bytes of the sorted kernel per launch: table windows read
+    # (32 entries x (4 B value + 2 B index)) + the m_local x n int32 tours
+    alg_sorted = windows * 32 * 6 + m_local * n * 4
+    # the reference's full-row gather: m (n-1) n 4 B per launch
+    alg_full = m_local * (n - 1) * n * 4
+    dom_ms = t_construct
+    roof = {"kernel": f"k_construct_{args.construct}", "bound": "hbm",
+            "achieved": (alg_sorted if args.construct == "sorted" else alg_full) / (dom_ms * 1e-3) / 1e9,
+            "peak": peak, "unit": "GB/s", "peak_kind": peak_kind, "traffic": None,
+            "ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step,
+            "alg_bytes_per_launch": alg_sorted if args.construct == "sorted" else alg_full,
+            "alg_bytes_def": ("sorted-table windows*32*6 B + tours m*n*4 B" if args.construct == "sorted"
+                              else "full-row stream m*(n-1)*n*4 B (SURVEY 8d)"),
+            "reference_equivalent_GBps": alg_full / (dom_ms * 1e-3) / 1e9}
+    roof["frac"] = roof["achieved"] / peak
+    line = {
+        "metric": METRIC, "value": it_per_s, "unit": "iterations/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32",
+        "data": "synthetic: U(0,2000)^2 Euclidean cities (seed 0), unrounded distances",
+        "config": {"workload": f"{args.config}: n={n} cities, m={m} ants, k={k}, {selection}, "
+                               f"alpha=1 beta=2 rho=0.1, gamma 1.5->1.0 period {period}",
+                   "n": n, "m": m, "k": k, "selection": selection, "construct": args.construct,
+                   "parallelism": f"ants sharded over {world} GPU(s)",
+                   "l2": "back-to-back iterations; per-iteration state (tau, eta^b, dist, tables, "
+                         "tours) > 126 MB L2; value_l2_flushed scrubs 256 MB before each iteration"},
+        "selections_per_s": m * (n - 1) * it_per_s,
+        "value_l2_flushed": 1000.0 / flushed_ms,
+        "kernel_ms": {"construct": t_construct, "update_p": t_update,
+                      "construct_dense_full_row": dense_ms},
+        "roofline": roof,
+        "e2e": {"value": args.steps / e2e_s, "unit": "iterations/s",
+                "h2d_bytes_per_step": (2 * n * n * 8) / args.steps,
+                "d2h_bytes_per_step": n * 4 + 8 + 16,
+                "what": "Solver(host instance: dist+eta H2D) + K x step() returning best tour/length (D2H)"},
+        "gpu_launches": args.steps * 6,
+        "gpu_launches_note": "6 libtaco kernels per iteration + CUB radix-sort kernels of the elite sort",
+        "best_length": best_len,
+    }
+    if dense_ms is not None:
+        line["roofline_dense"] = {"kernel": "k_construct_dense", "bound": "hbm",
+                                  "achieved": alg_full / (dense_ms * 1e-3) / 1e9, "peak": peak,
+                                  "unit": "GB/s", "frac": alg_full / (dense_ms * 1e-3) / 1e9 / peak,
+                                  "ms_per_launch": dense_ms,
+                                  "alg_bytes_def": "full-row stream m*(n-1)*n*4 B (SURVEY 8d)"}
+    if sampler:
+        line["clocks"] = sampler.summary()
+    if world == 1 and not args.no_cpu_baseline:
+        from oracle import cpu_baseline
+
+        s = cpu_baseline.sample_iteration(n, m, k, selection, seed=0, steps=args.cpu_steps, period=period)
+        line["cpu_baseline"] = {
+            "value": 1.0 / s["t_iter"], "unit": "iterations/s", "cores": 1, "kind": "port",
+            "sample": (f"oracle/reference_port, 1 thread: {s['steps_sampled']} construction steps "
+                       f"(mean {s['t_step'] * 1e3:.1f} ms) x (n-1) + P {s['t_p'] * 1e3:.0f} ms + logw "
+                       f"{s['t_logw'] * 1e3:.0f} ms + lengths {s['t_costs'] * 1e3:.0f} ms + update "
+                       f"{s['t_update'] * 1e3:.0f} ms; extrapolated"),
+            "t_iter_s": s["t_iter"]}
+    return line
+
+
+# ---------------------------------------------------------------------------
+# reference arm
+# ---------------------------------------------------------------------------
+def run_reference(args) -> dict | None:
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return None
+    from oracle import cpu_baseline
+
+    n, m, selection = CONFIGS[args.config]
+    k = max(1, m // 10)
+    cores = max(1, min(os.cpu_count() or 1, args.ref_procs))
+    # warm-up samples (untimed), then K sampled iterations, `cores` colonies at a time
+    if args.warmup:
+        cpu_baseline.parallel_samples(n, m, k, selection, min(args.warmup, cores), cores, steps=2)
+    t0 = time.perf_counter()
+    times = cpu_baseline.parallel_samples(n, m, k, selection, args.steps, cores, steps=args.cpu_steps)
+    wall = time.perf_counter() - t0
+    per_colony = 1.0 / float(np.mean(times))
+    value = per_colony * min(cores, args.steps)
+    return {
+        "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "data": "synthetic: U(0,2000)^2 Euclidean cities (seed 0), unrounded distances",
+        "config": {"workload": f"{args.config}: n={n} cities, m={m} ants, k={k}, {selection}",
+                   "n": n, "m": m, "k": k, "selection": selection},
+        "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": min(cores, args.steps),
+                         "kind": "port",
+                         "sample": (f"oracle/reference_port (numpy restatement of antbatch, pinned to its "
+                                    f"golden vectors): each step = one iteration extrapolated from "
+                                    f"{args.cpu_steps} construction steps; {min(cores, args.steps)} independent "
+                                    f"single-threaded colonies in parallel; per-colony "
+                                    f"{per_colony:.3g} it/s"),
+                         "wall_s": wall},
+        "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
+    ap.add_argument("--construct", choices=("sorted", "dense"), default="sorted")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-steps", type=int, default=6)
+    ap.add_argument("--ref-procs", type=int, default=16)
+    args = ap.parse_args()
+    if args.warmup < 0 or args.steps < 1:
+        ap.error("need --steps >= 1 and --warmup >= 0")
+    line = run_reference(args) if args.impl == "reference" else run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1 and args.impl == "ours":
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,186 @@
+/*
+ * taco.h — C ABI of libtaco.so, the B200 (sm_100a) engine behind the
+ * TensorACO hot path: one ACO iteration with Independent-Roulette (IR) or
+ * Adaptive-IR (AdaIR) selection.
+ *
+ * The reference (`antbatch`, /root/reference/pkg/src/antbatch) is a pure
+ * Python/numpy package and has no FFI of its own; its "plugin boundary" is the
+ * set of module-level functions listed below.  Each entry point here names the
+ * reference function it replaces (file:line) and is what the Python host layer
+ * (paper_2404_04895_b200/) binds through ctypes.
+ *
+ * Conventions
+ *   - Every pointer argument is a DEVICE pointer unless its name ends in _host.
+ *     Matrices are row-major (C order), n x n, leading dimension n unless a
+ *     separate ld argument is given.
+ *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous on
+ *     that stream and never allocates memory (callers pass workspaces).
+ *   - `status` points to 4 device int32 words, zeroed by the caller.  Kernels
+ *     record the first data-dependent failure there: status[0] = code
+ *     (TACO_UNDERFLOW / TACO_NO_CANDIDATE), status[1] = smallest offending
+ *     row (underflow) or ant (no candidate).
+ *   - The return value reports argument / launch errors synchronously:
+ *     0 = launched, negative = error (see taco_status_string).
+ */
+#ifndef TACO_H_
+#define TACO_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TACO_ABI_VERSION 1
+
+/* status codes (return values and status[0]) */
+#define TACO_OK 0
+#define TACO_UNDERFLOW 1          /* colony.py:63-68  NumericalUnderflow          */
+#define TACO_NO_CANDIDATE 2       /* colony.py:149   "selector chose a visited city" */
+#define TACO_ERR_ARG (-1)         /* bad argument (ValueError on the Python side)  */
+#define TACO_ERR_CUDA (-2)        /* CUDA launch / runtime error                  */
+#define TACO_ERR_UNSUPPORTED (-3) /* size outside the compiled kernel variants    */
+
+/* construction variants for taco_construct */
+#define TACO_CONSTRUCT_SORTED 0 /* pruned scan of the per-row descending table   */
+#define TACO_CONSTRUCT_DENSE 1  /* full-row streaming scan of dense W            */
+
+int taco_abi_version(void);
+const char *taco_status_string(int code);
+/* largest n the sorted-table (per-row block radix sort) path supports */
+int taco_max_sorted_n(void);
+
+/*
+ * Fused row kernel: evaporation + index-mapped deposit + P = RowNorm(tau^a eta^b)
+ * + the fp32 selection table W = P^(1/gamma) (dense and/or row-sorted).
+ * One CTA per row.  Replaces, in one pass over tau:
+ *   pheromone.accumulate_increments   pheromone.py:52-68   (delta source)
+ *   pheromone.apply_update            pheromone.py:71-83   (do_evap != 0)
+ *   colony.compute_probability_matrix colony.py:51-69      (p_out / rowsum_out)
+ *   selection.scaled_log_weights      selection.py:62-75   (folded into W)
+ *
+ * Delta source (at most one): nbr+inc (k elites; nbr[r*n + i] = (prev, next)
+ * of city i in elite r's tour, inc[r] = 1/cost_r, rank order r = 0..k-1) or a
+ * dense delta_in (n x n).  With neither, delta = 0.
+ * tau' = max(keep*tau + delta, 1e-12) when do_evap, else tau' = tau_in.
+ * eta_b = eta^beta (precomputed once per instance, n x n).
+ * Outputs (each nullable): delta_out, tau_out (may alias tau_in), p_out,
+ * rowsum_out (n), w_out (n x ldw fp32, pad columns zeroed), sw_out/si_out
+ * (n x n fp32 values / uint16 column indices, each row sorted descending).
+ * eta_b / p outputs are skipped when want_p == 0 (delta/tau-only modes).
+ */
+int taco_row_update(int n,
+                    const double *tau_in, double *tau_out,
+                    const double *eta_b,
+                    const int32_t *nbr, const double *inc, int k,
+                    const double *delta_in, double *delta_out,
+                    int do_evap, double keep,
+                    int want_p, double alpha, double inv_gamma,
+                    double *p_out, double *rowsum_out,
+                    float *w_out, int ldw,
+                    float *sw_out, uint16_t *si_out,
+                    int32_t *status, void *stream);
+
+/*
+ * Selection table from a given P (construct_tours drop-in, colony.py:116):
+ * W = fp32(P^(1/gamma)) dense (n x ldw) and/or row-sorted (sw_out/si_out).
+ */
+int taco_selection_table(int n, const double *p, double inv_gamma,
+                         float *w_out, int ldw, float *sw_out,
+                         uint16_t *si_out, void *stream);
+
+/*
+ * eta^beta with numpy's scalar-exponent dispatch (colony.py:60): exponents
+ * 0, 0.5, 1, 2 are exact (ones / sqrt / copy / square), others use pow.
+ */
+int taco_eta_power(int64_t count, const double *eta, double beta, double *out,
+                   void *stream);
+
+/*
+ * Tour construction, fast path (device Philox4x32-10 stream).
+ * Replaces colony.construct_tours colony.py:87-154 (IR / AdaIR branch) with
+ * the deviate block of rng.step_exponentials rng.py:42-49 replaced by the
+ * on-chip keyed uniform u(seed, iteration, step, ant, city) and the log-domain
+ * rule argmax(log P/gamma - E) by its product form argmax(W * u).
+ * Ants [ant_offset, ant_offset + m_local) are built; tours_out is
+ * m_local x n int32.  variant: TACO_CONSTRUCT_SORTED (needs sw/si) or
+ * TACO_CONSTRUCT_DENSE (needs w, ldw).  scan_count (nullable, device u64) is
+ * incremented by the number of 32-entry table windows the SORTED variant read
+ * (a traffic probe for the roofline report).
+ */
+int taco_construct(int n, int m_local, int ant_offset, int variant,
+                   const float *w, int ldw,
+                   const float *sw, const uint16_t *si,
+                   uint64_t seed, uint32_t iteration,
+                   int32_t *tours_out, int32_t *status,
+                   unsigned long long *scan_count, void *stream);
+
+/* Start cities of the device stream (rng.start_cities rng.py:65-68 analog). */
+int taco_starts(int n, int m_local, int ant_offset, uint64_t seed,
+                uint32_t iteration, int32_t *starts_out, void *stream);
+
+/* Raw device uniforms for given (step, ant, city) triples (test hook). */
+int taco_uniforms(int count, const uint32_t *step, const uint32_t *ant,
+                  const uint32_t *city, uint64_t seed, uint32_t iteration,
+                  float *u_out, void *stream);
+
+/* Philox4x32-10 bijection on `count` (counter, key) pairs (KAT hook). */
+int taco_philox4x32_10(int count, const uint32_t *ctr4, const uint32_t *key2,
+                       uint32_t *out4, void *stream);
+
+/*
+ * Reference-stream selection step (bit-exact parity mode).  One lockstep
+ * round of colony.py:143-152: next = argmax_j(logw[cur, j] - e[a, j]) with
+ * visited cities at -inf and first-of-ties (selection.py:143-155), the
+ * visited assert (colony.py:149), then current/visited/tours update.
+ * logw n x n f64, e_block m x n f64, current m int64, visited m x n uint8,
+ * tours m x n int64 (column `step` written).
+ */
+int taco_select_parity(int n, int m, int step, const double *logw,
+                       const double *e_block, int64_t *current,
+                       uint8_t *visited, int64_t *tours,
+                       int32_t *status, void *stream);
+
+/* logw = log(p)/gamma, -inf where p == 0 (selection.py:62-75). */
+int taco_log_weights(int64_t count, const double *p, double gamma,
+                     double *logw_out, void *stream);
+
+/*
+ * Tour lengths: costs[a] = pairwise-sum_s dist[t[s], t[(s+1) % n]] in numpy's
+ * pairwise order (model.batch_costs model.py:292-295).  tours int32 or int64
+ * (tours_is_i64), m x n.
+ */
+int taco_tour_cost(int n, int m, const void *tours, int tours_is_i64,
+                   const double *dist, double *costs_out, void *stream);
+
+/*
+ * Stable ascending argsort of m costs (pheromone.select_elite
+ * pheromone.py:17-25 = np.argsort(kind="stable")).  order_out has m entries.
+ */
+size_t taco_elite_workspace_bytes(int m);
+int taco_elite_order(int m, const double *costs, int32_t *order_out,
+                     void *workspace, size_t ws_bytes, void *stream);
+
+/*
+ * Elite edge map for the fused deposit: nbr[r*n + t[s]] = (t[s-1], t[s+1])
+ * and inc[r] = 1.0 / cost of elite r = order[r] (pheromone.py:52-68,
+ * edge_index_matrix pheromone.py:28-38).  tours int32 (ld = n) or int64.
+ */
+int taco_elite_neighbors(int n, int k, const void *tours, int tours_is_i64,
+                         const int32_t *order, const double *costs,
+                         int32_t *nbr_out, double *inc_out, void *stream);
+
+/*
+ * Best-so-far tracking for Solver.step(): if costs[order[0]] < *best_cost,
+ * copy that tour to best_tour and update best_cost / best_iter.
+ */
+int taco_track_best(int n, const int32_t *tours, const double *costs,
+                    const int32_t *order, double *best_cost,
+                    int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
+                    void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TACO_H_ */

@@ -1,0 +1,160 @@
+"""ORACLE (test infrastructure only): numpy restatement of the engine's device
+stream and product-form selection rule.
+
+The device rule replaces the reference's per-step Exp(1) block
+(rng.py:42-49) with counter-addressed uniforms and evaluates
+argmax(log P / gamma - E) (selection.py:143-155) in its product form
+argmax(W * u), W = fp32(P^(1/gamma)).  This module restates that rule with
+plain numpy so the CUDA kernels can be checked bit for bit, and also
+evaluates the reference's log-domain rule on the same uniforms so the
+product/log agreement can be counted.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+M0, M1 = 0xD2511F53, 0xCD9E8D57
+W0, W1 = 0x9E3779B9, 0xBB67AE85
+MASK32 = 0xFFFFFFFF
+
+
+def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:
+    """Random123 Philox4x32-10 on (N, 4) counters and (N, 2) or (2,) keys."""
+    c = [np.asarray(ctr[..., i], dtype=np.uint64) for i in range(4)]
+    key = np.asarray(key, dtype=np.uint64)
+    k0 = np.broadcast_to(key[..., 0], c[0].shape).copy()
+    k1 = np.broadcast_to(key[..., 1], c[0].shape).copy()
+    for _ in range(10):
+        p0 = c[0] * M0
+        p1 = c[2] * M1
+        hi0, lo0 = p0 >> 32, p0 & MASK32
+        hi1, lo1 = p1 >> 32, p1 & MASK32
+        c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
+        k0 = (k0 + W0) & MASK32
+        k1 = (k1 + W1) & MASK32
+    return np.stack(c, axis=-1).astype(np.uint32)
+
+
+def seed_key(seed: int) -> np.ndarray:
+    return np.array([seed & MASK32, (seed >> 32) & MASK32], dtype=np.uint64)
+
+
+def bits_to_uniform(x: np.ndarray) -> np.ndarray:
+    """((x >> 9) + 0.5) * 2^-23 as float32 — exact, in (0, 1)."""
+    k = (np.asarray(x, dtype=np.uint32) >> np.uint32(9)).astype(np.float32)
+    return k * np.float32(2.0 ** -23) + np.float32(2.0 ** -24)
+
+
+def uniforms(seed: int, iteration: int, step, ant, city) -> np.ndarray:
+    """u(seed, iteration, step, ant, city); arrays broadcast together."""
+    step, ant, city = np.broadcast_arrays(np.asarray(step, dtype=np.uint64),
+                                          np.asarray(ant, dtype=np.uint64),
+                                          np.asarray(city, dtype=np.uint64))
+    ctr = np.stack([city >> 2, step, ant, np.full_like(city, iteration & MASK32)], axis=-1)
+    words = philox4x32_10(ctr, seed_key(seed))
+    pick = np.take_along_axis(words, (city & 3).astype(np.int64)[..., None], axis=-1)[..., 0]
+    return bits_to_uniform(pick)
+
+
+def starts(seed: int, iteration: int, ants, n: int) -> np.ndarray:
+    """Device start cities: Lemire bound of word 0 of counter (0, 0, ant, it)."""
+    ants = np.asarray(ants, dtype=np.uint64)
+    z = np.zeros_like(ants)
+    ctr = np.stack([z, z, ants, np.full_like(ants, iteration & MASK32)], axis=-1)
+    x = philox4x32_10(ctr, seed_key(seed))[..., 0].astype(np.uint64)
+    return ((x * np.uint64(n)) >> np.uint64(32)).astype(np.int64)
+
+
+def selection_table(p: np.ndarray, g: float) -> np.ndarray:
+    """W = fp32(P^(1/g)); exact for g == 1.  (For g != 1 numpy's pow may
+    differ from CUDA's by an ulp before rounding; parity tests therefore feed
+    the device-built W to `build_tours`.)"""
+    if g == 1.0:
+        return p.astype(np.float32)
+    return np.power(p, 1.0 / g).astype(np.float32)
+
+
+def build_tours(w: np.ndarray, seed: int, iteration: int, ants) -> np.ndarray:
+    """Full-scan product-form construction for the given global ant ids:
+    next = argmax_j W[cur, j] * u over unvisited j with W > 0, first of ties."""
+    n = w.shape[0]
+    ants = np.asarray(ants, dtype=np.int64)
+    a = ants.size
+    rows = np.arange(a)
+    cur = starts(seed, iteration, ants, n)
+    seen = np.zeros((a, n), dtype=bool)
+    seen[rows, cur] = True
+    tours = np.empty((a, n), dtype=np.int64)
+    tours[:, 0] = cur
+    cities = np.arange(n, dtype=np.uint64)
+    for step in range(1, n):
+        u = uniforms(seed, iteration, step, ants[:, None], cities[None, :])
+        wr = w[cur]
+        score = wr * u  # float32 x float32, round to nearest
+        score[seen | (wr <= 0)] = np.float32(-1.0)
+        nxt = score.argmax(axis=1)
+        if (score[rows, nxt] < 0).any():
+            raise AssertionError("selector chose a visited city")
+        seen[rows, nxt] = True
+        tours[:, step] = nxt
+        cur = nxt
+    return tours
+
+
+def log_rule_tours(p: np.ndarray, g: float, seed: int, iteration: int, ants) -> np.ndarray:
+    """The reference's log-domain rule argmax(log P / g - E) (selection.py:
+    143-155) driven by the DEVICE uniforms, E = -log(float64(u)).  Counting
+    where it differs from `build_tours` measures the product/log agreement."""
+    n = p.shape[0]
+    logw = np.full(p.shape, -np.inf)
+    np.log(p, out=logw, where=p > 0)
+    logw /= g
+    ants = np.asarray(ants, dtype=np.int64)
+    a = ants.size
+    rows = np.arange(a)
+    cur = starts(seed, iteration, ants, n)
+    seen = np.zeros((a, n), dtype=bool)
+    seen[rows, cur] = True
+    tours = np.empty((a, n), dtype=np.int64)
+    tours[:, 0] = cur
+    cities = np.arange(n, dtype=np.uint64)
+    for step in range(1, n):
+        u = uniforms(seed, iteration, step, ants[:, None], cities[None, :]).astype(np.float64)
+        s = logw[cur] + np.log(u)
+        s[seen] = -np.inf
+        nxt = s.argmax(axis=1)
+        seen[rows, nxt] = True
+        tours[:, step] = nxt
+        cur = nxt
+    return tours
+
+
+def pairwise_sum(values) -> float:
+    """numpy's pairwise summation order for a contiguous float64 vector
+    (numpy/_core/src/umath/loops_utils.h.src: pairwise_sum)."""
+    a = [float(v) for v in values]
+
+    def rec(lo: int, n: int) -> float:
+        if n < 8:
+            res = 0.0
+            for i in range(lo, lo + n):
+                res += a[i]
+            return res
+        if n <= 128:
+            r = a[lo:lo + 8]
+            i = 8
+            while i < n - (n % 8):
+                for j in range(8):
+                    r[j] += a[lo + i + j]
+                i += 8
+            res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]))
+            while i < n:
+                res += a[lo + i]
+                i += 1
+            return res
+        n2 = n // 2
+        n2 -= n2 % 8
+        return rec(lo, n2) + rec(lo + n2, n - n2)
+
+    return rec(0, len(a))

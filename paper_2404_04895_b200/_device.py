@@ -1,0 +1,174 @@
+"""Device-side plumbing: torch owns memory and streams, libtaco does the math.
+
+Every helper here takes/returns CUDA torch tensors and launches on torch's
+current stream.  There is deliberately no CPU path: without a CUDA device or
+without libtaco.so the calls raise.
+"""
+
+from __future__ import annotations
+
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import check, ptr
+
+INT32_MAX = 2**31 - 1
+
+
+class NoCudaDevice(RuntimeError):
+    """The engine needs an sm_100a CUDA device; there is no CPU fallback."""
+
+
+def device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise NoCudaDevice("TensorACO-B200 needs a CUDA (sm_100a) device; no CPU fallback exists")
+    _lib.load()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def new_status(dev) -> torch.Tensor:
+    return torch.tensor([0, INT32_MAX, 0, 0], dtype=torch.int32, device=dev)
+
+
+def read_status(status: torch.Tensor) -> tuple[int, int]:
+    code, idx, _, _ = (int(v) for v in status.cpu().tolist())
+    return code, idx
+
+
+def upload(a: np.ndarray, dev, dtype=None) -> torch.Tensor:
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    if dtype is not None:
+        t = t.to(dtype)
+    return t.to(dev, non_blocking=False)
+
+
+def download(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+def pad_ld(n: int) -> int:
+    """Leading dimension of the dense fp32 table: rows start 128-byte aligned."""
+    return (n + 31) // 32 * 32
+
+
+# ---------------------------------------------------------------------------
+# per-instance device cache (dist, eta, eta^beta), keyed by object identity
+# ---------------------------------------------------------------------------
+class DeviceInstance:
+    def __init__(self, inst, dev):
+        self.n = int(inst.n)
+        self.dev = dev
+        self.dist = upload(np.asarray(inst.dist, dtype=np.float64), dev)
+        self.eta = upload(np.asarray(inst.eta, dtype=np.float64), dev)
+        self._eta_b: dict[float, torch.Tensor] = {}
+
+    def eta_beta(self, beta: float) -> torch.Tensor:
+        beta = float(beta)
+        t = self._eta_b.get(beta)
+        if t is None:
+            t = torch.empty_like(self.eta)
+            check(_lib.load().taco_eta_power(t.numel(), ptr(self.eta), beta, ptr(t), stream_handle()),
+                  "taco_eta_power")
+            self._eta_b[beta] = t
+        return t
+
+
+_INSTANCES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()
+
+
+def device_instance(inst) -> DeviceInstance:
+    dev = device()
+    try:
+        cached = _INSTANCES.get(inst)
+    except TypeError:  # unhashable / not weak-referenceable: no caching
+        return DeviceInstance(inst, dev)
+    if cached is None or cached.dev != dev:
+        cached = DeviceInstance(inst, dev)
+        _INSTANCES[inst] = cached
+    return cached
+
+
+# ---------------------------------------------------------------------------
+# thin typed wrappers over the C ABI
+# ---------------------------------------------------------------------------
+def row_update(n, *, tau_in=None, tau_out=None, eta_b=None, nbr=None, inc=None, k=0,
+               delta_in=None, delta_out=None, do_evap=False, keep=1.0, want_p=False,
+               alpha=1.0, inv_gamma=1.0, p_out=None, rowsum_out=None, w_out=None, ldw=0,
+               sw_out=None, si_out=None, status=None) -> None:
+    code = _lib.load().taco_row_update(
+        n, ptr(tau_in), ptr(tau_out), ptr(eta_b), ptr(nbr), ptr(inc), int(k), ptr(delta_in),
+        ptr(delta_out), int(bool(do_evap)), float(keep), int(bool(want_p)), float(alpha),
+        float(inv_gamma), ptr(p_out), ptr(rowsum_out), ptr(w_out), int(ldw), ptr(sw_out),
+        ptr(si_out), ptr(status), stream_handle())
+    check(code, "taco_row_update")
+
+
+class SelectionTables:
+    """fp32 selection table W = P^(1/gamma): dense (n x ldw) and/or sorted."""
+
+    def __init__(self, n: int, dev, dense: bool, sorted_: bool):
+        self.n = n
+        self.ldw = pad_ld(n)
+        self.w = torch.empty((n, self.ldw), dtype=torch.float32, device=dev) if dense else None
+        self.sw = torch.empty((n, n), dtype=torch.float32, device=dev) if sorted_ else None
+        self.si = torch.empty((n, n), dtype=torch.uint16, device=dev) if sorted_ else None
+
+
+def selection_table_from_p(p: torch.Tensor, inv_gamma: float, tables: SelectionTables) -> None:
+    code = _lib.load().taco_selection_table(
+        tables.n, ptr(p), float(inv_gamma), ptr(tables.w), tables.ldw, ptr(tables.sw), ptr(tables.si),
+        stream_handle())
+    check(code, "taco_selection_table")
+
+
+def construct(n: int, m_local: int, ant_offset: int, variant: int, tables: SelectionTables,
+              seed: int, iteration: int, tours_out: torch.Tensor, status: torch.Tensor,
+              scan_count: torch.Tensor | None = None) -> None:
+    code = _lib.load().taco_construct(
+        n, m_local, ant_offset, variant, ptr(tables.w), tables.ldw, ptr(tables.sw), ptr(tables.si),
+        int(seed), int(iteration) & 0xFFFFFFFF, ptr(tours_out), ptr(status), ptr(scan_count),
+        stream_handle())
+    check(code, "taco_construct")
+
+
+def tour_cost(tours: torch.Tensor, dist: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    m, n = tours.shape
+    if out is None:
+        out = torch.empty(m, dtype=torch.float64, device=tours.device)
+    is64 = 1 if tours.dtype == torch.int64 else 0
+    if not is64 and tours.dtype != torch.int32:
+        raise TypeError(f"tours must be int32 or int64, got {tours.dtype}")
+    check(_lib.load().taco_tour_cost(n, m, ptr(tours), is64, ptr(dist), ptr(out), stream_handle()),
+          "taco_tour_cost")
+    return out
+
+
+class EliteWorkspace:
+    def __init__(self, m: int, dev):
+        self.m = m
+        self.nbytes = int(_lib.load().taco_elite_workspace_bytes(m))
+        self.buf = torch.empty(max(self.nbytes, 1), dtype=torch.uint8, device=dev)
+
+
+def elite_order(costs: torch.Tensor, ws: EliteWorkspace, out: torch.Tensor | None = None) -> torch.Tensor:
+    m = costs.numel()
+    if out is None:
+        out = torch.empty(m, dtype=torch.int32, device=costs.device)
+    check(_lib.load().taco_elite_order(m, ptr(costs), ptr(out), ptr(ws.buf), ws.nbytes, stream_handle()),
+          "taco_elite_order")
+    return out
+
+
+def elite_neighbors(tours: torch.Tensor, order: torch.Tensor, costs: torch.Tensor, k: int,
+                    nbr: torch.Tensor, inc: torch.Tensor) -> None:
+    n = tours.shape[1]
+    is64 = 1 if tours.dtype == torch.int64 else 0
+    check(_lib.load().taco_elite_neighbors(n, k, ptr(tours), is64, ptr(order), ptr(costs), ptr(nbr),
+                                           ptr(inc), stream_handle()), "taco_elite_neighbors")

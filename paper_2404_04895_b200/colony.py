@@ -1,0 +1,180 @@
+"""Drop-in replacements of the reference's colony functions (colony.py) and
+tour lengths (model.py:285-295), executed on the B200 through libtaco.
+
+Signatures, return types and error behaviour follow the reference:
+``compute_probability_matrix(tau, inst, params) -> ProbabilityMatrix``
+(colony.py:51-69), ``construct_tours(p, inst, params, iteration,
+chunk_size=None, probe=None) -> TourBatch`` (colony.py:87-154),
+``init_starts`` (colony.py:72-78), ``batch_costs`` / ``tour_cost``.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _device, _lib
+from . import rng as _rng
+from .model import ProbabilityMatrix, Selection, TourBatch, check_permutations
+from .selection import gamma_at
+
+
+class NumericalUnderflow(ValueError):
+    """A transition-matrix row normalizer vanished or became non-finite
+    (colony.py:32-33)."""
+
+
+def _underflow_from_sums(sums: np.ndarray) -> NumericalUnderflow:
+    # same row choice as the reference's message (colony.py:64-68)
+    bad = int(np.argmin(np.where(np.isfinite(sums), sums, -np.inf)))
+    return NumericalUnderflow(
+        f"row {bad} normalizer is {float(sums[bad])!r}; "
+        "pheromone or heuristic values out of representable range")
+
+
+def _selection(params) -> Selection:
+    mech = Selection(getattr(params, "selection", Selection.ADAIR))
+    if mech is Selection.RW:
+        raise NotImplementedError(
+            "roulette-wheel selection is outside the accelerated IR/AdaIR path")
+    return mech
+
+
+def construction_gamma(params, iteration: int) -> float:
+    """gamma for one iteration: the cosine schedule for AdaIR, 1.0 for IR
+    (colony.py:103)."""
+    if _selection(params) is Selection.ADAIR:
+        return gamma_at(iteration, params.gamma_schedule)
+    return 1.0
+
+
+def compute_probability_matrix(tau, inst, params) -> ProbabilityMatrix:
+    """P = RowNorm(tau^alpha * eta^beta) with a zero diagonal (colony.py:51-69).
+
+    Bit-exact with the reference for alpha, beta in {0.5, 1, 2} (numpy's
+    scalar-power fast paths; beta also 0); other exponents go through pow and
+    agree to ~1 ulp.  Raises NumericalUnderflow when a row normalizer is zero
+    or non-finite.
+    """
+    n = int(inst.n)
+    di = _device.device_instance(inst)
+    dev = di.dev
+    tau_t = _device.upload(np.asarray(tau.tau, dtype=np.float64), dev)
+    p_t = torch.empty_like(tau_t)
+    sums = torch.empty(n, dtype=torch.float64, device=dev)
+    status = _device.new_status(dev)
+    _device.row_update(n, tau_in=tau_t, eta_b=di.eta_beta(params.beta), want_p=True,
+                       alpha=float(params.alpha), p_out=p_t, rowsum_out=sums, status=status)
+    code, _ = _device.read_status(status)
+    if code == _lib.TACO_UNDERFLOW:
+        raise _underflow_from_sums(_device.download(sums))
+    return ProbabilityMatrix(p=_device.download(p_t))
+
+
+def init_starts(m: int, n: int, rng_stream: np.random.Generator) -> np.ndarray:
+    """Uniform start city per ant from a host generator (colony.py:72-78);
+    kept for API compatibility — the device stream draws starts on chip."""
+    if m < 1:
+        raise ValueError(f"m must be >= 1, got {m}")
+    if n < 3:
+        raise ValueError(f"n must be >= 3, got {n}")
+    return rng_stream.integers(0, n, size=m, dtype=np.int64)
+
+
+def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = None,
+                    probe=None, *, stream: str = "device", variant: str = "sorted") -> TourBatch:
+    """Build m complete tours in n-1 lockstep selection rounds (colony.py:87-154).
+
+    stream="device" (default): keyed on-chip Philox4x32-10 uniforms and the
+    product-form rule argmax(W * u) — the fast path.
+    stream="numpy": reference-stream replay — the reference's own keyed numpy
+    deviates, start cities and log-weight table (rng.py:42-68,
+    selection.py:62-75) are produced on the host and the device runs the n-1
+    log-domain argmax rounds; tours equal the reference's bit for bit.
+    ``chunk_size`` is accepted and has no effect (chunking is bit-invisible in
+    the reference too, colony.py:119-124); ``probe`` is not supported.
+    variant: "sorted" (pruned scan of the row-sorted table) or "dense" (full
+    row streaming); both return identical tours.
+    """
+    if probe is not None:
+        raise NotImplementedError("construction probes are not supported by the device engine")
+    if chunk_size is not None and chunk_size < 1 and chunk_size < params.m:
+        raise ValueError(f"chunk_size must be >= 1, got {chunk_size}")
+    n, m = int(inst.n), int(params.m)
+    gamma = construction_gamma(params, iteration)
+    di = _device.device_instance(inst)
+    dev = di.dev
+    p_host = np.asarray(p.p, dtype=np.float64)
+    if stream == "numpy":
+        tours_t = _construct_reference_stream(p_host, n, m, params.seed, iteration, gamma, dev)
+    elif stream == "device":
+        tours_t = _construct_device_stream(p_host, n, m, params.seed, iteration, gamma, dev, variant)
+    else:
+        raise ValueError(f"stream must be 'device' or 'numpy', got {stream!r}")
+    costs_t = _device.tour_cost(tours_t, di.dist)
+    return TourBatch(tours=_device.download(tours_t).astype(np.int64, copy=False),
+                     costs=_device.download(costs_t))
+
+
+def _construct_device_stream(p_host, n, m, seed, iteration, gamma, dev, variant) -> torch.Tensor:
+    if variant == "sorted" and n > _lib.load().taco_max_sorted_n():
+        variant = "dense"
+    if variant not in ("sorted", "dense"):
+        raise ValueError(f"variant must be 'sorted' or 'dense', got {variant!r}")
+    p_t = _device.upload(p_host, dev)
+    tables = _device.SelectionTables(n, dev, dense=(variant == "dense"), sorted_=(variant == "sorted"))
+    _device.selection_table_from_p(p_t, 1.0 / gamma, tables)
+    tours = torch.zeros((m, n), dtype=torch.int32, device=dev)
+    status = _device.new_status(dev)
+    code = _lib.CONSTRUCT_SORTED if variant == "sorted" else _lib.CONSTRUCT_DENSE
+    _device.construct(n, m, 0, code, tables, seed, iteration, tours, status)
+    _raise_construct_status(status)
+    return tours
+
+
+def _raise_construct_status(status: torch.Tensor) -> None:
+    code, _ = _device.read_status(status)
+    if code == _lib.TACO_NO_CANDIDATE:
+        raise AssertionError("selector chose a visited city")
+
+
+def _construct_reference_stream(p_host, n, m, seed, iteration, gamma, dev) -> torch.Tensor:
+    # log-weight table with the reference's numpy arithmetic (selection.py:72-74)
+    logw = np.full(p_host.shape, -np.inf)
+    np.log(p_host, out=logw, where=p_host > 0)
+    np.divide(logw, gamma, out=logw)
+    logw_t = _device.upload(logw, dev)
+    starts = _rng.start_cities(seed, iteration, m, n)
+    current = _device.upload(starts, dev)
+    visited = torch.zeros((m, n), dtype=torch.uint8, device=dev)
+    visited[torch.arange(m, device=dev), current] = 1
+    tours = torch.zeros((m, n), dtype=torch.int64, device=dev)
+    tours[:, 0] = current
+    status = _device.new_status(dev)
+    lib = _lib.load()
+    for step in range(1, n):
+        e_t = _device.upload(_rng.step_exponentials(seed, iteration, step, m, n), dev)
+        _lib.check(lib.taco_select_parity(n, m, step, logw_t.data_ptr(), e_t.data_ptr(), current.data_ptr(),
+                                          visited.data_ptr(), tours.data_ptr(), status.data_ptr(),
+                                          _device.stream_handle()), "taco_select_parity")
+    _raise_construct_status(status)
+    return tours
+
+
+def batch_costs(tours, inst) -> np.ndarray:
+    """Closed-tour lengths of an (m, n) tour array in numpy's pairwise
+    summation order (model.py:292-295); bit-exact with the reference."""
+    t = np.ascontiguousarray(np.asarray(tours, dtype=np.int64))
+    if t.ndim != 2 or t.shape[1] != inst.n:
+        raise ValueError(f"tours must have shape (m, {inst.n}), got {t.shape}")
+    if t.size and (t.min() < 0 or t.max() >= inst.n):
+        raise IndexError("tour entries out of range")
+    di = _device.device_instance(inst)
+    return _device.download(_device.tour_cost(_device.upload(t, di.dev), di.dist))
+
+
+def tour_cost(tour, inst) -> float:
+    """Length of one closed tour (model.py:285-289)."""
+    t = np.asarray(tour, dtype=np.int64)
+    check_permutations(t, inst.n)
+    return float(batch_costs(t[None, :], inst)[0])

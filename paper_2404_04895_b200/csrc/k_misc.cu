@@ -1,0 +1,219 @@
+// Tour lengths, elite ordering, elite edge map, best-so-far tracking and the
+// log-weight table.
+//
+// Reference: model.batch_costs model.py:292-295, pheromone.select_elite
+// pheromone.py:17-25, edge_index_matrix pheromone.py:28-38 (edge map feeding
+// the fused deposit in k_row_update.cu), selection.scaled_log_weights
+// selection.py:62-75.
+#include <cub/device/device_radix_sort.cuh>
+
+#include "taco_common.cuh"
+
+namespace taco {
+
+// one warp per ant: lanes sum the pairwise-tree leaves of the gathered edge
+// lengths, lane 0 folds them (numpy's (m, n).sum(axis=1) order)
+template <int WARPS, typename TourT>
+__global__ void __launch_bounds__(WARPS * 32)
+    k_tour_cost(int n, int m, const TourT *__restrict__ tours, const double *__restrict__ dist,
+                double *__restrict__ costs, int n_leaves) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  int2 *leaves = reinterpret_cast<int2 *>(smem);
+  double *leaf_sum = reinterpret_cast<double *>(smem + 8 * (size_t)n_leaves);
+  if (threadIdx.x == 0) pw_leaves(n, leaves);
+  __syncthreads();
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int a = blockIdx.x * WARPS + warp;
+  if (a >= m) return;
+  const TourT *t = tours + (size_t)a * n;
+  double *ls = leaf_sum + (size_t)warp * n_leaves;
+  for (int L = lane; L < n_leaves; L += 32) {
+    const int2 lf = leaves[L];
+    ls[L] = pw_leaf_sum(lf.y, [&](int q) {
+      const int s = lf.x + q;
+      const int s1 = (s + 1 == n) ? 0 : s + 1;
+      return __ldg(dist + (size_t)t[s] * n + (size_t)t[s1]);
+    });
+  }
+  __syncwarp();
+  if (lane == 0) costs[a] = pw_fold(n, ls);
+}
+
+__global__ void k_cost_keys(int m, const double *costs, unsigned long long *keys, int32_t *vals) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a < m) {
+    // non-negative finite doubles order like their bit patterns
+    keys[a] = (unsigned long long)__double_as_longlong(costs[a]);
+    vals[a] = a;
+  }
+}
+
+template <typename TourT>
+__global__ void k_elite_neighbors(int n, int k, const TourT *__restrict__ tours, const int32_t *order,
+                                  const double *costs, int2 *nbr, double *inc) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)k * n) return;
+  const int r = (int)(idx / n);
+  const int s = (int)(idx % n);
+  const int a = order[r];
+  const TourT *t = tours + (size_t)a * n;
+  const int city = (int)t[s];
+  const int prev = (int)t[s == 0 ? n - 1 : s - 1];
+  const int next = (int)t[s + 1 == n ? 0 : s + 1];
+  nbr[(size_t)r * n + city] = make_int2(prev, next);
+  if (s == 0) inc[r] = __ddiv_rn(1.0, costs[a]);  // pheromone.py:66 inc = 1.0 / cost
+}
+
+__global__ void k_track_best(int n, const int32_t *tours, const double *costs, const int32_t *order,
+                             double *best_cost, int32_t *best_tour, int32_t *best_iter, uint32_t iteration) {
+  __shared__ int s_take;
+  __shared__ int s_ant;
+  if (threadIdx.x == 0) {
+    const int a = order[0];
+    const double c = costs[a];
+    s_ant = a;
+    s_take = (c < *best_cost);
+  }
+  __syncthreads();
+  if (!s_take) return;
+  const int32_t *t = tours + (size_t)s_ant * n;
+  for (int s = threadIdx.x; s < n; s += blockDim.x) best_tour[s] = t[s];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *best_cost = costs[s_ant];
+    *best_iter = (int32_t)iteration;
+  }
+}
+
+__global__ void k_log_weights(int64_t count, const double *p, double gamma, double *out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = p[t];
+    out[t] = (v > 0.0) ? __ddiv_rn(log(v), gamma) : -INFINITY;
+  }
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static size_t cub_temp_bytes(int m) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const unsigned long long *)nullptr,
+                                  (unsigned long long *)nullptr, (const int32_t *)nullptr, (int32_t *)nullptr, m);
+  return bytes;
+}
+
+}  // namespace taco
+
+using namespace taco;
+
+extern "C" int taco_tour_cost(int n, int m, const void *tours, int tours_is_i64, const double *dist,
+                              double *costs_out, void *stream) {
+  if (n < 1 || m < 0 || tours == nullptr || dist == nullptr || costs_out == nullptr) return TACO_ERR_ARG;
+  if (m == 0) return TACO_OK;
+  constexpr int WARPS = 8;
+  const int n_leaves = pw_num_leaves(n);
+  const size_t smem = 8 * (size_t)n_leaves + 8 * (size_t)WARPS * n_leaves;
+  if (smem > 200 * 1024) return TACO_ERR_UNSUPPORTED;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const int grid = (m + WARPS - 1) / WARPS;
+  if (tours_is_i64) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_tour_cost<WARPS, int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_tour_cost<WARPS, int64_t><<<grid, WARPS * 32, smem, s>>>(n, m, (const int64_t *)tours, dist, costs_out,
+                                                               n_leaves);
+  } else {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(k_tour_cost<WARPS, int32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_tour_cost<WARPS, int32_t><<<grid, WARPS * 32, smem, s>>>(n, m, (const int32_t *)tours, dist, costs_out,
+                                                               n_leaves);
+  }
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+extern "C" size_t taco_elite_workspace_bytes(int m) {
+  if (m < 1) return 0;
+  return align256((size_t)m * 8) * 2 + align256((size_t)m * 4) + align256(cub_temp_bytes(m));
+}
+
+extern "C" int taco_elite_order(int m, const double *costs, int32_t *order_out, void *workspace, size_t ws_bytes,
+                                void *stream) {
+  if (m < 1 || costs == nullptr || order_out == nullptr) return TACO_ERR_ARG;
+  if (ws_bytes < taco_elite_workspace_bytes(m) || workspace == nullptr) return TACO_ERR_ARG;
+  unsigned char *ws = reinterpret_cast<unsigned char *>(workspace);
+  auto *keys_in = reinterpret_cast<unsigned long long *>(ws);
+  ws += align256((size_t)m * 8);
+  auto *keys_out = reinterpret_cast<unsigned long long *>(ws);
+  ws += align256((size_t)m * 8);
+  auto *vals_in = reinterpret_cast<int32_t *>(ws);
+  ws += align256((size_t)m * 4);
+  size_t temp = cub_temp_bytes(m);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  k_cost_keys<<<(m + 255) / 256, 256, 0, s>>>(m, costs, keys_in, vals_in);
+  TACO_CUDA_CHECK_LAUNCH();
+  // LSD radix sort is stable: equal costs keep ascending ant order, exactly
+  // np.argsort(costs, kind="stable")
+  if (cub::DeviceRadixSort::SortPairs(ws, temp, keys_in, keys_out, vals_in, order_out, m, 0, 64, s) !=
+      cudaSuccess)
+    return TACO_ERR_CUDA;
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+extern "C" int taco_elite_neighbors(int n, int k, const void *tours, int tours_is_i64, const int32_t *order,
+                                    const double *costs, int32_t *nbr_out, double *inc_out, void *stream) {
+  if (n < 3 || k < 1 || tours == nullptr || order == nullptr || costs == nullptr) return TACO_ERR_ARG;
+  const size_t total = (size_t)k * n;
+  const int grid = (int)((total + 255) / 256);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  if (tours_is_i64)
+    k_elite_neighbors<int64_t><<<grid, 256, 0, s>>>(n, k, (const int64_t *)tours, order, costs,
+                                                    reinterpret_cast<int2 *>(nbr_out), inc_out);
+  else
+    k_elite_neighbors<int32_t><<<grid, 256, 0, s>>>(n, k, (const int32_t *)tours, order, costs,
+                                                    reinterpret_cast<int2 *>(nbr_out), inc_out);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+extern "C" int taco_track_best(int n, const int32_t *tours, const double *costs, const int32_t *order,
+                               double *best_cost, int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
+                               void *stream) {
+  if (n < 1) return TACO_ERR_ARG;
+  k_track_best<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(n, tours, costs, order, best_cost,
+                                                                      best_tour, best_iter, iteration);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+extern "C" int taco_log_weights(int64_t count, const double *p, double gamma, double *logw_out, void *stream) {
+  if (count < 0 || !(gamma > 0.0)) return TACO_ERR_ARG;
+  if (count == 0) return TACO_OK;
+  const int64_t blocks64 = (count + 255) / 256;
+  const int grid = (int)(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
+  k_log_weights<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(count, p, gamma, logw_out);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+extern "C" int taco_abi_version(void) { return TACO_ABI_VERSION; }
+
+extern "C" const char *taco_status_string(int code) {
+  switch (code) {
+    case TACO_OK:
+      return "ok";
+    case TACO_UNDERFLOW:
+      return "transition-matrix row normalizer is zero or non-finite";
+    case TACO_NO_CANDIDATE:
+      return "selector chose a visited city";
+    case TACO_ERR_ARG:
+      return "invalid argument";
+    case TACO_ERR_CUDA:
+      return "CUDA error";
+    case TACO_ERR_UNSUPPORTED:
+      return "size outside the compiled kernel variants";
+    default:
+      return "unknown status";
+  }
+}

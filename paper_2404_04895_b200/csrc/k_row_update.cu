@@ -1,0 +1,341 @@
+// Fused pheromone update + transition matrix + selection table, one CTA per row.
+//
+// Replaces, for row i of every n x n matrix (reference file:line):
+//   accumulate_increments  pheromone.py:52-68  delta[i, :] in elite rank order
+//   apply_update           pheromone.py:71-83  tau' = max((1-rho) tau + delta, 1e-12)
+//   compute_probability_matrix colony.py:51-69 P = unnorm / pairwise_rowsum(unnorm)
+//   scaled_log_weights     selection.py:62-75  folded into W = fp32(P^(1/gamma))
+//
+// HBM traffic per row (Solver mode): read tau 8n + eta^beta 8n, write tau 8n,
+// write W (dense 4n and/or sorted 6n), nbr 8k gathers.  The row lives in shared
+// memory between the phases so tau / unnorm are touched once.
+#include <cub/block/block_radix_sort.cuh>
+
+#include "taco_common.cuh"
+
+namespace taco {
+
+struct RowParams {
+  int n;
+  const double *tau_in;
+  double *tau_out;
+  const double *eta_b;
+  const int2 *nbr;
+  const double *inc;
+  int k;
+  const double *delta_in;
+  double *delta_out;
+  int do_evap;
+  double keep;
+  int want_p;
+  int p_given;  // tau_in holds P itself: no normalization (selection-table mode)
+  double alpha;
+  int gamma_one;
+  double inv_gamma;
+  double *p_out;
+  double *rowsum_out;
+  float *w_out;
+  int ldw;
+  float *sw_out;
+  uint16_t *si_out;
+  int32_t *status;
+  int n_leaves;
+};
+
+constexpr int kDepositChunk = 512;  // elites staged in shared memory per pass
+
+// np.power(x, e) for a scalar float exponent: numpy dispatches e in
+// {-1, 0, 0.5, 1, 2} to reciprocal / ones / sqrt / copy / square (bit-exact
+// here); any other exponent uses pow (<= 1 ulp from numpy's SIMD pow).
+__device__ __forceinline__ double numpy_scalar_power(double x, double e) {
+  if (e == 1.0) return x;
+  if (e == 2.0) return __dmul_rn(x, x);
+  if (e == 0.0) return 1.0;
+  if (e == 0.5) return __dsqrt_rn(x);
+  if (e == -1.0) return __ddiv_rn(1.0, x);
+  return pow(x, e);
+}
+
+__device__ __forceinline__ float selection_weight(double p, const RowParams &a) {
+  // W = P^(1/gamma) rounded once to fp32; gamma == 1 is the exact conversion
+  return a.gamma_one ? __double2float_rn(p) : __double2float_rn(pow(p, a.inv_gamma));
+}
+
+// Dynamic shared memory layout (bytes):
+//   [0, row_bytes)                      double row[n]   (also CUB sort storage)
+//   [row_bytes, + 16*n_leaves)          int2 leaves[], double leaf_sum[]
+//   [.., + 16*kDepositChunk)            int2 nb stage[], double inc stage[]
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, size_t row_bytes) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  double *row = reinterpret_cast<double *>(smem);
+  int2 *leaves = reinterpret_cast<int2 *>(smem + row_bytes);
+  double *leaf_sum = reinterpret_cast<double *>(smem + row_bytes + 8 * (size_t)a.n_leaves);
+  int2 *nb_stage = reinterpret_cast<int2 *>(smem + row_bytes + 16 * (size_t)a.n_leaves);
+  double *inc_stage = reinterpret_cast<double *>(nb_stage + kDepositChunk);
+  __shared__ double s_sum;
+  __shared__ double s_stage[32];
+
+  const int n = a.n;
+  const int i = blockIdx.x;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const size_t rowoff = (size_t)i * n;
+
+  if (a.want_p && tid == 0) pw_leaves(n, leaves);
+
+  // ---- delta row -----------------------------------------------------------
+  const bool have_delta = (a.nbr != nullptr) || (a.delta_in != nullptr);
+  if (a.nbr != nullptr) {
+    for (int j = tid; j < n; j += BLOCK) row[j] = 0.0;
+    for (int rbase = 0; rbase < a.k; rbase += kDepositChunk) {
+      const int rcount = min(kDepositChunk, a.k - rbase);
+      __syncthreads();
+      for (int r = tid; r < rcount; r += BLOCK) {
+        nb_stage[r] = a.nbr[(size_t)(rbase + r) * n + i];
+        inc_stage[r] = a.inc[rbase + r];
+      }
+      __syncthreads();
+      if (tid < 32) {
+        // entries e = 2r + side in rank order; one cell is hit at most once per
+        // elite (prev != next for n >= 3), so within a 32-entry window the
+        // lanes sharing a column are in rank order and their leader folds them
+        // sequentially: ((delta + inc_a) + inc_b) + ... exactly like the
+        // reference's per-elite fancy += (pheromone.py:62-67).
+        const int total = 2 * rcount;
+        for (int base = 0; base < total; base += 32) {
+          const int e = base + lane;
+          int col = -1;
+          double v = 0.0;
+          if (e < total) {
+            const int2 nb = nb_stage[e >> 1];
+            col = (e & 1) ? nb.y : nb.x;
+            v = inc_stage[e >> 1];
+          }
+          const unsigned peers = __match_any_sync(0xffffffffu, col);
+          s_stage[lane] = v;
+          __syncwarp();
+          if (col >= 0 && lane == __ffs(peers) - 1) {
+            double acc = row[col];
+            unsigned p = peers;
+            while (p) {
+              const int l = __ffs(p) - 1;
+              p &= p - 1;
+              acc = __dadd_rn(acc, s_stage[l]);
+            }
+            row[col] = acc;
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (a.delta_in != nullptr) {
+    for (int j = tid; j < n; j += BLOCK) row[j] = a.delta_in[rowoff + j];
+  }
+  __syncthreads();
+  if (a.delta_out != nullptr) {
+    for (int j = tid; j < n; j += BLOCK) a.delta_out[rowoff + j] = have_delta ? row[j] : 0.0;
+  }
+  if (a.tau_in == nullptr) return;  // delta-only mode (accumulate_increments)
+
+  // ---- tau' and unnormalized weights -------------------------------------
+  for (int j = tid; j < n; j += BLOCK) {
+    double t = a.tau_in[rowoff + j];
+    if (a.do_evap) {
+      const double d = have_delta ? row[j] : 0.0;
+      t = __dadd_rn(__dmul_rn(a.keep, t), d);
+      t = (t < 1e-12) ? 1e-12 : t;  // np.maximum(new_tau, TAU_MIN), NaN kept
+    }
+    if (a.tau_out != nullptr) a.tau_out[rowoff + j] = t;
+    if (a.p_given) {
+      row[j] = t;
+    } else if (a.want_p) {
+      double u = __dmul_rn(numpy_scalar_power(t, a.alpha), a.eta_b[rowoff + j]);
+      if (j == i) u = 0.0;  // np.fill_diagonal(unnorm, 0.0)
+      row[j] = u;
+    }
+  }
+  if (!a.want_p) return;
+  __syncthreads();
+
+  // ---- pairwise row sum (numpy order) --------------------------------------
+  if (a.p_given) {
+    if (tid == 0) s_sum = 1.0;  // P / 1.0 == P exactly
+  } else {  // a.p_given is uniform over the CTA, so the barrier below is safe
+    for (int L = tid; L < a.n_leaves; L += BLOCK) {
+      const int2 lf = leaves[L];
+      const double *base = row + lf.x;
+      leaf_sum[L] = pw_leaf_sum(lf.y, [&](int q) { return base[q]; });
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double s = pw_fold(n, leaf_sum);
+      s_sum = s;
+      if (a.rowsum_out != nullptr) a.rowsum_out[i] = s;
+      if (!(isfinite(s) && s > 0.0)) record_status(a.status, TACO_UNDERFLOW, i);
+    }
+  }
+  __syncthreads();
+  const double s = s_sum;
+
+  // ---- dense outputs (coalesced, striped) ------------------------------------
+  if (a.p_out != nullptr || a.w_out != nullptr) {
+    for (int j = tid; j < n; j += BLOCK) {
+      const double p = __ddiv_rn(row[j], s);
+      if (a.p_out != nullptr) a.p_out[rowoff + j] = p;
+      if (a.w_out != nullptr) a.w_out[(size_t)i * a.ldw + j] = selection_weight(p, a);
+    }
+    if (a.w_out != nullptr)
+      for (int j = n + tid; j < a.ldw; j += BLOCK) a.w_out[(size_t)i * a.ldw + j] = 0.0f;
+  }
+
+  // ---- row-sorted selection table ------------------------------------------
+  if constexpr (ITEMS > 0) {
+    if (a.sw_out != nullptr) {
+      using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint16_t>;
+      uint32_t keys[ITEMS];
+      uint16_t vals[ITEMS];
+#pragma unroll
+      for (int q = 0; q < ITEMS; ++q) {
+        const int j = tid * ITEMS + q;
+        if (j < n) {
+          const float w = selection_weight(__ddiv_rn(row[j], s), a);
+          keys[q] = __float_as_uint(w);
+          vals[q] = (uint16_t)j;
+        } else {
+          keys[q] = 0u;  // pads sort after every real entry (stable)
+          vals[q] = 0xffffu;
+        }
+      }
+      __syncthreads();  // row[] is dead: its storage becomes the sort workspace
+      auto &ts = *reinterpret_cast<typename Sort::TempStorage *>(smem);
+      Sort(ts).SortDescendingBlockedToStriped(keys, vals, 0, 31);
+#pragma unroll
+      for (int q = 0; q < ITEMS; ++q) {
+        const int pos = tid + q * BLOCK;
+        if (pos < n) {
+          a.sw_out[rowoff + pos] = __uint_as_float(keys[q]);
+          a.si_out[rowoff + pos] = vals[q];
+        }
+      }
+    }
+  }
+}
+
+template <int BLOCK, int ITEMS>
+static int launch_row(const RowParams &a, cudaStream_t stream) {
+  size_t row_bytes = (size_t)a.n * sizeof(double);
+  if constexpr (ITEMS > 0) {
+    using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint16_t>;
+    if (sizeof(typename Sort::TempStorage) > row_bytes) row_bytes = sizeof(typename Sort::TempStorage);
+  }
+  row_bytes = (row_bytes + 15) & ~(size_t)15;
+  const size_t smem = row_bytes + 16 * (size_t)a.n_leaves + 16 * (size_t)kDepositChunk;
+  if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
+  static size_t configured = 0;  // per template instance
+  if (smem > 48 * 1024 && smem > configured) {
+    if (cudaFuncSetAttribute(k_row_update<BLOCK, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return TACO_ERR_CUDA;
+    configured = smem;
+  }
+  k_row_update<BLOCK, ITEMS><<<a.n, BLOCK, smem, stream>>>(a, row_bytes);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+}  // namespace taco
+
+using namespace taco;
+
+extern "C" int taco_max_sorted_n(void) { return 20480; }
+
+static int launch_variant(RowParams &a, bool sorted, cudaStream_t s) {
+  if (!sorted) return launch_row<256, 0>(a, s);
+  const int n = a.n;
+  if (n <= 1024) return launch_row<128, 8>(a, s);
+  if (n <= 2560) return launch_row<256, 10>(a, s);
+  if (n <= 5120) return launch_row<512, 10>(a, s);
+  if (n <= 10240) return launch_row<512, 20>(a, s);
+  if (n <= 20480) return launch_row<1024, 20>(a, s);
+  return TACO_ERR_UNSUPPORTED;
+}
+
+extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, const double *eta_b,
+                               const int32_t *nbr, const double *inc, int k, const double *delta_in,
+                               double *delta_out, int do_evap, double keep, int want_p, double alpha,
+                               double inv_gamma, double *p_out, double *rowsum_out, float *w_out,
+                               int ldw, float *sw_out, uint16_t *si_out, int32_t *status,
+                               void *stream) {
+  if (n < 3 || n > 65535) return TACO_ERR_ARG;
+  if (tau_in == nullptr && (do_evap || want_p || tau_out != nullptr)) return TACO_ERR_ARG;
+  if (nbr != nullptr && (inc == nullptr || k < 1)) return TACO_ERR_ARG;
+  if (nbr != nullptr && delta_in != nullptr) return TACO_ERR_ARG;
+  if (want_p && eta_b == nullptr) return TACO_ERR_ARG;
+  if (w_out != nullptr && ldw < n) return TACO_ERR_ARG;
+  if ((sw_out == nullptr) != (si_out == nullptr)) return TACO_ERR_ARG;
+  if ((sw_out != nullptr || w_out != nullptr || p_out != nullptr) && !want_p) return TACO_ERR_ARG;
+  RowParams a;
+  a.n = n;
+  a.tau_in = tau_in;
+  a.tau_out = tau_out;
+  a.eta_b = eta_b;
+  a.nbr = reinterpret_cast<const int2 *>(nbr);
+  a.inc = inc;
+  a.k = k;
+  a.delta_in = delta_in;
+  a.delta_out = delta_out;
+  a.do_evap = do_evap;
+  a.keep = keep;
+  a.want_p = want_p;
+  a.p_given = 0;
+  a.alpha = alpha;
+  a.gamma_one = (inv_gamma == 1.0);
+  a.inv_gamma = inv_gamma;
+  a.p_out = p_out;
+  a.rowsum_out = rowsum_out;
+  a.w_out = w_out;
+  a.ldw = ldw;
+  a.sw_out = sw_out;
+  a.si_out = si_out;
+  a.status = status;
+  a.n_leaves = want_p ? pw_num_leaves(n) : 0;
+  return launch_variant(a, sw_out != nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int taco_selection_table(int n, const double *p, double inv_gamma, float *w_out, int ldw,
+                                    float *sw_out, uint16_t *si_out, void *stream) {
+  if (n < 3 || n > 65535 || p == nullptr) return TACO_ERR_ARG;
+  if (w_out != nullptr && ldw < n) return TACO_ERR_ARG;
+  if ((sw_out == nullptr) != (si_out == nullptr)) return TACO_ERR_ARG;
+  RowParams a = {};
+  a.n = n;
+  a.tau_in = p;
+  a.want_p = 1;
+  a.p_given = 1;
+  a.alpha = 1.0;
+  a.gamma_one = (inv_gamma == 1.0);
+  a.inv_gamma = inv_gamma;
+  a.w_out = w_out;
+  a.ldw = ldw;
+  a.sw_out = sw_out;
+  a.si_out = si_out;
+  a.n_leaves = pw_num_leaves(n);
+  return launch_variant(a, sw_out != nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+__global__ void k_eta_power(int64_t count, const double *eta, double beta, double *out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < count;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = numpy_scalar_power(eta[t], beta);
+}
+
+extern "C" int taco_eta_power(int64_t count, const double *eta, double beta, double *out, void *stream) {
+  if (count < 0 || eta == nullptr || out == nullptr) return TACO_ERR_ARG;
+  if (count == 0) return TACO_OK;
+  const int64_t blocks64 = (count + 255) / 256;
+  const int grid = (int)(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
+  k_eta_power<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(count, eta, beta, out);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}

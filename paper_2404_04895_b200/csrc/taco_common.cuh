@@ -1,0 +1,206 @@
+// Shared device helpers for libtaco: Philox4x32-10, the keyed uniform stream,
+// numpy-order pairwise summation, status recording.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/taco.h"
+
+namespace taco {
+
+// ---------------------------------------------------------------------------
+// Philox4x32-10 (Salmon et al., Random123).  Known-answer vectors are pinned
+// in tests/test_oracle_golden.py and tests/test_gpu_parity.py.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
+constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
+constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
+constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+
+struct U4 {
+  uint32_t x, y, z, w;
+};
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = kPhiloxM0 * c.x;
+    const uint32_t hi0 = __umulhi(kPhiloxM0, c.x);
+    const uint32_t lo1 = kPhiloxM1 * c.z;
+    const uint32_t hi1 = __umulhi(kPhiloxM1, c.z);
+    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
+    k0 += kPhiloxW0;
+    k1 += kPhiloxW1;
+  }
+  return c;
+}
+
+// The device construction stream:
+//   key     = (seed & 0xffffffff, seed >> 32)
+//   counter = (city >> 2, step, ant, iteration)      selection, step >= 1
+//   counter = (0, 0, ant, iteration), word 0         start city (step 0)
+//   u       = ((x >> 9) + 0.5) * 2^-23  in (0, 1), exact in fp32
+__device__ __forceinline__ float bits_to_uniform(uint32_t x) {
+  return __fmaf_rn(__uint2float_rn(x >> 9), 0x1p-23f, 0x1p-24f);
+}
+
+__device__ __forceinline__ uint32_t lemire_bound(uint32_t x, uint32_t n) {
+  return (uint32_t)(((uint64_t)x * (uint64_t)n) >> 32);
+}
+
+__device__ __forceinline__ uint32_t word_of(const U4 &v, uint32_t i) {
+  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
+}
+
+__device__ __forceinline__ uint32_t start_city(uint32_t n, uint32_t ant, uint32_t iteration,
+                                               uint32_t k0, uint32_t k1) {
+  U4 r = philox4x32_10(U4{0u, 0u, ant, iteration}, k0, k1);
+  return lemire_bound(r.x, n);
+}
+
+// ---------------------------------------------------------------------------
+// status word: [0] = first failure code, [1] = smallest offending index
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void record_status(int32_t *status, int code, int index) {
+  if (status == nullptr) return;
+  atomicCAS(status, 0, code);
+  atomicMin(status + 1, index);
+}
+
+// ---------------------------------------------------------------------------
+// numpy pairwise summation (numpy/_core/src/umath/loops_utils.h.src,
+// pairwise_sum): blocks < 8 sum sequentially from 0.0, blocks <= 128 use eight
+// strided accumulators, larger blocks split at n/2 rounded down to a multiple
+// of 8.  The split tree depends only on n, so it is enumerated once per CTA
+// into a leaf table; lanes/threads sum leaves in parallel and one thread folds
+// the leaves in tree order.  Bit-exact with ndarray.sum(axis=-1) on
+// contiguous float64 rows (verified in tests/test_oracle_golden.py against
+// numpy, and on device in tests/test_gpu_parity.py).
+// ---------------------------------------------------------------------------
+constexpr int kPwBlock = 128;
+
+__host__ __device__ __forceinline__ int pw_split(int len) {
+  int n2 = len / 2;
+  return n2 - (n2 % 8);
+}
+
+// number of leaves of the pairwise tree for length n
+__host__ __device__ inline int pw_num_leaves(int n) {
+  // leaves are the maximal blocks of length <= 128 (or the whole array if < 8)
+  if (n <= kPwBlock) return 1;
+  // iterative count with an explicit stack
+  int stack[40];
+  int sp = 0, count = 0;
+  stack[sp++] = n;
+  while (sp) {
+    int len = stack[--sp];
+    if (len <= kPwBlock) {
+      ++count;
+    } else {
+      int n2 = pw_split(len);
+      stack[sp++] = len - n2;
+      stack[sp++] = n2;
+    }
+  }
+  return count;
+}
+
+// fill leaf (offset, length) pairs in left-to-right order; returns count
+__device__ inline int pw_leaves(int n, int2 *leaves) {
+  int stack_off[40], stack_len[40];
+  int sp = 0, count = 0;
+  stack_off[sp] = 0;
+  stack_len[sp] = n;
+  ++sp;
+  while (sp) {
+    --sp;
+    int off = stack_off[sp], len = stack_len[sp];
+    if (len <= kPwBlock) {
+      leaves[count++] = make_int2(off, len);
+    } else {
+      int n2 = pw_split(len);
+      // push right first so the left half is processed first
+      stack_off[sp] = off + n2;
+      stack_len[sp] = len - n2;
+      ++sp;
+      stack_off[sp] = off;
+      stack_len[sp] = n2;
+      ++sp;
+    }
+  }
+  return count;
+}
+
+// Sum one leaf exactly as numpy's pairwise_sum base cases do.
+// `at(i)` returns element i of the leaf.
+template <typename F>
+__device__ __forceinline__ double pw_leaf_sum(int len, F at) {
+  if (len < 8) {
+    double res = 0.0;
+    for (int i = 0; i < len; ++i) res = __dadd_rn(res, at(i));
+    return res;
+  }
+  double r0 = at(0), r1 = at(1), r2 = at(2), r3 = at(3);
+  double r4 = at(4), r5 = at(5), r6 = at(6), r7 = at(7);
+  int i = 8;
+  const int stop = len - (len % 8);
+  for (; i < stop; i += 8) {
+    r0 = __dadd_rn(r0, at(i + 0));
+    r1 = __dadd_rn(r1, at(i + 1));
+    r2 = __dadd_rn(r2, at(i + 2));
+    r3 = __dadd_rn(r3, at(i + 3));
+    r4 = __dadd_rn(r4, at(i + 4));
+    r5 = __dadd_rn(r5, at(i + 5));
+    r6 = __dadd_rn(r6, at(i + 6));
+    r7 = __dadd_rn(r7, at(i + 7));
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < len; ++i) res = __dadd_rn(res, at(i));
+  return res;
+}
+
+// Fold leaf sums (left-to-right order) along the pairwise tree of length n.
+__device__ inline double pw_fold(int n, const double *leaf_sum) {
+  if (n <= kPwBlock) return leaf_sum[0];
+  int lens[40];
+  int phase[40];
+  double lefts[40];
+  int sp = 0, li = 0;
+  lens[0] = n;
+  phase[0] = 0;
+  double ret = 0.0;
+  for (;;) {
+    int len = lens[sp];
+    if (len <= kPwBlock) {
+      ret = leaf_sum[li++];
+      for (;;) {
+        if (sp == 0) return ret;
+        --sp;
+        if (phase[sp] == 1) {
+          lefts[sp] = ret;
+          phase[sp] = 2;
+          lens[sp + 1] = lens[sp] - pw_split(lens[sp]);
+          phase[sp + 1] = 0;
+          ++sp;
+          break;
+        }
+        ret = __dadd_rn(lefts[sp], ret);
+      }
+    } else {
+      phase[sp] = 1;
+      lens[sp + 1] = pw_split(len);
+      phase[sp + 1] = 0;
+      ++sp;
+    }
+  }
+}
+
+}  // namespace taco
+
+#define TACO_CUDA_CHECK_LAUNCH()                              \
+  do {                                                        \
+    cudaError_t e_ = cudaGetLastError();                      \
+    if (e_ != cudaSuccess) return TACO_ERR_CUDA;              \
+  } while (0)

@@ -1,0 +1,89 @@
+"""Ant sharding across the GPUs of one box (one process per GPU).
+
+Ants are independent within an iteration (colony.py:126-152; chunking is
+bit-invisible, tests/test_colony.py:120-129 of the reference), and the device
+stream is keyed by the GLOBAL ant index, so a rank that builds ants
+[offset, offset + count) produces exactly the rows a single GPU would.  One
+exchange per iteration: the tours and lengths are all-gathered, then every
+rank runs the identical elite sort, deposit and P rebuild on replicated
+state — no n x n all-reduce.  The helpers work on any torch.distributed
+backend (NCCL on the B200 box, gloo for the CPU tests).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+import torch.distributed as dist
+
+
+@dataclass(frozen=True)
+class AntShard:
+    """Contiguous slice of the colony owned by one rank."""
+
+    rank: int
+    world: int
+    m: int
+    offset: int
+    count: int
+    per_rank: int  # padded slice length used by the all-gather
+
+
+def shard_ants(m: int, rank: int, world: int) -> AntShard:
+    """Split m ants into `world` contiguous slices; the first m % world ranks
+    take one extra ant."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    if m < world:
+        raise ValueError(f"need at least one ant per rank (m={m}, world={world})")
+    base, extra = divmod(m, world)
+    offset = rank * base + min(rank, extra)
+    count = base + (1 if rank < extra else 0)
+    return AntShard(rank, world, m, offset, count, base + (1 if extra else 0))
+
+
+def gather_index(m: int, world: int) -> torch.Tensor | None:
+    """Rows of the padded gather buffer that hold real ants, in global order
+    (None when m divides evenly and the buffer is already compact)."""
+    if m % world == 0:
+        return None
+    rows = []
+    for r in range(world):
+        s = shard_ants(m, r, world)
+        rows.extend(range(r * s.per_rank, r * s.per_rank + s.count))
+    return torch.tensor(rows, dtype=torch.long)
+
+
+def _all_gather_into(out: torch.Tensor, inp: torch.Tensor, group) -> None:
+    try:
+        dist.all_gather_into_tensor(out, inp, group=group)
+    except (RuntimeError, NotImplementedError, AttributeError):
+        # backends without the fused form (older gloo): list all-gather
+        parts = list(out.chunk(dist.get_world_size(group)))
+        dist.all_gather(parts, inp, group=group)
+
+
+def gather_colony(local_tours: torch.Tensor, local_costs: torch.Tensor, shard: AntShard,
+                  tours_all: torch.Tensor, costs_all: torch.Tensor, group=None,
+                  pad_tours: torch.Tensor | None = None,
+                  pad_costs: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """All-gather every rank's tours (per_rank x n) and lengths into the
+    global (m x n) / (m,) buffers, in global ant order.
+
+    ``local_tours``/``local_costs`` must be per_rank rows long (rows past
+    ``shard.count`` are padding).  When m % world != 0 the gather lands in
+    ``pad_tours``/``pad_costs`` (world * per_rank rows) and is compacted.
+    """
+    if shard.m % shard.world == 0:
+        _all_gather_into(tours_all, local_tours, group)
+        _all_gather_into(costs_all, local_costs, group)
+        return tours_all, costs_all
+    if pad_tours is None or pad_costs is None:
+        raise ValueError("uneven shards need padded gather buffers")
+    _all_gather_into(pad_tours, local_tours, group)
+    _all_gather_into(pad_costs, local_costs, group)
+    idx = gather_index(shard.m, shard.world).to(pad_tours.device)
+    torch.index_select(pad_tours, 0, idx, out=tours_all)
+    torch.index_select(pad_costs, 0, idx, out=costs_all)
+    return tours_all, costs_all

@@ -1,0 +1,227 @@
+"""Device-resident TensorACO solver: ``Solver(instance, params).step()`` /
+``.run()``.
+
+The reference has no solver object; its iteration is the loop body of
+``run_experiment`` (bench.py:199-206):
+    construct_tours -> select_elite -> accumulate_increments -> apply_update
+    -> compute_probability_matrix
+The Solver runs exactly that sequence per ``step()`` with all state resident in
+HBM and five kernel launches per iteration:
+
+    1. taco_construct        tours (m x n int32) from the fp32 selection table
+    2. taco_tour_cost        tour lengths, numpy pairwise order
+       [multi-GPU: all-gather of tours + lengths over NCCL]
+    3. taco_elite_order      stable radix argsort of the lengths
+    4. taco_track_best       best-so-far tour / length on device
+       taco_elite_neighbors  (prev, next) of every city in the k elite tours
+    5. taco_row_update       deposit + evaporation + P + W(gamma of it+1)
+
+The host synchronizes only when a result is read (``step()`` returns the best
+tour and length; ``run()`` reads once at the end).
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+import torch.distributed as tdist
+
+from . import _device, _lib
+from .colony import NumericalUnderflow, construction_gamma
+from .distributed import AntShard, gather_colony, shard_ants
+from .model import AcoParams, PheromoneState, ProbabilityMatrix, TourBatch, instance_from_distances
+
+
+def _as_instance(instance):
+    if hasattr(instance, "dist") and hasattr(instance, "eta") and hasattr(instance, "n"):
+        return instance
+    return instance_from_distances(np.asarray(instance, dtype=np.float64))
+
+
+def _as_params(params, n: int, overrides: dict):
+    if params is None:
+        return AcoParams.for_instance(n, **overrides)
+    if overrides:
+        raise TypeError("pass either an AcoParams object or keyword parameters, not both")
+    return params
+
+
+class _Timer:
+    """CUDA-event pairs around selected launches (no-op without a dict)."""
+
+    def __init__(self, timers: dict | None):
+        self.timers = timers
+        self._open = {}
+
+    def start(self, name: str) -> None:
+        if self.timers is not None and name in self.timers:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self._open[name] = e
+
+    def stop(self, name: str) -> None:
+        if name in self._open:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record()
+            self.timers[name].append((self._open.pop(name), e))
+
+
+class Solver:
+    """TensorACO on one B200, or sharded over the ranks of a process group.
+
+    instance: a TspInstance (this package's or the reference's) or an (n, n)
+    distance matrix.  params: an AcoParams, or keyword overrides of
+    ``AcoParams.for_instance`` (alpha, beta, rho, n_ants / m, k, selection,
+    seed, gamma_schedule, q0_tau, max_iters).
+    construct: "sorted" (pruned scan, default) or "dense" (full-row stream).
+    group: torch.distributed group to shard ants over (default: the world
+    group when initialized with more than one rank).
+    """
+
+    def __init__(self, instance, params=None, *, construct: str = "sorted", group=None, **overrides):
+        self.inst = _as_instance(instance)
+        self.n = n = int(self.inst.n)
+        self.params = p = _as_params(params, n, overrides)
+        construction_gamma(p, 0)  # validates the mechanism (RW is out of scope)
+        if construct not in ("sorted", "dense"):
+            raise ValueError(f"construct must be 'sorted' or 'dense', got {construct!r}")
+        lib = _lib.load()
+        if construct == "sorted" and n > lib.taco_max_sorted_n():
+            construct = "dense"
+        self.construct = construct
+        self._variant = _lib.CONSTRUCT_SORTED if construct == "sorted" else _lib.CONSTRUCT_DENSE
+
+        self.group = group
+        if group is None and tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1:
+            self.group = tdist.group.WORLD
+        world = tdist.get_world_size(self.group) if self.group is not None else 1
+        rank = tdist.get_rank(self.group) if self.group is not None else 0
+        self.shard: AntShard = shard_ants(p.m, rank, world)
+
+        self.di = _device.device_instance(self.inst)
+        dev = self.dev = self.di.dev
+        m, k = p.m, p.k
+        self.eta_b = self.di.eta_beta(p.beta)
+        self.tau = torch.full((n, n), float(p.q0_tau), dtype=torch.float64, device=dev)
+        self.tau.fill_diagonal_(0.0)
+        self.tables = _device.SelectionTables(n, dev, dense=(construct == "dense"),
+                                              sorted_=(construct == "sorted"))
+        sh = self.shard
+        # zero-initialized so a failed construction never leaves out-of-range cities
+        self.tours_local = torch.zeros((sh.per_rank, n), dtype=torch.int32, device=dev)
+        self.costs_local = torch.zeros(sh.per_rank, dtype=torch.float64, device=dev)
+        if world > 1:
+            self.tours_all = torch.zeros((m, n), dtype=torch.int32, device=dev)
+            self.costs_all = torch.zeros(m, dtype=torch.float64, device=dev)
+            uneven = m % world != 0
+            self._pad_tours = torch.zeros((world * sh.per_rank, n), dtype=torch.int32, device=dev) if uneven else None
+            self._pad_costs = torch.zeros(world * sh.per_rank, dtype=torch.float64, device=dev) if uneven else None
+        else:
+            self.tours_all, self.costs_all = self.tours_local, self.costs_local
+        self.order = torch.zeros(m, dtype=torch.int32, device=dev)
+        self.elite_ws = _device.EliteWorkspace(m, dev)
+        self.nbr = torch.zeros((k, n, 2), dtype=torch.int32, device=dev)
+        self.inc = torch.zeros(k, dtype=torch.float64, device=dev)
+        self.best_cost = torch.full((1,), math.inf, dtype=torch.float64, device=dev)
+        self.best_tour = torch.zeros(n, dtype=torch.int32, device=dev)
+        self.best_iter = torch.full((1,), -1, dtype=torch.int32, device=dev)
+        self.rowsum = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.status = _device.new_status(dev)
+        self.iteration = 0
+        self.keep = 1.0 - p.rho  # pheromone.py:81 evaluates (1.0 - rho) in float64
+        # P / W for iteration 0 from the initial pheromone (bench.py:191-192)
+        self._rebuild_tables(evaporate=False, gamma_next=construction_gamma(p, 0))
+
+    # ------------------------------------------------------------------
+    def _rebuild_tables(self, evaporate: bool, gamma_next: float) -> None:
+        t = self.tables
+        _device.row_update(
+            self.n, tau_in=self.tau, tau_out=self.tau if evaporate else None, eta_b=self.eta_b,
+            nbr=self.nbr if evaporate else None, inc=self.inc if evaporate else None,
+            k=self.params.k if evaporate else 0, do_evap=evaporate, keep=self.keep, want_p=True,
+            alpha=float(self.params.alpha), inv_gamma=1.0 / gamma_next, rowsum_out=self.rowsum,
+            w_out=t.w, ldw=t.ldw, sw_out=t.sw, si_out=t.si, status=self.status)
+
+    def step_async(self, timers: dict | None = None, scan_count: torch.Tensor | None = None) -> None:
+        """Enqueue one full iteration on the current stream (no host sync).
+
+        timers: optional {"construct": [...], "update": [...]} lists that get
+        a (start, end) CUDA-event pair around those launches (bench.py).
+        scan_count: optional device u64 that accumulates the table windows
+        the sorted construction kernel read.
+        """
+        p, sh, it = self.params, self.shard, self.iteration
+        lib = _lib.load()
+        ev = _Timer(timers)
+        ev.start("construct")
+        _device.construct(self.n, sh.count, sh.offset, self._variant, self.tables, p.seed, it,
+                          self.tours_local, self.status, scan_count)
+        ev.stop("construct")
+        _device.tour_cost(self.tours_local[:sh.count], self.di.dist, self.costs_local[:sh.count])
+        if sh.world > 1:
+            gather_colony(self.tours_local, self.costs_local, sh, self.tours_all, self.costs_all,
+                          self.group, self._pad_tours, self._pad_costs)
+        _device.elite_order(self.costs_all, self.elite_ws, self.order)
+        _lib.check(lib.taco_track_best(self.n, self.tours_all.data_ptr(), self.costs_all.data_ptr(),
+                                       self.order.data_ptr(), self.best_cost.data_ptr(),
+                                       self.best_tour.data_ptr(), self.best_iter.data_ptr(), it & 0xFFFFFFFF,
+                                       _device.stream_handle()), "taco_track_best")
+        _device.elite_neighbors(self.tours_all, self.order, self.costs_all, p.k, self.nbr, self.inc)
+        ev.start("update")
+        self._rebuild_tables(evaporate=True, gamma_next=construction_gamma(p, it + 1))
+        ev.stop("update")
+        self.iteration = it + 1
+
+    def check(self) -> None:
+        """Raise the reference's exception for any failure recorded so far."""
+        code, _ = _device.read_status(self.status)
+        if code == _lib.TACO_UNDERFLOW:
+            from .colony import _underflow_from_sums
+            raise _underflow_from_sums(_device.download(self.rowsum))
+        if code == _lib.TACO_NO_CANDIDATE:
+            raise AssertionError("selector chose a visited city")
+        if code != 0:
+            raise RuntimeError(f"device status {code}")
+
+    def best(self) -> tuple[np.ndarray, float]:
+        """(best tour so far as int64 array, its length)."""
+        tour = _device.download(self.best_tour).astype(np.int64)
+        return tour, float(self.best_cost.item())
+
+    def step(self) -> tuple[np.ndarray, float]:
+        """Run one iteration; return the best tour so far and its length."""
+        self.step_async()
+        self.check()
+        return self.best()
+
+    def run(self, max_iters: int | None = None) -> tuple[np.ndarray, float]:
+        """Run ``max_iters`` iterations (default params.max_iters) and return
+        the best tour and length."""
+        iters = self.params.max_iters if max_iters is None else int(max_iters)
+        for _ in range(iters):
+            self.step_async()
+        self.check()
+        return self.best()
+
+    # ---- state inspection (host copies) ---------------------------------
+    def pheromone(self) -> PheromoneState:
+        return PheromoneState(tau=_device.download(self.tau), iteration=self.iteration)
+
+    def probability(self) -> ProbabilityMatrix:
+        p = torch.empty_like(self.tau)
+        _device.row_update(self.n, tau_in=self.tau, eta_b=self.eta_b, want_p=True,
+                           alpha=float(self.params.alpha), p_out=p)
+        return ProbabilityMatrix(p=_device.download(p))
+
+    def last_batch(self) -> TourBatch:
+        """Tours and lengths of the most recent iteration (all ranks' ants)."""
+        return TourBatch(tours=_device.download(self.tours_all).astype(np.int64),
+                         costs=_device.download(self.costs_all))
+
+    def elite_order(self) -> np.ndarray:
+        return _device.download(self.order)
+
+
+__all__ = ["Solver", "NumericalUnderflow"]

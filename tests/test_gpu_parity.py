@@ -1,0 +1,300 @@
+"""GPU parity: the CUDA path through the C ABI against the oracle and the
+golden vectors of the reference.
+
+Bars (BASELINE.json north_star): tours / argmax choices bit-exact given the
+same P and the same uniform stream; P, tau, deltas bit-exact (alpha, beta in
+numpy's exact power set) else <= 1e-12 relative (tolerance well inside the
+1e-6 the north star allows); tour lengths bit-exact (pairwise order).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2404_04895_b200 as taco
+from paper_2404_04895_b200 import _device, _lib
+from paper_2404_04895_b200 import rng as trng
+from conftest import euclid
+from oracle import fastpath, reference_port as ref
+
+pytestmark = pytest.mark.gpu
+
+
+def _params(golden, name, seed):
+    n, m, k, iters, alpha, beta, rho, period, adair = golden[f"{name}/meta"]
+    return taco.AcoParams(m=int(m), k=int(k), alpha=alpha, beta=beta, rho=rho,
+                          selection="adair" if adair else "ir",
+                          gamma_schedule=taco.GammaSchedule(1.5, 1.0, int(period)), seed=seed), int(iters)
+
+
+def _inst(golden, name):
+    return taco.TspInstance(n=golden[f"{name}/dist"].shape[0], dist=golden[f"{name}/dist"],
+                            eta=golden[f"{name}/eta"])
+
+
+# ---------------------------------------------------------------------------
+# RNG
+# ---------------------------------------------------------------------------
+def test_device_philox_known_answers():
+    dev = _device.device()
+    ctr = torch.tensor([[0, 0, 0, 0], [-1, -1, -1, -1],
+                        [0x243F6A88, 0x85A308D3 - 2**32, 0x13198A2E, 0x03707344]], dtype=torch.int32, device=dev)
+    key = torch.tensor([[0, 0], [-1, -1], [0xA4093822 - 2**32, 0x299F31D0]], dtype=torch.int32, device=dev)
+    out = torch.empty((3, 4), dtype=torch.int32, device=dev)
+    _lib.check(_lib.load().taco_philox4x32_10(3, ctr.data_ptr(), key.data_ptr(), out.data_ptr(),
+                                              _device.stream_handle()), "philox")
+    got = out.cpu().numpy().astype(np.uint32)
+    assert got.tolist() == [[0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8],
+                            [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD],
+                            [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]]
+
+
+def test_device_uniforms_and_starts_match_restatement():
+    g = np.random.default_rng(0)
+    step = g.integers(1, 5000, 4096)
+    ant = g.integers(0, 70000, 4096)
+    city = g.integers(0, 10000, 4096)
+    seed = 2**40 + 12345
+    u = trng.device_uniforms(seed, 77, step, ant, city)
+    assert np.array_equal(u, fastpath.uniforms(seed, 77, step, ant, city))
+    assert np.array_equal(trng.device_starts(seed, 3, 2392, 4096, ant_offset=100),
+                          fastpath.starts(seed, 3, np.arange(100, 4196), 2392))
+
+
+# ---------------------------------------------------------------------------
+# drop-ins against the reference's golden pipeline
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("name", ["int12_ir", "int12_adair", "euc23_adair", "euc17_ab"])
+def test_dropin_pipeline_matches_reference_golden(golden, name):
+    inst = _inst(golden, name)
+    for seed in golden[f"{name}/seeds"].tolist():
+        params, iters = _params(golden, name, seed)
+        tau = taco.PheromoneState.initial(inst.n, params.q0_tau)
+        prob = taco.compute_probability_matrix(tau, inst, params)
+        for it in range(iters):
+            key = f"{name}/s{seed}/it{it}"
+            if params.alpha in (0.5, 1.0, 2.0) and params.beta in (0.0, 0.5, 1.0, 2.0):
+                assert np.array_equal(prob.p, golden[f"{key}/p"])
+            else:
+                np.testing.assert_allclose(prob.p, golden[f"{key}/p"], rtol=1e-12, atol=0)
+            # reference-stream replay: feed the golden P so tours are comparable bitwise
+            batch = taco.construct_tours(taco.ProbabilityMatrix(golden[f"{key}/p"]), inst, params, it,
+                                         stream="numpy")
+            assert np.array_equal(batch.tours, golden[f"{key}/tours"])
+            assert np.array_equal(batch.costs, golden[f"{key}/costs"])
+            elites = taco.select_elite(batch, params.k)
+            assert [c for _, c in elites] == golden[f"{key}/costs"][golden[f"{key}/order"]].tolist()
+            delta = taco.accumulate_increments(elites, inst.n)
+            assert np.array_equal(delta, golden[f"{key}/delta"])
+            tau = taco.apply_update(tau, delta, params.rho)
+            assert np.array_equal(tau.tau, golden[f"{key}/tau"])
+            assert tau.iteration == it + 1
+            prob = taco.compute_probability_matrix(tau, inst, params)
+
+
+@pytest.mark.parametrize("mech", ["ir", "adair"])
+@pytest.mark.parametrize("n,m", [(5, 1), (10, 7), (51, 64)])
+def test_reference_stream_tours_bit_exact(mech, n, m):
+    inst = euclid(n + m, n)
+    for seed in range(3):
+        params = taco.AcoParams(m=m, k=1, selection=mech, seed=seed,
+                                gamma_schedule=taco.GammaSchedule(1.5, 1.0, 7))
+        tau = ref.initial_tau(n, 1.0)
+        p = ref.transition(tau, inst.eta, 1.0, 2.0)
+        for it in (0, 3):
+            got = taco.construct_tours(taco.ProbabilityMatrix(p), inst, params, it, stream="numpy")
+            want = ref.build_tours(p, m, seed, it, ref.gamma(it, 1.5, 1.0, 7) if mech == "adair" else 1.0)
+            assert np.array_equal(got.tours, want)
+            assert np.array_equal(got.costs, ref.lengths(want, inst.dist))
+
+
+# ---------------------------------------------------------------------------
+# fast path: both construction variants against the product-rule restatement
+# ---------------------------------------------------------------------------
+def _device_tables(p, gamma):
+    dev = _device.device()
+    n = p.shape[0]
+    t = _device.SelectionTables(n, dev, dense=True, sorted_=True)
+    _device.selection_table_from_p(_device.upload(p, dev), 1.0 / gamma, t)
+    return t
+
+
+@pytest.mark.parametrize("n,m,gamma", [(7, 5, 1.0), (40, 33, 1.0), (97, 64, 1.37), (300, 40, 1.5)])
+def test_fast_construction_matches_restatement(n, m, gamma):
+    inst = euclid(n, n)
+    g = np.random.default_rng(n)
+    tau = g.uniform(0.05, 3.0, (n, n))
+    tau = (tau + tau.T) / 2
+    p = ref.transition(tau, inst.eta, 1.0, 2.0)
+    t = _device_tables(p, gamma)
+    w = t.w[:, :n].cpu().numpy()
+    # the tables hold exactly fp32(P^(1/gamma)), row-sorted descending
+    if gamma == 1.0:
+        assert np.array_equal(w, p.astype(np.float32))
+    sw, si = t.sw.cpu().numpy(), t.si.cpu().numpy().astype(np.int64)
+    assert np.array_equal(np.take_along_axis(w, si, axis=1), sw)
+    assert (np.diff(sw, axis=1) <= 0).all()
+    seed, it = 11, 5
+    want = fastpath.build_tours(w, seed, it, np.arange(m))
+    for variant in (_lib.CONSTRUCT_SORTED, _lib.CONSTRUCT_DENSE):
+        tours = torch.zeros((m, n), dtype=torch.int32, device=t.w.device)
+        status = _device.new_status(t.w.device)
+        _device.construct(n, m, 0, variant, t, seed, it, tours, status)
+        assert _device.read_status(status)[0] == 0
+        assert np.array_equal(tours.cpu().numpy(), want), variant
+
+
+def test_fast_rule_agrees_with_reference_log_rule():
+    # same device uniforms, reference log-domain rule vs the fast kernel
+    n, m = 120, 48
+    inst = euclid(5, n)
+    p = ref.transition(ref.initial_tau(n, 1.0), inst.eta, 1.0, 2.0)
+    params = taco.AcoParams(m=m, k=1, selection="ir", seed=4)
+    got = taco.construct_tours(taco.ProbabilityMatrix(p), inst, params, 2).tours
+    want = fastpath.log_rule_tours(p, 1.0, 4, 2, np.arange(m))
+    mismatches = int((got != want).any(axis=1).sum())
+    assert mismatches == 0
+
+
+def test_dense_and_sorted_agree_at_scale():
+    n, m = 1000, 256
+    inst = euclid(1, n)
+    params = taco.AcoParams(m=m, k=25, selection="adair", seed=3)
+    p = taco.compute_probability_matrix(taco.PheromoneState.initial(n, 1.0), inst, params)
+    a = taco.construct_tours(p, inst, params, 0, variant="sorted")
+    b = taco.construct_tours(p, inst, params, 0, variant="dense")
+    assert np.array_equal(a.tours, b.tours)
+    assert np.array_equal(np.sort(a.tours, axis=1), np.broadcast_to(np.arange(n), (m, n)))
+    assert np.array_equal(a.costs, ref.lengths(a.tours, inst.dist))
+
+
+# ---------------------------------------------------------------------------
+# individual ops and error behaviour
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [3, 8, 129, 1000, 2392])
+def test_batch_costs_bit_exact(n):
+    inst = euclid(n, n)
+    g = np.random.default_rng(n)
+    tours = np.stack([g.permutation(n) for _ in range(17)])
+    assert np.array_equal(taco.batch_costs(tours, inst), ref.lengths(tours, inst.dist))
+
+
+def test_probability_general_exponents_and_underflow():
+    inst = euclid(2, 31)
+    tau = np.random.default_rng(0).uniform(0.1, 2.0, (31, 31))
+    for alpha, beta in ((1.0, 2.0), (0.5, 0.0), (1.3, 2.7), (2.0, 1.0)):
+        params = taco.AcoParams(m=4, k=1, alpha=alpha, beta=beta)
+        got = taco.compute_probability_matrix(taco.PheromoneState(tau), inst, params).p
+        want = ref.transition(tau, inst.eta, alpha, beta)
+        if alpha in (0.5, 1.0, 2.0) and beta in (0.0, 0.5, 1.0, 2.0):
+            assert np.array_equal(got, want)
+        else:
+            np.testing.assert_allclose(got, want, rtol=1e-12, atol=0)
+    with pytest.raises(taco.NumericalUnderflow):
+        taco.compute_probability_matrix(taco.PheromoneState(np.zeros((31, 31))), inst,
+                                        taco.AcoParams(m=4, k=1))
+    hot = np.full((31, 31), 1e308)
+    with pytest.raises(taco.NumericalUnderflow):
+        taco.compute_probability_matrix(taco.PheromoneState(hot), inst, taco.AcoParams(m=4, k=1, alpha=4.0))
+
+
+def test_select_elite_ties_and_bounds():
+    b = taco.TourBatch(tours=np.array([[0, 1, 2], [1, 2, 0], [2, 0, 1]]), costs=np.array([4.0, 4.0, 1.0]))
+    e = taco.select_elite(b, 2)
+    assert np.array_equal(e[0][0], [2, 0, 1]) and np.array_equal(e[1][0], [0, 1, 2])
+    with pytest.raises(ValueError):
+        taco.select_elite(b, 0)
+    g = np.random.default_rng(1)
+    costs = g.integers(0, 50, 5000).astype(np.float64)  # many ties
+    order = np.argsort(costs, kind="stable")
+    batch = taco.TourBatch(tours=np.zeros((5000, 3), dtype=np.int64) + np.arange(3), costs=costs)
+    got = [c for _, c in taco.select_elite(batch, 5000)]
+    assert got == costs[order].tolist()
+
+
+def test_accumulate_matches_reference_with_duplicates():
+    g = np.random.default_rng(7)
+    for n, k in ((3, 1), (9, 40), (64, 33), (500, 3)):
+        base = [g.permutation(n) for _ in range(max(1, k // 3))]
+        elites = [(base[g.integers(len(base))], float(g.uniform(1.0, 50.0))) for _ in range(k)]
+        want = ref.deposit(np.stack([t for t, _ in elites]), np.array([c for _, c in elites]), n)
+        assert np.array_equal(taco.accumulate_increments(elites, n), want)
+    with pytest.raises(taco.InvalidPermutation):
+        taco.accumulate_increments([(np.array([0, 1, 1]), 3.0)], 3)
+    with pytest.raises(ValueError):
+        taco.accumulate_increments([], 3)
+
+
+def test_apply_update_floor_and_formula():
+    tau0 = taco.PheromoneState(tau=np.full((3, 3), 2.0) - 2.0 * np.eye(3), iteration=4)
+    delta = np.zeros((3, 3))
+    delta[0, 1] = delta[1, 0] = 0.5
+    out = taco.apply_update(tau0, delta, rho=0.25)
+    assert out.iteration == 5 and out.tau[0, 1] == 2.0 * 0.75 + 0.5 and out.tau[0, 2] == 1.5
+    assert out.tau[0, 0] == taco.TAU_MIN
+    with pytest.raises(ValueError):
+        taco.apply_update(tau0, delta, rho=1.0)
+
+
+# ---------------------------------------------------------------------------
+# Solver
+# ---------------------------------------------------------------------------
+@pytest.mark.parametrize("construct", ["sorted", "dense"])
+def test_solver_matches_chained_dropins(construct):
+    n, m = 60, 40
+    inst = euclid(8, n)
+    params = taco.AcoParams(m=m, k=4, selection="adair", seed=6, gamma_schedule=taco.GammaSchedule(1.5, 1.0, 5))
+    s = taco.Solver(inst, params, construct=construct)
+    tau = taco.PheromoneState.initial(n, 1.0)
+    best = np.inf
+    for it in range(6):
+        prob = taco.compute_probability_matrix(tau, inst, params)
+        batch = taco.construct_tours(prob, inst, params, it, variant=construct)
+        elites = taco.select_elite(batch, params.k)
+        tau = taco.apply_update(tau, taco.accumulate_increments(elites, n), params.rho)
+        tour, length = s.step()
+        got = s.last_batch()
+        assert np.array_equal(got.tours, batch.tours)
+        assert np.array_equal(got.costs, batch.costs)
+        assert np.array_equal(s.pheromone().tau, tau.tau)
+        best = min(best, batch.costs.min())
+        assert length == best
+        assert taco.tour_cost(tour, inst) == length
+
+
+def test_solver_shard_offsets_are_invisible():
+    # two "ranks" emulated by construction offsets on one GPU: same rows
+    n, m = 80, 24
+    inst = euclid(9, n)
+    params = taco.AcoParams(m=m, k=3, selection="ir", seed=1)
+    p = taco.compute_probability_matrix(taco.PheromoneState.initial(n, 1.0), inst, params)
+    t = _device_tables(p.p, 1.0)
+    dev = t.w.device
+    whole = torch.zeros((m, n), dtype=torch.int32, device=dev)
+    st = _device.new_status(dev)
+    _device.construct(n, m, 0, _lib.CONSTRUCT_SORTED, t, 1, 0, whole, st)
+    a = torch.zeros((10, n), dtype=torch.int32, device=dev)
+    b = torch.zeros((14, n), dtype=torch.int32, device=dev)
+    _device.construct(n, 10, 0, _lib.CONSTRUCT_SORTED, t, 1, 0, a, st)
+    _device.construct(n, 14, 10, _lib.CONSTRUCT_SORTED, t, 1, 0, b, st)
+    assert torch.equal(torch.cat([a, b]), whole)
+
+
+def test_solver_quality_matches_reference_statistically():
+    # best-tour quality over 10 seeds: engine vs the reference algorithm
+    n, m, iters = 30, 30, 40
+    coords = np.random.default_rng(123).uniform(0, 1000, (n, 2))
+    inst = taco.euclidean_instance(coords)
+    dist, eta = ref.instance_arrays(coords)
+    ours, theirs = [], []
+    for seed in range(10):
+        params = taco.AcoParams(m=m, k=3, selection="adair", seed=seed,
+                                gamma_schedule=taco.GammaSchedule(1.5, 1.0, iters))
+        ours.append(taco.Solver(inst, params).run(iters)[1])
+        cfg = ref.Config(m=m, k=3, selection="adair", period=iters, seed=seed)
+        theirs.append(ref.run(dist, eta, cfg, iters)[-1])
+    ours, theirs = np.array(ours), np.array(theirs)
+    # mean best lengths within 3%, and neither side systematically better by > 3 sigma
+    assert abs(ours.mean() - theirs.mean()) / theirs.mean() < 0.03
+    se = np.sqrt(ours.var(ddof=1) / 10 + theirs.var(ddof=1) / 10)
+    assert abs(ours.mean() - theirs.mean()) <= 3 * se + 1e-9 * theirs.mean()

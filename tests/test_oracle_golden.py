@@ -1,0 +1,139 @@
+"""CPU: pin the oracle restatements before trusting them.
+
+* oracle.reference_port reproduces the golden vectors produced by running the
+  reference package itself (tests/golden/make_golden.py) bit for bit.
+* oracle.fastpath's Philox4x32-10 reproduces the Random123 known-answer
+  vectors, and its pairwise-sum restatement equals numpy's ndarray.sum.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_cases
+from oracle import fastpath, reference_port as ref
+
+
+def _case(golden, name):
+    n, m, k, iters, alpha, beta, rho, period, adair = golden[f"{name}/meta"]
+    cfg = ref.Config(m=int(m), k=int(k), alpha=alpha, beta=beta, rho=rho,
+                     selection="adair" if adair else "ir", period=int(period))
+    return int(n), int(iters), cfg, golden[f"{name}/dist"], golden[f"{name}/eta"]
+
+
+def test_golden_has_cases(golden):
+    assert len(golden_cases(golden)) >= 4
+
+
+@pytest.mark.parametrize("name", ["int12_ir", "int12_adair", "euc23_adair", "euc17_ab"])
+def test_reference_port_reproduces_reference_pipeline(golden, name):
+    n, iters, cfg, dist, eta = _case(golden, name)
+    for seed in golden[f"{name}/seeds"].tolist():
+        cfg.seed = seed
+        tau = ref.initial_tau(n, cfg.q0_tau)
+        p = ref.transition(tau, eta, cfg.alpha, cfg.beta)
+        for it in range(iters):
+            key = f"{name}/s{seed}/it{it}"
+            assert np.array_equal(p, golden[f"{key}/p"])
+            assert cfg.gamma(it) == golden[f"{key}/gamma"][0]
+            assert np.array_equal(ref.start_block(seed, it, cfg.m, n), golden[f"{key}/starts"])
+            out = ref.iterate(tau, p, dist, eta, cfg, it)
+            assert np.array_equal(out["tours"], golden[f"{key}/tours"])
+            assert np.array_equal(out["costs"], golden[f"{key}/costs"])
+            assert np.array_equal(out["order"], golden[f"{key}/order"])
+            assert np.array_equal(out["delta"], golden[f"{key}/delta"])
+            assert np.array_equal(out["tau"], golden[f"{key}/tau"])
+            tau, p = out["tau"], out["p"]
+
+
+def test_gamma_known_answers(golden):
+    got = [ref.gamma(t) for t in (0, 250, 500, 999, 1000)]
+    assert got == golden["kat/gamma"].tolist()
+    assert got[0] == 1.5 and got[-1] == 1.5
+    assert abs(got[1] - 1.4268) < 5e-5  # reference tests/test_selection.py:28-41
+
+
+def test_deposit_hand_case(golden):
+    # reference tests/test_pheromone.py:59-67: tour [0,1,2] of cost 4
+    d = ref.deposit(np.array([[0, 1, 2]]), np.array([4.0]), 3)
+    assert np.array_equal(d, golden["kat/increment_0_1_2_cost4"])
+    assert np.array_equal(d, 0.25 * (1 - np.eye(3)))
+
+
+def test_update_hand_case():
+    # reference tests/test_pheromone.py:110-124
+    tau = np.full((3, 3), 2.0) - 2.0 * np.eye(3)
+    delta = np.zeros((3, 3))
+    delta[0, 1] = delta[1, 0] = 0.5
+    out = ref.evaporate(tau, delta, 0.25)
+    assert out[0, 1] == 2.0 * 0.75 + 0.5 and out[0, 2] == 1.5
+    assert out[0, 0] == ref.TAU_MIN
+
+
+def test_probability_known_answer():
+    # SPEC.md:183 example: tau = 1, alpha = beta = 1, dist row 0 = [0, 1, 2]
+    dist = np.array([[0.0, 1.0, 2.0], [1.0, 0.0, 1.0], [2.0, 1.0, 0.0]])
+    eta = np.where(dist > 0, 1.0 / np.where(dist > 0, dist, 1.0), 0.0)
+    p = ref.transition(np.ones((3, 3)), eta, 1.0, 1.0)
+    assert np.allclose(p[0], [0.0, 2 / 3, 1 / 3], rtol=0, atol=1e-15)
+
+
+# ---------------------------------------------------------------------------
+# fast-path restatement
+# ---------------------------------------------------------------------------
+KAT = [  # Random123 philox4x32-10 known-answer vectors
+    ((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
+    ((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2, (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
+    ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
+     (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
+]
+
+
+@pytest.mark.parametrize("ctr,key,want", KAT)
+def test_philox_known_answers(ctr, key, want):
+    got = fastpath.philox4x32_10(np.array([ctr], dtype=np.uint64), np.array(key, dtype=np.uint64))[0]
+    assert tuple(int(v) for v in got) == want
+
+
+def test_uniform_conversion_is_exact_and_open():
+    x = np.array([0, 1 << 9, 0xFFFFFFFF, 0x80000000], dtype=np.uint32)
+    u = fastpath.bits_to_uniform(x)
+    assert u.dtype == np.float32
+    k = (x >> 9).astype(np.float64)
+    assert np.array_equal(u.astype(np.float64), (k + 0.5) * 2.0 ** -23)
+    assert 0.0 < u.min() and u.max() < 1.0
+
+
+def test_pairwise_restatement_matches_numpy():
+    g = np.random.default_rng(3)
+    for n in list(range(1, 140)) + [255, 256, 257, 1000, 2392]:
+        a = g.uniform(0, 1, n) * 10.0 ** g.uniform(-6, 6, n)
+        assert fastpath.pairwise_sum(a) == a.sum()
+        rows = g.uniform(0, 1, (3, n))
+        s = rows.sum(axis=1)
+        for i in range(3):
+            assert fastpath.pairwise_sum(rows[i]) == s[i]
+
+
+def test_fastpath_tours_are_permutations_and_shard_invariant():
+    g = np.random.default_rng(0)
+    n = 29
+    dist, eta = ref.instance_arrays(g.uniform(0, 100, (n, 2)))
+    p = ref.transition(ref.initial_tau(n, 1.0), eta, 1.0, 2.0)
+    w = fastpath.selection_table(p, 1.0)
+    whole = fastpath.build_tours(w, 9, 4, np.arange(12))
+    assert np.array_equal(np.sort(whole, axis=1), np.broadcast_to(np.arange(n), whole.shape))
+    parts = np.concatenate([fastpath.build_tours(w, 9, 4, np.arange(0, 5)),
+                            fastpath.build_tours(w, 9, 4, np.arange(5, 12))])
+    assert np.array_equal(whole, parts)
+
+
+def test_product_rule_agrees_with_log_rule_on_shared_uniforms():
+    # same uniforms, product form vs the reference's log form: count mismatches
+    g = np.random.default_rng(1)
+    n = 40
+    dist, eta = ref.instance_arrays(g.uniform(0, 1000, (n, 2)))
+    p = ref.transition(ref.initial_tau(n, 1.0), eta, 1.0, 2.0)
+    w = fastpath.selection_table(p, 1.0)
+    a = fastpath.build_tours(w, 2, 0, np.arange(32))
+    b = fastpath.log_rule_tours(p, 1.0, 2, 0, np.arange(32))
+    assert (a != b).sum() == 0
