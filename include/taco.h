@@ -48,6 +48,9 @@ extern "C" {
 
 int taco_abi_version(void);
 const char *taco_status_string(int code);
+/* message of the last CUDA error a libtaco call returned TACO_ERR_CUDA for
+ * (per host thread; "" if none) */
+const char *taco_last_cuda_error(void);
 /* largest n the sorted-table (per-row block radix sort) path supports */
 int taco_max_sorted_n(void);
 
@@ -105,16 +108,20 @@ int taco_eta_power(int64_t count, const double *eta, double beta, double *out,
  * rule argmax(log P/gamma - E) by its product form argmax(W * u).
  * Ants [ant_offset, ant_offset + m_local) are built; tours_out is
  * m_local x n int32.  variant: TACO_CONSTRUCT_SORTED (needs sw/si) or
- * TACO_CONSTRUCT_DENSE (needs w, ldw).  scan_count (nullable, device u64) is
- * incremented by the number of 32-entry table windows the SORTED variant read
- * (a traffic probe for the roofline report).
+ * TACO_CONSTRUCT_DENSE (needs w, ldw).  When costs_out is given, the tour
+ * lengths are accumulated during construction from dist (n x n f64) in numpy's
+ * pairwise order (model.batch_costs model.py:292-295, bit-exact).
+ * scan_count (nullable, device u64) is incremented by the number of 32-entry
+ * global table windows the SORTED variant read (traffic probe for the
+ * roofline report).
  */
 int taco_construct(int n, int m_local, int ant_offset, int variant,
                    const float *w, int ldw,
                    const float *sw, const uint16_t *si,
                    uint64_t seed, uint32_t iteration,
-                   int32_t *tours_out, int32_t *status,
-                   unsigned long long *scan_count, void *stream);
+                   const double *dist, int32_t *tours_out, double *costs_out,
+                   int32_t *status, unsigned long long *scan_count,
+                   void *stream);
 
 /* Start cities of the device stream (rng.start_cities rng.py:65-68 analog). */
 int taco_starts(int n, int m_local, int ant_offset, uint64_t seed,

@@ -130,11 +130,13 @@ def selection_table_from_p(p: torch.Tensor, inv_gamma: float, tables: SelectionT
 
 def construct(n: int, m_local: int, ant_offset: int, variant: int, tables: SelectionTables,
               seed: int, iteration: int, tours_out: torch.Tensor, status: torch.Tensor,
-              scan_count: torch.Tensor | None = None) -> None:
+              scan_count: torch.Tensor | None = None, dist: torch.Tensor | None = None,
+              costs_out: torch.Tensor | None = None) -> None:
+    """Build tours (and, with dist + costs_out, their lengths) on the device."""
     code = _lib.load().taco_construct(
         n, m_local, ant_offset, variant, ptr(tables.w), tables.ldw, ptr(tables.sw), ptr(tables.si),
-        int(seed), int(iteration) & 0xFFFFFFFF, ptr(tours_out), ptr(status), ptr(scan_count),
-        stream_handle())
+        int(seed), int(iteration) & 0xFFFFFFFF, ptr(dist), ptr(tours_out), ptr(costs_out), ptr(status),
+        ptr(scan_count), stream_handle())
     check(code, "taco_construct")
 
 

@@ -35,6 +35,7 @@ _p = ctypes.c_void_p
 SIGNATURES = {
     "taco_abi_version": (_c_int, []),
     "taco_status_string": (ctypes.c_char_p, [_c_int]),
+    "taco_last_cuda_error": (ctypes.c_char_p, []),
     "taco_max_sorted_n": (_c_int, []),
     "taco_row_update": (_c_int, [
         _c_int, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _c_f64, _c_int, _c_f64, _c_f64,
@@ -42,7 +43,7 @@ SIGNATURES = {
     "taco_selection_table": (_c_int, [_c_int, _p, _c_f64, _p, _c_int, _p, _p, _p]),
     "taco_eta_power": (_c_int, [_c_i64, _p, _c_f64, _p, _p]),
     "taco_construct": (_c_int, [
-        _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_u64, _c_u32, _p, _p, _p, _p]),
+        _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _p]),
     "taco_starts": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u32, _p, _p]),
     "taco_uniforms": (_c_int, [_c_int, _p, _p, _p, _c_u64, _c_u32, _p, _p]),
     "taco_philox4x32_10": (_c_int, [_c_int, _p, _p, _p, _p]),
@@ -95,6 +96,8 @@ def check(code: int, what: str) -> None:
     msg = load().taco_status_string(code).decode()
     if code == TACO_ERR_ARG:
         raise ValueError(f"{what}: {msg}")
+    if code == TACO_ERR_CUDA:
+        msg += f" ({load().taco_last_cuda_error().decode()})"
     raise TacoError(f"{what}: {msg} (code {code})")
 
 

@@ -98,7 +98,7 @@ def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = No
     """
     if probe is not None:
         raise NotImplementedError("construction probes are not supported by the device engine")
-    if chunk_size is not None and chunk_size < 1 and chunk_size < params.m:
+    if chunk_size is not None and chunk_size < 1:
         raise ValueError(f"chunk_size must be >= 1, got {chunk_size}")
     n, m = int(inst.n), int(params.m)
     gamma = construction_gamma(params, iteration)
@@ -107,16 +107,17 @@ def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = No
     p_host = np.asarray(p.p, dtype=np.float64)
     if stream == "numpy":
         tours_t = _construct_reference_stream(p_host, n, m, params.seed, iteration, gamma, dev)
+        costs_t = _device.tour_cost(tours_t, di.dist)
     elif stream == "device":
-        tours_t = _construct_device_stream(p_host, n, m, params.seed, iteration, gamma, dev, variant)
+        tours_t, costs_t = _construct_device_stream(p_host, n, m, params.seed, iteration, gamma, dev,
+                                                    variant, di.dist)
     else:
         raise ValueError(f"stream must be 'device' or 'numpy', got {stream!r}")
-    costs_t = _device.tour_cost(tours_t, di.dist)
     return TourBatch(tours=_device.download(tours_t).astype(np.int64, copy=False),
                      costs=_device.download(costs_t))
 
 
-def _construct_device_stream(p_host, n, m, seed, iteration, gamma, dev, variant) -> torch.Tensor:
+def _construct_device_stream(p_host, n, m, seed, iteration, gamma, dev, variant, dist):
     if variant == "sorted" and n > _lib.load().taco_max_sorted_n():
         variant = "dense"
     if variant not in ("sorted", "dense"):
@@ -125,11 +126,12 @@ def _construct_device_stream(p_host, n, m, seed, iteration, gamma, dev, variant)
     tables = _device.SelectionTables(n, dev, dense=(variant == "dense"), sorted_=(variant == "sorted"))
     _device.selection_table_from_p(p_t, 1.0 / gamma, tables)
     tours = torch.zeros((m, n), dtype=torch.int32, device=dev)
+    costs = torch.empty(m, dtype=torch.float64, device=dev)
     status = _device.new_status(dev)
     code = _lib.CONSTRUCT_SORTED if variant == "sorted" else _lib.CONSTRUCT_DENSE
-    _device.construct(n, m, 0, code, tables, seed, iteration, tours, status)
+    _device.construct(n, m, 0, code, tables, seed, iteration, tours, status, dist=dist, costs_out=costs)
     _raise_construct_status(status)
-    return tours
+    return tours, costs
 
 
 def _raise_construct_status(status: torch.Tensor) -> None:

@@ -1,7 +1,8 @@
 // Tour construction kernels: one warp owns one ant for all n-1 lockstep steps.
 //
 // Reference: colony.construct_tours colony.py:87-154 (IR / AdaIR branch),
-// argmax_select_block selection.py:143-155, start cities rng.py:65-68.
+// argmax_select_block selection.py:143-155, start cities rng.py:65-68, tour
+// lengths model.batch_costs model.py:292-295 (fused).
 //
 // Fast-path rule: next = argmax_j { W[cur, j] * u(step, ant, j) }
 // over unvisited j with W[cur, j] > 0, first (lowest j) of ties, where
@@ -11,13 +12,20 @@
 // Two variants compute the identical argmax:
 //   DENSE  streams the whole fp32 row W[cur, :] with 16-byte loads and draws
 //          four uniforms per Philox block (the north-star "row streaming"
-//          kernel; HBM/L2-bandwidth + ALU bound).
+//          kernel; ALU bound on Philox).
 //   SORTED scans the row's descending (W, j) table and stops as soon as the
 //          next table entry satisfies W < best score: since u < 1, no later
 //          entry can reach the running best, so the result is bit-identical to
 //          the full scan while touching only the head of the row.  Because the
 //          uniforms are counter-addressed by city, visiting candidates in
-//          sorted order draws exactly the values the full scan would.
+//          sorted order draws exactly the values the full scan would.  The
+//          first T entries of every row are cached in shared memory (one CTA
+//          per SM), so most steps never leave the SM: the median step stops
+//          after 3 entries.
+// Both variants accumulate the tour length on the fly in numpy's pairwise
+// order (bit-exact with batch_costs), so no separate m x n gather pass runs.
+#include <cstdlib>
+
 #include "taco_common.cuh"
 
 namespace taco {
@@ -41,55 +49,188 @@ struct TourWriter {
   }
 };
 
+// Tour length in numpy's pairwise order, fed one edge at a time in position
+// order e = 0..n-1 (edge e joins t[e] and t[(e+1) % n]).  Edge lengths of the
+// current pairwise-tree leaf (<= 128 positions, taco_common.cuh) are parked in
+// a per-ant shared buffer; when the leaf is complete lane 0 sums it with
+// pw_leaf_sum, and the leaf sums are folded at the end — the exact operation
+// sequence of ndarray.sum(axis=1), at one shared store per step.
+struct LeafCost {
+  const double *dist;
+  const int2 *leaves;
+  double *buf;       // per-ant shared buffer, kPwBlock entries
+  double *leaf_sum;  // per-ant shared, n_leaves entries
+  int n, lane, L, i, len;
+  double pending;
+  bool active;
+
+  __device__ __forceinline__ void init(const double *d, const int2 *lv, double *b, double *ls, int n_,
+                                       int lane_) {
+    dist = d;
+    leaves = lv;
+    buf = b;
+    leaf_sum = ls;
+    n = n_;
+    lane = lane_;
+    active = d != nullptr;
+    L = 0;
+    i = 0;
+    len = active ? leaves[0].y : 0;
+    pending = 0.0;
+  }
+  // lane 0 starts loading the length of edge (a, b); it is parked one step later
+  __device__ __forceinline__ void load(uint32_t a, uint32_t b) {
+    if (active && lane == 0) pending = __ldg(dist + (size_t)a * n + b);
+  }
+  __device__ __forceinline__ void push() {
+    if (!active) return;
+    if (lane == 0) buf[i] = pending;
+    if (++i == len) {
+      if (lane == 0) leaf_sum[L] = pw_leaf_sum(len, [&](int q) { return buf[q]; });
+      __syncwarp();
+      const bool more = leaves[L].x + len < n;  // leaves tile [0, n) exactly
+      ++L;
+      if (more) {
+        len = leaves[L].y;
+        i = 0;
+      }
+    }
+  }
+  __device__ __forceinline__ double finish() {
+    __syncwarp();
+    return pw_fold(n, leaf_sum);  // meaningful in lane 0
+  }
+};
+
+// per-ant shared scratch: leaf buffer, leaf sums, visited bitmask (16-B aligned)
+__host__ __device__ __forceinline__ size_t ant_scratch_bytes(int n_leaves, int nwords) {
+  return ((size_t)8 * kPwBlock + (size_t)8 * n_leaves + (size_t)4 * nwords + 15) & ~(size_t)15;
+}
+
 __device__ __forceinline__ bool is_visited(const uint32_t *vis, uint32_t j) {
   return (vis[j >> 5] >> (j & 31)) & 1u;
 }
 
-template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    k_construct_sorted(int n, int m_local, int ant_offset, const float *__restrict__ sw,
-                       const uint16_t *__restrict__ si, uint32_t k0, uint32_t k1, uint32_t iteration,
-                       int32_t *__restrict__ tours, int32_t *status, int nwords,
-                       unsigned long long *scan_count) {
-  extern __shared__ uint32_t vis_all[];
+__device__ __forceinline__ uint32_t score_key(float w, uint32_t j, int step, uint32_t gant, uint32_t iteration,
+                                              const PhiloxKeys &ks) {
+  const U4 r = philox4x32_10(U4{j >> 2, (uint32_t)step, gant, iteration}, ks);
+  return __float_as_uint(__fmul_rn(w, bits_to_uniform(word_of(r, j & 3)))) + 1u;
+}
+
+// candidate key of table entry (w, j): (bits(w * u) + 1) or 0 when excluded
+__device__ __forceinline__ uint32_t entry_key(float w, uint32_t j, float best, const uint32_t *vis, int step,
+                                              uint32_t gant, uint32_t iteration, const PhiloxKeys &ks) {
+  if (!(w > 0.0f && w >= best) || is_visited(vis, j)) return 0u;
+  return score_key(w, j, step, gant, iteration, ks);
+}
+
+// Shared-memory layout of the sorted kernel (dynamic):
+//   float  cache_w[n * T]    first T entries of every sorted row
+//   uint16 cache_i[n * T]
+//   int2   leaves[n_leaves]
+//   per ant: double leaf_buf[kPwBlock], double leaf_sum[n_leaves], uint32 vis[nwords]
+struct SortedArgs {
+  int n, m_local, ant_offset, T, nwords, n_leaves;
+  const float *sw;
+  const uint16_t *si;
+  const double *dist;
+  uint32_t iteration;
+  int32_t *tours;
+  double *costs;
+  int32_t *status;
+  unsigned long long *scan_count;
+  PhiloxKeys ks;
+};
+
+constexpr int kSortedMaxWarps = 28;
+
+__global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const __grid_constant__ SortedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n, T = a.T;
+  float *cache_w = reinterpret_cast<float *>(smem);
+  uint16_t *cache_i = reinterpret_cast<uint16_t *>(smem + (size_t)4 * n * T);
+  size_t off = ((size_t)6 * n * T + 15) & ~(size_t)15;
+  int2 *leaves = reinterpret_cast<int2 *>(smem + off);
+  off += ((size_t)8 * a.n_leaves + 15) & ~(size_t)15;
+  const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int ant = blockIdx.x * WARPS + warp;
-  if (ant >= m_local) return;
-  const uint32_t gant = (uint32_t)(ant_offset + ant);
-  uint32_t *vis = vis_all + (size_t)warp * nwords;
-  for (int w = lane; w < nwords; w += 32) vis[w] = 0u;
-  const uint32_t start = start_city((uint32_t)n, gant, iteration, k0, k1);
+  const size_t per_ant = ant_scratch_bytes(a.n_leaves, a.nwords);
+  unsigned char *mine = smem + off + per_ant * warp;
+  double *leaf_buf = reinterpret_cast<double *>(mine);
+  double *leaf_sum = leaf_buf + kPwBlock;
+  uint32_t *vis = reinterpret_cast<uint32_t *>(leaf_sum + a.n_leaves);
+
+  // stage the head of every row (written by k_row_update this iteration)
+  for (int idx = threadIdx.x; idx < n * T; idx += blockDim.x) {
+    const int row = idx / T, t = idx - row * T;
+    cache_w[idx] = __ldg(a.sw + (size_t)row * n + t);
+    cache_i[idx] = __ldg(a.si + (size_t)row * n + t);
+  }
+  if (threadIdx.x == 0) pw_leaves(n, leaves);
+  __syncthreads();
+
+  const int ant = blockIdx.x * warps + warp;
+  if (ant >= a.m_local) return;
+  const uint32_t gant = (uint32_t)(a.ant_offset + ant);
+  const uint32_t it = a.iteration;
+  for (int w = lane; w < a.nwords; w += 32) vis[w] = 0u;
+  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, (uint32_t)n);
   __syncwarp();
   if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
   __syncwarp();
 
-  TourWriter tw{tours + (size_t)ant * n, n, lane, 0};
+  TourWriter tw{a.tours + (size_t)ant * n, n, lane, 0};
   tw.put(0, (int32_t)start);
+  LeafCost lc;
+  lc.init(a.costs != nullptr ? a.dist : nullptr, leaves, leaf_buf, leaf_sum, n, lane);
   uint32_t cur = start;
-  unsigned long long windows = 0;  // 32-entry table windows read (traffic probe)
+  unsigned long long windows = 0;  // 32-entry global windows read (traffic probe)
   for (int step = 1; step < n; ++step) {
-    const float *wr = sw + (size_t)cur * n;
-    const uint16_t *ir = si + (size_t)cur * n;
+    // speculative load of the first global window: in flight while the row
+    // head is scored from shared memory
+    const float *wrow = a.sw + (size_t)cur * n;
+    const uint16_t *irow = a.si + (size_t)cur * n;
+    float wg = 0.0f;
+    uint32_t jg = 0;
+    if (T + lane < n) {
+      wg = __ldg(wrow + T + lane);
+      jg = __ldg(irow + T + lane);
+    }
     float best = -1.0f;
     uint32_t bestj = 0xffffffffu;
-    for (int base = 0; base < n; base += 32) {
-      const int e = base + lane;
+    bool done = false;
+    if (T > 0) {  // window 0: the row head from shared memory
       float w = 0.0f;
       uint32_t j = 0;
-      if (e < n) {
-        w = __ldg(wr + e);
-        j = __ldg(ir + e);
+      if (lane < T) {
+        w = cache_w[cur * T + lane];
+        j = cache_i[cur * T + lane];
       }
-      uint32_t key = 0u;
-      if (w > 0.0f && w >= best && !is_visited(vis, j)) {
-        const U4 r = philox4x32_10(U4{j >> 2, (uint32_t)step, gant, iteration}, k0, k1);
-        const float s = __fmul_rn(w, bits_to_uniform(word_of(r, j & 3)));
-        key = __float_as_uint(s) + 1u;
-      }
+      const bool vis_j = is_visited(vis, j);  // issued alongside the Philox chain
+      uint32_t key = score_key(w, j, step, gant, it, a.ks);
+      if (!(w > 0.0f) || vis_j) key = 0u;
       const uint32_t mkey = __reduce_max_sync(kFull, key);
       if (mkey != 0u) {
-        const uint32_t jmin = __reduce_min_sync(kFull, key == mkey ? j : 0xffffffffu);
+        bestj = __reduce_min_sync(kFull, key == mkey ? j : 0xffffffffu);
+        best = __uint_as_float(mkey - 1u);
+      }
+      const float wl = __shfl_sync(kFull, w, T - 1);
+      done = (wl < best || wl <= 0.0f);
+    }
+    for (int base = T; !done && base < n; base += 32) {
+      if (base != T) {
+        wg = 0.0f;
+        jg = 0;
+        if (base + lane < n) {
+          wg = __ldg(wrow + base + lane);
+          jg = __ldg(irow + base + lane);
+        }
+      }
+      const uint32_t key = entry_key(wg, jg, best, vis, step, gant, it, a.ks);
+      const uint32_t mkey = __reduce_max_sync(kFull, key);
+      if (mkey != 0u) {
+        const uint32_t jmin = __reduce_min_sync(kFull, key == mkey ? jg : 0xffffffffu);
         const float sc = __uint_as_float(mkey - 1u);
         if (sc > best || (sc == best && jmin < bestj)) {
           best = sc;
@@ -98,46 +239,76 @@ __global__ void __launch_bounds__(WARPS * 32)
       }
       ++windows;
       // entries after this window have W <= the window's last W
-      const float wl = __shfl_sync(kFull, w, 31);
-      if (wl < best || wl <= 0.0f) break;
+      const float wl = __shfl_sync(kFull, wg, 31);
+      done = (wl < best || wl <= 0.0f);
     }
     if (bestj == 0xffffffffu) {
-      if (lane == 0) record_status(status, TACO_NO_CANDIDATE, (int)gant);
+      if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
       return;
     }
     if (lane == 0) vis[bestj >> 5] |= 1u << (bestj & 31);
+    if (step > 1) lc.push();  // edge step-2, loaded one step ago
+    lc.load(cur, bestj);      // edge step-1
     __syncwarp();
     tw.put(step, (int32_t)bestj);
     cur = bestj;
   }
   tw.flush();
-  if (scan_count != nullptr && lane == 0) atomicAdd(scan_count, windows);
+  if (lc.active) {
+    lc.push();  // edge n-2
+    lc.load(cur, start);
+    lc.push();  // closing edge n-1
+    const double c = lc.finish();
+    if (lane == 0) a.costs[ant] = c;
+  }
+  if (a.scan_count != nullptr && lane == 0) atomicAdd(a.scan_count, windows);
 }
 
+struct DenseArgs {
+  int n, m_local, ant_offset, ldw, nwords, n_leaves;
+  const float *w;
+  const double *dist;
+  uint32_t iteration;
+  int32_t *tours;
+  double *costs;
+  int32_t *status;
+  PhiloxKeys ks;
+};
+
+// Shared memory: int2 leaves[n_leaves]; per ant: double leaf_buf[kPwBlock],
+// double leaf_sum[n_leaves], uint32 vis[nwords]
 template <int WARPS>
-__global__ void __launch_bounds__(WARPS * 32)
-    k_construct_dense(int n, int m_local, int ant_offset, const float *__restrict__ w, int ldw,
-                      uint32_t k0, uint32_t k1, uint32_t iteration, int32_t *__restrict__ tours,
-                      int32_t *status, int nwords) {
-  extern __shared__ uint32_t vis_all[];
+__global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_constant__ DenseArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n;
+  int2 *leaves = reinterpret_cast<int2 *>(smem);
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
+  const size_t per_ant = ant_scratch_bytes(a.n_leaves, a.nwords);
+  unsigned char *mine = smem + (((size_t)8 * a.n_leaves + 15) & ~(size_t)15) + per_ant * warp;
+  double *leaf_buf = reinterpret_cast<double *>(mine);
+  double *leaf_sum = leaf_buf + kPwBlock;
+  uint32_t *vis = reinterpret_cast<uint32_t *>(leaf_sum + a.n_leaves);
+  if (threadIdx.x == 0) pw_leaves(n, leaves);
+  __syncthreads();
   const int ant = blockIdx.x * WARPS + warp;
-  if (ant >= m_local) return;
-  const uint32_t gant = (uint32_t)(ant_offset + ant);
-  uint32_t *vis = vis_all + (size_t)warp * nwords;
-  for (int q = lane; q < nwords; q += 32) vis[q] = 0u;
-  const uint32_t start = start_city((uint32_t)n, gant, iteration, k0, k1);
+  if (ant >= a.m_local) return;
+  const uint32_t gant = (uint32_t)(a.ant_offset + ant);
+  const uint32_t it = a.iteration;
+  for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
+  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, (uint32_t)n);
   __syncwarp();
   if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
   __syncwarp();
 
-  TourWriter tw{tours + (size_t)ant * n, n, lane, 0};
+  TourWriter tw{a.tours + (size_t)ant * n, n, lane, 0};
   tw.put(0, (int32_t)start);
+  LeafCost lc;
+  lc.init(a.costs != nullptr ? a.dist : nullptr, leaves, leaf_buf, leaf_sum, n, lane);
   uint32_t cur = start;
   const int nq = (n + 3) >> 2;
   for (int step = 1; step < n; ++step) {
-    const float4 *row = reinterpret_cast<const float4 *>(w + (size_t)cur * ldw);
+    const float4 *row = reinterpret_cast<const float4 *>(a.w + (size_t)cur * a.ldw);
     uint32_t lkey = 0u, lj = 0xffffffffu;
 #pragma unroll 4
     for (int q = lane; q < nq; q += 32) {
@@ -145,7 +316,7 @@ __global__ void __launch_bounds__(WARPS * 32)
       const uint32_t nib = (vis[q >> 3] >> ((q & 7) * 4)) & 0xfu;
       const bool any = (nib != 0xfu) && (wv.x > 0.0f || wv.y > 0.0f || wv.z > 0.0f || wv.w > 0.0f);
       if (any) {
-        const U4 r = philox4x32_10(U4{(uint32_t)q, (uint32_t)step, gant, iteration}, k0, k1);
+        const U4 r = philox4x32_10(U4{(uint32_t)q, (uint32_t)step, gant, it}, a.ks);
         const float wc[4] = {wv.x, wv.y, wv.z, wv.w};
         const uint32_t rc[4] = {r.x, r.y, r.z, r.w};
 #pragma unroll
@@ -163,16 +334,25 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
     const uint32_t mkey = __reduce_max_sync(kFull, lkey);
     if (mkey == 0u) {
-      if (lane == 0) record_status(status, TACO_NO_CANDIDATE, (int)gant);
+      if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
       return;
     }
     const uint32_t bestj = __reduce_min_sync(kFull, lkey == mkey ? lj : 0xffffffffu);
     if (lane == 0) vis[bestj >> 5] |= 1u << (bestj & 31);
+    if (step > 1) lc.push();
+    lc.load(cur, bestj);
     __syncwarp();
     tw.put(step, (int32_t)bestj);
     cur = bestj;
   }
   tw.flush();
+  if (lc.active) {
+    lc.push();
+    lc.load(cur, start);
+    lc.push();
+    const double c = lc.finish();
+    if (lane == 0) a.costs[ant] = c;
+  }
 }
 
 __global__ void k_starts(int n, int m_local, int ant_offset, uint32_t k0, uint32_t k1,
@@ -252,28 +432,79 @@ static inline void split_seed(uint64_t seed, uint32_t *k0, uint32_t *k1) {
   *k1 = (uint32_t)(seed >> 32);
 }
 
+static int sm_count() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
+      cached = 148;
+  }
+  return cached;
+}
+
+static int set_smem(const void *fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return TACO_OK;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) {
+    note_cuda_error(e);
+    return TACO_ERR_CUDA;
+  }
+  return TACO_OK;
+}
+
+constexpr size_t kSmemBudget = 200 * 1024;
+
 extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, const float *w, int ldw,
                               const float *sw, const uint16_t *si, uint64_t seed, uint32_t iteration,
-                              int32_t *tours_out, int32_t *status, unsigned long long *scan_count,
-                              void *stream) {
+                              const double *dist, int32_t *tours_out, double *costs_out, int32_t *status,
+                              unsigned long long *scan_count, void *stream) {
   if (n < 3 || n > 65535 || m_local < 0 || ant_offset < 0 || tours_out == nullptr) return TACO_ERR_ARG;
+  if (costs_out != nullptr && dist == nullptr) return TACO_ERR_ARG;
   if (m_local == 0) return TACO_OK;
-  uint32_t k0, k1;
-  split_seed(seed, &k0, &k1);
+  const PhiloxKeys ks = philox_keys(seed);
   const int nwords = (n + 31) / 32;
+  const int n_leaves = pw_num_leaves(n);
+  const size_t per_ant = ant_scratch_bytes(n_leaves, nwords);
+  const size_t leaves_bytes = ((size_t)8 * n_leaves + 15) & ~(size_t)15;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  constexpr int WARPS = 4;
-  const int grid = (m_local + WARPS - 1) / WARPS;
-  const size_t smem = (size_t)WARPS * nwords * sizeof(uint32_t);
   if (variant == TACO_CONSTRUCT_SORTED) {
     if (sw == nullptr || si == nullptr) return TACO_ERR_ARG;
-    k_construct_sorted<WARPS><<<grid, WARPS * 32, smem, s>>>(n, m_local, ant_offset, sw, si, k0, k1, iteration,
-                                                             tours_out, status, nwords, scan_count);
+    // one CTA per SM when the colony allows it: the row-head cache is staged
+    // once per CTA.  Knobs (tuning only): TACO_SORTED_WARPS, TACO_SORTED_T.
+    int warps = (m_local + sm_count() - 1) / sm_count();
+    warps = warps < 1 ? 1 : (warps > kSortedMaxWarps ? kSortedMaxWarps : warps);
+    if (const char *ev = getenv("TACO_SORTED_WARPS")) warps = atoi(ev);
+    if (warps < 1 || warps > kSortedMaxWarps) return TACO_ERR_ARG;
+    const size_t fixed = leaves_bytes + per_ant * warps;
+    int T = 0;
+    for (int cand : {16, 8, 4, 2}) {
+      if (cand < n && fixed + (((size_t)6 * n * cand + 15) & ~(size_t)15) <= kSmemBudget) {
+        T = cand;
+        break;
+      }
+    }
+    // With > ~20 ants per SM the kernel is issue-bound and the extra shared
+    // window costs more than the L2 latency it hides (measured crossover at
+    // m ~ 3000 on 148 SMs, n = 2392; profiles/README.md).
+    if (m_local > 20 * sm_count()) T = 0;
+    if (const char *ev = getenv("TACO_SORTED_T")) T = atoi(ev);
+    if (T < 0 || T > 32 || T >= n) return TACO_ERR_ARG;
+    const size_t smem = (((size_t)6 * n * T + 15) & ~(size_t)15) + fixed;
+    if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
+    SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, sw, si, dist, iteration,
+                 tours_out, costs_out, status, scan_count, ks};
+    if (set_smem((const void *)k_construct_sorted, smem) != TACO_OK) return TACO_ERR_CUDA;
+    k_construct_sorted<<<(m_local + warps - 1) / warps, warps * 32, smem, s>>>(a);
   } else if (variant == TACO_CONSTRUCT_DENSE) {
     if (w == nullptr || ldw < n || (ldw % 4) != 0) return TACO_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(w) & 15u) != 0) return TACO_ERR_ARG;
-    k_construct_dense<WARPS><<<grid, WARPS * 32, smem, s>>>(n, m_local, ant_offset, w, ldw, k0, k1, iteration,
-                                                            tours_out, status, nwords);
+    constexpr int WARPS = 4;
+    const size_t smem = leaves_bytes + per_ant * WARPS;
+    if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
+    if (set_smem((const void *)k_construct_dense<WARPS>, smem) != TACO_OK) return TACO_ERR_CUDA;
+    DenseArgs a{n, m_local, ant_offset, ldw, nwords, n_leaves, w, dist, iteration, tours_out, costs_out, status, ks};
+    k_construct_dense<WARPS><<<(m_local + WARPS - 1) / WARPS, WARPS * 32, smem, s>>>(a);
   } else {
     return TACO_ERR_ARG;
   }

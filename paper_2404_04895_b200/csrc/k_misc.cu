@@ -40,6 +40,24 @@ __global__ void __launch_bounds__(WARPS * 32)
   if (lane == 0) costs[a] = pw_fold(n, ls);
 }
 
+// Stable rank by counting for small colonies: rank(a) = #{b : c_b < c_a} +
+// #{b < a : c_b == c_a}; order[rank(a)] = a.  Every CTA stages all m costs in
+// shared memory; one thread per ant.  Exact np.argsort(kind="stable").
+constexpr int kRankMaxM = 16384;
+
+__global__ void __launch_bounds__(256) k_elite_rank(int m, const double *__restrict__ costs, int32_t *order) {
+  extern __shared__ unsigned long long keys[];
+  for (int b = threadIdx.x; b < m; b += blockDim.x) keys[b] = (unsigned long long)__double_as_longlong(costs[b]);
+  __syncthreads();
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  const unsigned long long ka = keys[a];
+  int rank = 0;
+  for (int b = 0; b < a; ++b) rank += keys[b] <= ka;  // earlier ants win ties
+  for (int b = a + 1; b < m; ++b) rank += keys[b] < ka;
+  order[rank] = a;
+}
+
 __global__ void k_cost_keys(int m, const double *costs, unsigned long long *keys, int32_t *vals) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a < m) {
@@ -133,13 +151,23 @@ extern "C" int taco_tour_cost(int n, int m, const void *tours, int tours_is_i64,
 }
 
 extern "C" size_t taco_elite_workspace_bytes(int m) {
-  if (m < 1) return 0;
+  if (m <= kRankMaxM) return 0;  // counting-rank kernel needs no workspace
   return align256((size_t)m * 8) * 2 + align256((size_t)m * 4) + align256(cub_temp_bytes(m));
 }
 
 extern "C" int taco_elite_order(int m, const double *costs, int32_t *order_out, void *workspace, size_t ws_bytes,
                                 void *stream) {
   if (m < 1 || costs == nullptr || order_out == nullptr) return TACO_ERR_ARG;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (m <= kRankMaxM) {
+    const size_t smem = (size_t)m * 8;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(k_elite_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return TACO_ERR_CUDA;
+    k_elite_rank<<<(m + 255) / 256, 256, smem, st>>>(m, costs, order_out);
+    TACO_CUDA_CHECK_LAUNCH();
+    return TACO_OK;
+  }
   if (ws_bytes < taco_elite_workspace_bytes(m) || workspace == nullptr) return TACO_ERR_ARG;
   unsigned char *ws = reinterpret_cast<unsigned char *>(workspace);
   auto *keys_in = reinterpret_cast<unsigned long long *>(ws);
@@ -195,6 +223,15 @@ extern "C" int taco_log_weights(int64_t count, const double *p, double gamma, do
   k_log_weights<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(count, p, gamma, logw_out);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
+}
+
+namespace taco {
+static thread_local cudaError_t g_last_cuda_error = cudaSuccess;
+void note_cuda_error(cudaError_t e) { g_last_cuda_error = e; }
+}  // namespace taco
+
+extern "C" const char *taco_last_cuda_error(void) {
+  return taco::g_last_cuda_error == cudaSuccess ? "" : cudaGetErrorString(taco::g_last_cuda_error);
 }
 
 extern "C" int taco_abi_version(void) { return TACO_ABI_VERSION; }

@@ -36,13 +36,47 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
   return c;
 }
 
+// Precomputed key schedule (k + r*W for r = 0..9).  Passed by value inside
+// kernel parameter structs, so after unrolling every round key is a
+// constant-bank operand of the LOP3: no registers, no per-call key adds.
+struct PhiloxKeys {
+  uint32_t k0[10], k1[10];
+};
+
+inline PhiloxKeys philox_keys(uint64_t seed) {
+  PhiloxKeys s;
+  uint32_t a = (uint32_t)(seed & 0xffffffffu), b = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    s.k0[r] = a;
+    s.k1[r] = b;
+    a += kPhiloxW0;
+    b += kPhiloxW1;
+  }
+  return s;
+}
+
+__device__ __forceinline__ U4 philox4x32_10(U4 c, const PhiloxKeys &ks) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = kPhiloxM0 * c.x;
+    const uint32_t hi0 = __umulhi(kPhiloxM0, c.x);
+    const uint32_t lo1 = kPhiloxM1 * c.z;
+    const uint32_t hi1 = __umulhi(kPhiloxM1, c.z);
+    c = U4{hi1 ^ c.y ^ ks.k0[r], lo1, hi0 ^ c.w ^ ks.k1[r], lo0};
+  }
+  return c;
+}
+
 // The device construction stream:
 //   key     = (seed & 0xffffffff, seed >> 32)
 //   counter = (city >> 2, step, ant, iteration)      selection, step >= 1
 //   counter = (0, 0, ant, iteration), word 0         start city (step 0)
 //   u       = ((x >> 9) + 0.5) * 2^-23  in (0, 1), exact in fp32
 __device__ __forceinline__ float bits_to_uniform(uint32_t x) {
-  return __fmaf_rn(__uint2float_rn(x >> 9), 0x1p-23f, 0x1p-24f);
+  // 1 + k 2^-23 (k = x >> 9) built from bits, minus (1 - 2^-24): both steps
+  // exact (Sterbenz), so u = (k + 1/2) 2^-23 without an int->float conversion
+  // (conversions run on the quarter-rate XU pipe)
+  return __fsub_rn(__uint_as_float(0x3f800000u | (x >> 9)), 0x1.fffffep-1f);
 }
 
 __device__ __forceinline__ uint32_t lemire_bound(uint32_t x, uint32_t n) {
@@ -199,8 +233,16 @@ __device__ inline double pw_fold(int n, const double *leaf_sum) {
 
 }  // namespace taco
 
+namespace taco {
+// last CUDA error seen by a libtaco entry point (taco_last_cuda_error)
+void note_cuda_error(cudaError_t e);
+}  // namespace taco
+
 #define TACO_CUDA_CHECK_LAUNCH()                              \
   do {                                                        \
     cudaError_t e_ = cudaGetLastError();                      \
-    if (e_ != cudaSuccess) return TACO_ERR_CUDA;              \
+    if (e_ != cudaSuccess) {                                  \
+      taco::note_cuda_error(e_);                              \
+      return TACO_ERR_CUDA;                                   \
+    }                                                         \
   } while (0)

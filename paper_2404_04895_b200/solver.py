@@ -8,8 +8,9 @@ The reference has no solver object; its iteration is the loop body of
 The Solver runs exactly that sequence per ``step()`` with all state resident in
 HBM and five kernel launches per iteration:
 
-    1. taco_construct        tours (m x n int32) from the fp32 selection table
-    2. taco_tour_cost        tour lengths, numpy pairwise order
+    1. taco_construct        tours (m x n int32) from the fp32 selection table,
+                             with their lengths accumulated on the fly in
+                             numpy's pairwise order
        [multi-GPU: all-gather of tours + lengths over NCCL]
     3. taco_elite_order      stable radix argsort of the lengths
     4. taco_track_best       best-so-far tour / length on device
@@ -157,9 +158,9 @@ class Solver:
         ev = _Timer(timers)
         ev.start("construct")
         _device.construct(self.n, sh.count, sh.offset, self._variant, self.tables, p.seed, it,
-                          self.tours_local, self.status, scan_count)
+                          self.tours_local, self.status, scan_count, dist=self.di.dist,
+                          costs_out=self.costs_local)
         ev.stop("construct")
-        _device.tour_cost(self.tours_local[:sh.count], self.di.dist, self.costs_local[:sh.count])
         if sh.world > 1:
             gather_colony(self.tours_local, self.costs_local, sh, self.tours_all, self.costs_all,
                           self.group, self._pad_tours, self._pad_costs)

@@ -119,7 +119,8 @@ def _device_tables(p, gamma):
     return t
 
 
-@pytest.mark.parametrize("n,m,gamma", [(7, 5, 1.0), (40, 33, 1.0), (97, 64, 1.37), (300, 40, 1.5)])
+@pytest.mark.parametrize("n,m,gamma", [(3, 4, 1.0), (7, 5, 1.0), (40, 33, 1.0), (97, 64, 1.37),
+                                         (300, 40, 1.5), (700, 150, 1.2)])
 def test_fast_construction_matches_restatement(n, m, gamma):
     inst = euclid(n, n)
     g = np.random.default_rng(n)
@@ -136,12 +137,16 @@ def test_fast_construction_matches_restatement(n, m, gamma):
     assert (np.diff(sw, axis=1) <= 0).all()
     seed, it = 11, 5
     want = fastpath.build_tours(w, seed, it, np.arange(m))
+    dist = _device.upload(inst.dist, t.w.device)
     for variant in (_lib.CONSTRUCT_SORTED, _lib.CONSTRUCT_DENSE):
         tours = torch.zeros((m, n), dtype=torch.int32, device=t.w.device)
+        costs = torch.zeros(m, dtype=torch.float64, device=t.w.device)
         status = _device.new_status(t.w.device)
-        _device.construct(n, m, 0, variant, t, seed, it, tours, status)
+        _device.construct(n, m, 0, variant, t, seed, it, tours, status, dist=dist, costs_out=costs)
         assert _device.read_status(status)[0] == 0
         assert np.array_equal(tours.cpu().numpy(), want), variant
+        # lengths accumulated during construction == numpy's pairwise batch_costs
+        assert np.array_equal(costs.cpu().numpy(), ref.lengths(want, inst.dist)), variant
 
 
 def test_fast_rule_agrees_with_reference_log_rule():
@@ -205,11 +210,14 @@ def test_select_elite_ties_and_bounds():
     with pytest.raises(ValueError):
         taco.select_elite(b, 0)
     g = np.random.default_rng(1)
-    costs = g.integers(0, 50, 5000).astype(np.float64)  # many ties
-    order = np.argsort(costs, kind="stable")
-    batch = taco.TourBatch(tours=np.zeros((5000, 3), dtype=np.int64) + np.arange(3), costs=costs)
-    got = [c for _, c in taco.select_elite(batch, 5000)]
-    assert got == costs[order].tolist()
+    for m in (5000, 20000):  # counting-rank kernel and the CUB radix path
+        costs = g.integers(0, 50, m).astype(np.float64) + 0.25  # many ties
+        order = np.argsort(costs, kind="stable")
+        batch = taco.TourBatch(tours=np.zeros((m, 3), dtype=np.int64) + np.arange(3), costs=costs)
+        dev = _device.device()
+        got = _device.download(_device.elite_order(_device.upload(costs, dev), _device.EliteWorkspace(m, dev)))
+        assert np.array_equal(got, order)
+        assert [c for _, c in taco.select_elite(batch, 7)] == costs[order[:7]].tolist()
 
 
 def test_accumulate_matches_reference_with_duplicates():
