@@ -68,30 +68,36 @@ class ClockSampler:
     def __init__(self, gpu: int):
         self.gpu = gpu
         self.rows: list[list[str]] = []
-        self._stop = threading.Event()
+        self._proc = None
         self._thread = None
 
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                for line in out.strip().splitlines():
-                    self.rows.append([c.strip() for c in line.split(",")])
-            except Exception:  # noqa: BLE001 - sampling is best effort
-                pass
-            self._stop.wait(0.2)
+    def _reader(self):
+        for line in self._proc.stdout:
+            parts = [c.strip() for c in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
 
     def __enter__(self):
-        self._thread = threading.Thread(target=self._run, daemon=True)
-        self._thread.start()
+        try:  # one long-lived nvidia-smi polling every 100 ms during the timed region
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._thread = threading.Thread(target=self._reader, daemon=True)
+            self._thread.start()
+        except OSError:
+            self._proc = None
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
         if self._thread is not None:
-            self._thread.join(timeout=10)
+            self._thread.join(timeout=5)
 
     def summary(self) -> dict:
         if not self.rows:
@@ -168,6 +174,10 @@ def run_ours(args) -> dict | None:
     del warm
     _device._INSTANCES.clear()
     torch.cuda.synchronize()
+    # clocks are sampled over both timed regions (e2e + device), ~100 ms apart
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
     _barrier(world)
     t0 = time.perf_counter()
     e2e_solver = taco.Solver(e2e_inst, params, construct=args.construct)
@@ -186,9 +196,6 @@ def run_ours(args) -> dict | None:
     timers = {"construct": [], "update": []}
     scan = torch.zeros(1, dtype=torch.int64, device=dev)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    sampler = ClockSampler(local) if rank == 0 else None
-    if sampler:
-        sampler.__enter__()
     _barrier(world)
     torch.cuda.synchronize()
     start.record()
