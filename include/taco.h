@@ -57,20 +57,21 @@ int taco_max_sorted_n(void);
 /*
  * Fused row kernel: evaporation + index-mapped deposit + P = RowNorm(tau^a eta^b)
  * + the fp32 selection table W = P^(1/gamma) (dense and/or row-sorted).
- * One CTA per row.  Replaces, in one pass over tau:
+ * Persistent CTAs, one row at a time.  Replaces, in one pass over tau:
  *   pheromone.accumulate_increments   pheromone.py:52-68   (delta source)
  *   pheromone.apply_update            pheromone.py:71-83   (do_evap != 0)
  *   colony.compute_probability_matrix colony.py:51-69      (p_out / rowsum_out)
  *   selection.scaled_log_weights      selection.py:62-75   (folded into W)
  *
- * Delta source (at most one): nbr+inc (k elites; nbr[r*n + i] = (prev, next)
+ * Delta source (at most one): nbr+inc (k elites; nbr[i*k + r] = (prev, next)
  * of city i in elite r's tour, inc[r] = 1/cost_r, rank order r = 0..k-1) or a
  * dense delta_in (n x n).  With neither, delta = 0.
  * tau' = max(keep*tau + delta, 1e-12) when do_evap, else tau' = tau_in.
  * eta_b = eta^beta (precomputed once per instance, n x n).
  * Outputs (each nullable): delta_out, tau_out (may alias tau_in), p_out,
  * rowsum_out (n), w_out (n x ldw fp32, pad columns zeroed), sw_out/si_out
- * (n x n fp32 values / uint16 column indices, each row sorted descending).
+ * (n x n fp32 values / uint16 column indices, each row sorted descending by
+ * the W bits above bit 16, stable in the column index).
  * eta_b / p outputs are skipped when want_p == 0 (delta/tau-only modes).
  */
 int taco_row_update(int n,
@@ -170,7 +171,7 @@ int taco_elite_order(int m, const double *costs, int32_t *order_out,
                      void *workspace, size_t ws_bytes, void *stream);
 
 /*
- * Elite edge map for the fused deposit: nbr[r*n + t[s]] = (t[s-1], t[s+1])
+ * Elite edge map for the fused deposit: nbr[t[s]*k + r] = (t[s-1], t[s+1])
  * and inc[r] = 1.0 / cost of elite r = order[r] (pheromone.py:52-68,
  * edge_index_matrix pheromone.py:28-38).  tours int32 (ld = n) or int64.
  */

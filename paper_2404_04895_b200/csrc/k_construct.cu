@@ -144,9 +144,36 @@ struct SortedArgs {
 
 constexpr int kSortedMaxWarps = 28;
 
+// Score the 32-entry window (w, j) of the sorted row against the running
+// (best, bestj).  Warp-uniform control flow: the Philox chain runs once per
+// window for all lanes iff any lane holds a candidate (unvisited, W > 0,
+// W >= best); a window without candidates costs one shared load per lane.
+__device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t *vis, uint32_t step,
+                                             uint32_t gant, uint32_t it, const PhiloxKeys &ks, float &best,
+                                             uint32_t &bestj) {
+  const uint32_t vw = vis[j >> 5];
+  const bool cand = (w > 0.0f) && (w >= best) && !((vw >> (j & 31)) & 1u);
+  if (__any_sync(kFull, cand)) {
+    const U4 r = philox4x32_10(U4{j >> 2, step, gant, it}, ks);
+    const uint32_t x = word_of(r, j & 3);
+    const uint32_t key = cand ? __float_as_uint(__fmul_rn(w, bits_to_uniform(x))) + 1u : 0u;
+    const uint32_t mkey = __reduce_max_sync(kFull, key);
+    if (mkey != 0u) {
+      const uint32_t jmin = __reduce_min_sync(kFull, key == mkey ? j : 0xffffffffu);
+      const float sc = __uint_as_float(mkey - 1u);
+      if (sc > best || (sc == best && jmin < bestj)) {
+        best = sc;
+        bestj = jmin;
+      }
+    }
+  }
+}
+
+template <bool HEAD, bool PROBE>
 __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const __grid_constant__ SortedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int n = a.n, T = a.T;
+  const int n = a.n;
+  const int T = HEAD ? a.T : 0;
   float *cache_w = reinterpret_cast<float *>(smem);
   uint16_t *cache_i = reinterpret_cast<uint16_t *>(smem + (size_t)4 * n * T);
   size_t off = ((size_t)6 * n * T + 15) & ~(size_t)15;
@@ -155,17 +182,17 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const size_t per_ant = ant_scratch_bytes(a.n_leaves, a.nwords);
-  unsigned char *mine = smem + off + per_ant * warp;
+  unsigned char *mine = smem + off + ant_scratch_bytes(a.n_leaves, a.nwords) * warp;
   double *leaf_buf = reinterpret_cast<double *>(mine);
   double *leaf_sum = leaf_buf + kPwBlock;
   uint32_t *vis = reinterpret_cast<uint32_t *>(leaf_sum + a.n_leaves);
 
-  // stage the head of every row (written by k_row_update this iteration)
-  for (int idx = threadIdx.x; idx < n * T; idx += blockDim.x) {
-    const int row = idx / T, t = idx - row * T;
-    cache_w[idx] = __ldg(a.sw + (size_t)row * n + t);
-    cache_i[idx] = __ldg(a.si + (size_t)row * n + t);
+  if (HEAD) {  // stage the head of every row (written by k_row_update this iteration)
+    for (int idx = threadIdx.x; idx < n * T; idx += blockDim.x) {
+      const int row = idx / T, t = idx - row * T;
+      cache_w[idx] = __ldg(a.sw + (size_t)row * n + t);
+      cache_i[idx] = __ldg(a.si + (size_t)row * n + t);
+    }
   }
   if (threadIdx.x == 0) pw_leaves(n, leaves);
   __syncthreads();
@@ -174,8 +201,11 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   if (ant >= a.m_local) return;
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.iteration;
-  for (int w = lane; w < a.nwords; w += 32) vis[w] = 0u;
-  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, (uint32_t)n);
+  const uint32_t un = (uint32_t)n;  // n <= 65535, so every row offset fits in 32 bits
+  const float *__restrict__ sw = a.sw;
+  const uint16_t *__restrict__ si = a.si;
+  for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
+  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, un);
   __syncwarp();
   if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
   __syncwarp();
@@ -186,61 +216,48 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   lc.init(a.costs != nullptr ? a.dist : nullptr, leaves, leaf_buf, leaf_sum, n, lane);
   uint32_t cur = start;
   unsigned long long windows = 0;  // 32-entry global windows read (traffic probe)
-  for (int step = 1; step < n; ++step) {
-    // speculative load of the first global window: in flight while the row
-    // head is scored from shared memory
-    const float *wrow = a.sw + (size_t)cur * n;
-    const uint16_t *irow = a.si + (size_t)cur * n;
+  for (uint32_t step = 1; step < un; ++step) {
+    const uint32_t row = cur * un;
+    // first global window: issued before the row head is scored, so its L2
+    // latency overlaps the shared-memory work
+    uint32_t e = (uint32_t)T + lane;
     float wg = 0.0f;
     uint32_t jg = 0;
-    if (T + lane < n) {
-      wg = __ldg(wrow + T + lane);
-      jg = __ldg(irow + T + lane);
+    if (e < un) {
+      wg = __ldg(sw + (row + e));
+      jg = __ldg(si + (row + e));
     }
     float best = -1.0f;
     uint32_t bestj = 0xffffffffu;
     bool done = false;
-    if (T > 0) {  // window 0: the row head from shared memory
+    if (HEAD) {
       float w = 0.0f;
       uint32_t j = 0;
       if (lane < T) {
         w = cache_w[cur * T + lane];
         j = cache_i[cur * T + lane];
       }
-      const bool vis_j = is_visited(vis, j);  // issued alongside the Philox chain
-      uint32_t key = score_key(w, j, step, gant, it, a.ks);
-      if (!(w > 0.0f) || vis_j) key = 0u;
-      const uint32_t mkey = __reduce_max_sync(kFull, key);
-      if (mkey != 0u) {
-        bestj = __reduce_min_sync(kFull, key == mkey ? j : 0xffffffffu);
-        best = __uint_as_float(mkey - 1u);
-      }
+      score_window(w, j, vis, step, gant, it, a.ks, best, bestj);
       const float wl = __shfl_sync(kFull, w, T - 1);
-      done = (wl < best || wl <= 0.0f);
+      done = (bucket_ceiling(wl) < best) || (wl <= 0.0f);
     }
-    for (int base = T; !done && base < n; base += 32) {
-      if (base != T) {
+    uint32_t base = (uint32_t)T;
+    while (!done) {
+      score_window(wg, jg, vis, step, gant, it, a.ks, best, bestj);
+      if (PROBE) ++windows;
+      // entries after this window have W <= bucket_ceiling(window's last W)
+      const float wl = __shfl_sync(kFull, wg, 31);
+      base += 32;
+      done = (bucket_ceiling(wl) < best) || (wl <= 0.0f) || (base >= un);
+      if (!done) {
+        e = base + lane;
         wg = 0.0f;
         jg = 0;
-        if (base + lane < n) {
-          wg = __ldg(wrow + base + lane);
-          jg = __ldg(irow + base + lane);
+        if (e < un) {
+          wg = __ldg(sw + (row + e));
+          jg = __ldg(si + (row + e));
         }
       }
-      const uint32_t key = entry_key(wg, jg, best, vis, step, gant, it, a.ks);
-      const uint32_t mkey = __reduce_max_sync(kFull, key);
-      if (mkey != 0u) {
-        const uint32_t jmin = __reduce_min_sync(kFull, key == mkey ? jg : 0xffffffffu);
-        const float sc = __uint_as_float(mkey - 1u);
-        if (sc > best || (sc == best && jmin < bestj)) {
-          best = sc;
-          bestj = jmin;
-        }
-      }
-      ++windows;
-      // entries after this window have W <= the window's last W
-      const float wl = __shfl_sync(kFull, wg, 31);
-      done = (wl < best || wl <= 0.0f);
     }
     if (bestj == 0xffffffffu) {
       if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
@@ -250,7 +267,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
     if (step > 1) lc.push();  // edge step-2, loaded one step ago
     lc.load(cur, bestj);      // edge step-1
     __syncwarp();
-    tw.put(step, (int32_t)bestj);
+    tw.put((int)step, (int32_t)bestj);
     cur = bestj;
   }
   tw.flush();
@@ -261,7 +278,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
     const double c = lc.finish();
     if (lane == 0) a.costs[ant] = c;
   }
-  if (a.scan_count != nullptr && lane == 0) atomicAdd(a.scan_count, windows);
+  if (PROBE && lane == 0) atomicAdd(a.scan_count, windows);
 }
 
 struct DenseArgs {
@@ -494,8 +511,19 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
     SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, sw, si, dist, iteration,
                  tours_out, costs_out, status, scan_count, ks};
-    if (set_smem((const void *)k_construct_sorted, smem) != TACO_OK) return TACO_ERR_CUDA;
-    k_construct_sorted<<<(m_local + warps - 1) / warps, warps * 32, smem, s>>>(a);
+    const int grid = (m_local + warps - 1) / warps;
+    const void *fn = T > 0 ? (scan_count ? (const void *)k_construct_sorted<true, true>
+                                         : (const void *)k_construct_sorted<true, false>)
+                           : (scan_count ? (const void *)k_construct_sorted<false, true>
+                                         : (const void *)k_construct_sorted<false, false>);
+    if (set_smem(fn, smem) != TACO_OK) return TACO_ERR_CUDA;
+    if (T > 0) {
+      if (scan_count) k_construct_sorted<true, true><<<grid, warps * 32, smem, s>>>(a);
+      else k_construct_sorted<true, false><<<grid, warps * 32, smem, s>>>(a);
+    } else {
+      if (scan_count) k_construct_sorted<false, true><<<grid, warps * 32, smem, s>>>(a);
+      else k_construct_sorted<false, false><<<grid, warps * 32, smem, s>>>(a);
+    }
   } else if (variant == TACO_CONSTRUCT_DENSE) {
     if (w == nullptr || ldw < n || (ldw % 4) != 0) return TACO_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(w) & 15u) != 0) return TACO_ERR_ARG;

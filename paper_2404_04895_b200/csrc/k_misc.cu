@@ -79,7 +79,7 @@ __global__ void k_elite_neighbors(int n, int k, const TourT *__restrict__ tours,
   const int city = (int)t[s];
   const int prev = (int)t[s == 0 ? n - 1 : s - 1];
   const int next = (int)t[s + 1 == n ? 0 : s + 1];
-  nbr[(size_t)r * n + city] = make_int2(prev, next);
+  nbr[(size_t)city * k + r] = make_int2(prev, next);  // city-major: row i reads k contiguous pairs
   if (s == 0) inc[r] = __ddiv_rn(1.0, costs[a]);  // pheromone.py:66 inc = 1.0 / cost
 }
 

@@ -1,4 +1,5 @@
-// Fused pheromone update + transition matrix + selection table, one CTA per row.
+// Fused pheromone update + transition matrix + selection table, one row per
+// CTA iteration (persistent CTAs stride over the rows).
 //
 // Replaces, for row i of every n x n matrix (reference file:line):
 //   accumulate_increments  pheromone.py:52-68  delta[i, :] in elite rank order
@@ -7,8 +8,9 @@
 //   scaled_log_weights     selection.py:62-75  folded into W = fp32(P^(1/gamma))
 //
 // HBM traffic per row (Solver mode): read tau 8n + eta^beta 8n, write tau 8n,
-// write W (dense 4n and/or sorted 6n), nbr 8k gathers.  The row lives in shared
-// memory between the phases so tau / unnorm are touched once.
+// write the sorted table 6n, read the row's k elite (prev, next) pairs 8k
+// (contiguous: the edge map is city-major).  The row lives in shared memory
+// between the phases so tau / unnorm are touched once.
 #include <cub/block/block_radix_sort.cuh>
 
 #include "taco_common.cuh"
@@ -20,7 +22,7 @@ struct RowParams {
   const double *tau_in;
   double *tau_out;
   const double *eta_b;
-  const int2 *nbr;
+  const int2 *nbr;  // [n][k] (prev, next) of city i in elite r
   const double *inc;
   int k;
   const double *delta_in;
@@ -61,185 +63,254 @@ __device__ __forceinline__ float selection_weight(double p, const RowParams &a) 
   return a.gamma_one ? __double2float_rn(p) : __double2float_rn(pow(p, a.inv_gamma));
 }
 
-// Dynamic shared memory layout (bytes):
-//   [0, row_bytes)                      double row[n]   (also CUB sort storage)
-//   [row_bytes, + 16*n_leaves)          int2 leaves[], double leaf_sum[]
-//   [.., + 16*kDepositChunk)            int2 nb stage[], double inc stage[]
+// Shared-memory layout (bytes, all regions 16-B aligned):
+//   row      double[n]        delta, then unnorm (also the CUB sort workspace)
+//   plan     leaves int2[L], left/right/order u16[L], level_start int[42],
+//            leaf_sum double[L], ival double[L], hgt u8[L]
+//   stage    int2[kDepositChunk], double[kDepositChunk]
+struct RowLayout {
+  size_t row_bytes, plan_off, stage_off, total;
+};
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+__host__ __device__ inline RowLayout row_layout(int n, int L, size_t sort_bytes) {
+  RowLayout l;
+  l.row_bytes = align16((size_t)8 * n > sort_bytes ? (size_t)8 * n : sort_bytes);
+  l.plan_off = l.row_bytes;
+  const size_t plan = align16((size_t)8 * L) + 3 * align16((size_t)2 * L) + align16(4 * (kMaxPlanHeight + 2)) +
+                      2 * align16((size_t)8 * L) + align16((size_t)L);
+  l.stage_off = l.plan_off + plan;
+  l.total = l.stage_off + (size_t)16 * kDepositChunk;
+  return l;
+}
+
 template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, size_t row_bytes) {
+__global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay) {
   extern __shared__ __align__(16) unsigned char smem[];
   double *row = reinterpret_cast<double *>(smem);
-  int2 *leaves = reinterpret_cast<int2 *>(smem + row_bytes);
-  double *leaf_sum = reinterpret_cast<double *>(smem + row_bytes + 8 * (size_t)a.n_leaves);
-  int2 *nb_stage = reinterpret_cast<int2 *>(smem + row_bytes + 16 * (size_t)a.n_leaves);
+  const int L = a.n_leaves > 0 ? a.n_leaves : 1;
+  unsigned char *pp = smem + lay.plan_off;
+  PwPlan plan;
+  plan.leaves = reinterpret_cast<int2 *>(pp);
+  pp += align16((size_t)8 * L);
+  plan.left = reinterpret_cast<uint16_t *>(pp);
+  pp += align16((size_t)2 * L);
+  plan.right = reinterpret_cast<uint16_t *>(pp);
+  pp += align16((size_t)2 * L);
+  plan.order = reinterpret_cast<uint16_t *>(pp);
+  pp += align16((size_t)2 * L);
+  plan.level_start = reinterpret_cast<int *>(pp);
+  pp += align16(4 * (kMaxPlanHeight + 2));
+  double *leaf_sum = reinterpret_cast<double *>(pp);
+  pp += align16((size_t)8 * L);
+  double *ival = reinterpret_cast<double *>(pp);
+  pp += align16((size_t)8 * L);
+  uint8_t *hgt = pp;
+  int2 *nb_stage = reinterpret_cast<int2 *>(smem + lay.stage_off);
   double *inc_stage = reinterpret_cast<double *>(nb_stage + kDepositChunk);
-  __shared__ double s_sum;
+  __shared__ int s_meta[3];  // n_leaves, n_internal, height of the plan
   __shared__ double s_stage[32];
 
   const int n = a.n;
-  const int i = blockIdx.x;
   const int tid = threadIdx.x;
   const int lane = tid & 31;
-  const size_t rowoff = (size_t)i * n;
-
-  if (a.want_p && tid == 0) pw_leaves(n, leaves);
-
-  // ---- delta row -----------------------------------------------------------
+  const bool need_sum = a.want_p && !a.p_given;
   const bool have_delta = (a.nbr != nullptr) || (a.delta_in != nullptr);
-  if (a.nbr != nullptr) {
-    for (int j = tid; j < n; j += BLOCK) row[j] = 0.0;
-    for (int rbase = 0; rbase < a.k; rbase += kDepositChunk) {
-      const int rcount = min(kDepositChunk, a.k - rbase);
-      __syncthreads();
-      for (int r = tid; r < rcount; r += BLOCK) {
-        nb_stage[r] = a.nbr[(size_t)(rbase + r) * n + i];
-        inc_stage[r] = a.inc[rbase + r];
-      }
-      __syncthreads();
-      if (tid < 32) {
-        // entries e = 2r + side in rank order; one cell is hit at most once per
-        // elite (prev != next for n >= 3), so within a 32-entry window the
-        // lanes sharing a column are in rank order and their leader folds them
-        // sequentially: ((delta + inc_a) + inc_b) + ... exactly like the
-        // reference's per-elite fancy += (pheromone.py:62-67).
-        const int total = 2 * rcount;
-        for (int base = 0; base < total; base += 32) {
-          const int e = base + lane;
-          int col = -1;
-          double v = 0.0;
-          if (e < total) {
-            const int2 nb = nb_stage[e >> 1];
-            col = (e & 1) ? nb.y : nb.x;
-            v = inc_stage[e >> 1];
-          }
-          const unsigned peers = __match_any_sync(0xffffffffu, col);
-          s_stage[lane] = v;
-          __syncwarp();
-          if (col >= 0 && lane == __ffs(peers) - 1) {
-            double acc = row[col];
-            unsigned p = peers;
-            while (p) {
-              const int l = __ffs(p) - 1;
-              p &= p - 1;
-              acc = __dadd_rn(acc, s_stage[l]);
+
+  // the pairwise tree depends only on n: build it once per CTA
+  if (need_sum && tid == 0) {
+    pw_plan_build(n, plan, hgt);
+    s_meta[0] = plan.n_leaves;
+    s_meta[1] = plan.n_internal;
+    s_meta[2] = plan.height;
+  }
+  __syncthreads();
+  plan.n_leaves = s_meta[0];
+  plan.n_internal = s_meta[1];
+  plan.height = s_meta[2];
+
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const size_t rowoff = (size_t)i * n;
+
+    // ---- delta row ---------------------------------------------------------
+    if (a.nbr != nullptr) {
+      for (int j = tid; j < n; j += BLOCK) row[j] = 0.0;
+      for (int rbase = 0; rbase < a.k; rbase += kDepositChunk) {
+        const int rcount = min(kDepositChunk, a.k - rbase);
+        __syncthreads();
+        for (int r = tid; r < rcount; r += BLOCK) {
+          nb_stage[r] = a.nbr[(size_t)i * a.k + rbase + r];  // contiguous per city
+          inc_stage[r] = a.inc[rbase + r];
+        }
+        __syncthreads();
+        if (tid < 32) {
+          // entries e = 2r + side in rank order; one cell is hit at most once
+          // per elite (prev != next for n >= 3), so within a 32-entry window
+          // the lanes sharing a column are in rank order and their leader folds
+          // them sequentially: ((delta + inc_a) + inc_b) + ... exactly like the
+          // reference's per-elite fancy += (pheromone.py:62-67).
+          const int total = 2 * rcount;
+          for (int base = 0; base < total; base += 32) {
+            const int e = base + lane;
+            int col = -1;
+            double v = 0.0;
+            if (e < total) {
+              const int2 nb = nb_stage[e >> 1];
+              col = (e & 1) ? nb.y : nb.x;
+              v = inc_stage[e >> 1];
             }
-            row[col] = acc;
+            const unsigned peers = __match_any_sync(0xffffffffu, col);
+            s_stage[lane] = v;
+            __syncwarp();
+            if (col >= 0 && lane == __ffs(peers) - 1) {
+              double acc = row[col];
+              unsigned p = peers;
+              while (p) {
+                const int l = __ffs(p) - 1;
+                p &= p - 1;
+                acc = __dadd_rn(acc, s_stage[l]);
+              }
+              row[col] = acc;
+            }
+            __syncwarp();
           }
-          __syncwarp();
         }
       }
-    }
-  } else if (a.delta_in != nullptr) {
-    for (int j = tid; j < n; j += BLOCK) row[j] = a.delta_in[rowoff + j];
-  }
-  __syncthreads();
-  if (a.delta_out != nullptr) {
-    for (int j = tid; j < n; j += BLOCK) a.delta_out[rowoff + j] = have_delta ? row[j] : 0.0;
-  }
-  if (a.tau_in == nullptr) return;  // delta-only mode (accumulate_increments)
-
-  // ---- tau' and unnormalized weights -------------------------------------
-  for (int j = tid; j < n; j += BLOCK) {
-    double t = a.tau_in[rowoff + j];
-    if (a.do_evap) {
-      const double d = have_delta ? row[j] : 0.0;
-      t = __dadd_rn(__dmul_rn(a.keep, t), d);
-      t = (t < 1e-12) ? 1e-12 : t;  // np.maximum(new_tau, TAU_MIN), NaN kept
-    }
-    if (a.tau_out != nullptr) a.tau_out[rowoff + j] = t;
-    if (a.p_given) {
-      row[j] = t;
-    } else if (a.want_p) {
-      double u = __dmul_rn(numpy_scalar_power(t, a.alpha), a.eta_b[rowoff + j]);
-      if (j == i) u = 0.0;  // np.fill_diagonal(unnorm, 0.0)
-      row[j] = u;
-    }
-  }
-  if (!a.want_p) return;
-  __syncthreads();
-
-  // ---- pairwise row sum (numpy order) --------------------------------------
-  if (a.p_given) {
-    if (tid == 0) s_sum = 1.0;  // P / 1.0 == P exactly
-  } else {  // a.p_given is uniform over the CTA, so the barrier below is safe
-    for (int L = tid; L < a.n_leaves; L += BLOCK) {
-      const int2 lf = leaves[L];
-      const double *base = row + lf.x;
-      leaf_sum[L] = pw_leaf_sum(lf.y, [&](int q) { return base[q]; });
+    } else if (a.delta_in != nullptr) {
+      for (int j = tid; j < n; j += BLOCK) row[j] = a.delta_in[rowoff + j];
     }
     __syncthreads();
-    if (tid == 0) {
-      const double s = pw_fold(n, leaf_sum);
-      s_sum = s;
-      if (a.rowsum_out != nullptr) a.rowsum_out[i] = s;
-      if (!(isfinite(s) && s > 0.0)) record_status(a.status, TACO_UNDERFLOW, i);
+    if (a.delta_out != nullptr) {
+      for (int j = tid; j < n; j += BLOCK) a.delta_out[rowoff + j] = have_delta ? row[j] : 0.0;
     }
-  }
-  __syncthreads();
-  const double s = s_sum;
+    if (a.tau_in == nullptr) {  // delta-only mode (accumulate_increments)
+      __syncthreads();
+      continue;
+    }
 
-  // ---- dense outputs (coalesced, striped) ------------------------------------
-  if (a.p_out != nullptr || a.w_out != nullptr) {
+    // ---- tau' and unnormalized weights ---------------------------------------
     for (int j = tid; j < n; j += BLOCK) {
-      const double p = __ddiv_rn(row[j], s);
-      if (a.p_out != nullptr) a.p_out[rowoff + j] = p;
-      if (a.w_out != nullptr) a.w_out[(size_t)i * a.ldw + j] = selection_weight(p, a);
+      double t = a.tau_in[rowoff + j];
+      if (a.do_evap) {
+        const double d = have_delta ? row[j] : 0.0;
+        t = __dadd_rn(__dmul_rn(a.keep, t), d);
+        t = (t < 1e-12) ? 1e-12 : t;  // np.maximum(new_tau, TAU_MIN), NaN kept
+      }
+      if (a.tau_out != nullptr) a.tau_out[rowoff + j] = t;
+      if (a.p_given) {
+        row[j] = t;
+      } else if (a.want_p) {
+        double u = __dmul_rn(numpy_scalar_power(t, a.alpha), a.eta_b[rowoff + j]);
+        if (j == i) u = 0.0;  // np.fill_diagonal(unnorm, 0.0)
+        row[j] = u;
+      }
     }
-    if (a.w_out != nullptr)
-      for (int j = n + tid; j < a.ldw; j += BLOCK) a.w_out[(size_t)i * a.ldw + j] = 0.0f;
-  }
+    if (!a.want_p) {
+      __syncthreads();
+      continue;
+    }
+    __syncthreads();
 
-  // ---- row-sorted selection table ------------------------------------------
-  if constexpr (ITEMS > 0) {
-    if (a.sw_out != nullptr) {
-      using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint16_t>;
-      uint32_t keys[ITEMS];
-      uint16_t vals[ITEMS];
-#pragma unroll
-      for (int q = 0; q < ITEMS; ++q) {
-        const int j = tid * ITEMS + q;
-        if (j < n) {
-          const float w = selection_weight(__ddiv_rn(row[j], s), a);
-          keys[q] = __float_as_uint(w);
-          vals[q] = (uint16_t)j;
-        } else {
-          keys[q] = 0u;  // pads sort after every real entry (stable)
-          vals[q] = 0xffffu;
-        }
+    // ---- pairwise row sum (numpy order): parallel leaves, parallel fold ----
+    double s = 1.0;  // P / 1.0 == P exactly in selection-table mode
+    if (need_sum) {
+      for (int q = tid; q < plan.n_leaves; q += BLOCK) {
+        const int2 lf = plan.leaves[q];
+        const double *base = row + lf.x;
+        leaf_sum[q] = pw_leaf_sum(lf.y, [&](int x) { return base[x]; });
       }
-      __syncthreads();  // row[] is dead: its storage becomes the sort workspace
-      auto &ts = *reinterpret_cast<typename Sort::TempStorage *>(smem);
-      Sort(ts).SortDescendingBlockedToStriped(keys, vals, 0, 31);
+      __syncthreads();
+      s = pw_plan_fold(plan, leaf_sum, ival);
+      if (tid == 0) {
+        if (a.rowsum_out != nullptr) a.rowsum_out[i] = s;
+        if (!(isfinite(s) && s > 0.0)) record_status(a.status, TACO_UNDERFLOW, i);
+      }
+    }
+
+    // ---- dense outputs (coalesced, striped) ---------------------------------
+    if (a.p_out != nullptr || a.w_out != nullptr) {
+      for (int j = tid; j < n; j += BLOCK) {
+        const double p = __ddiv_rn(row[j], s);
+        if (a.p_out != nullptr) a.p_out[rowoff + j] = p;
+        if (a.w_out != nullptr) a.w_out[(size_t)i * a.ldw + j] = selection_weight(p, a);
+      }
+      if (a.w_out != nullptr)
+        for (int j = n + tid; j < a.ldw; j += BLOCK) a.w_out[(size_t)i * a.ldw + j] = 0.0f;
+    }
+
+    // ---- row-sorted selection table ------------------------------------------
+    if constexpr (ITEMS > 0) {
+      if (a.sw_out != nullptr) {
+        using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint16_t>;
+        uint32_t keys[ITEMS];
+        uint16_t vals[ITEMS];
 #pragma unroll
-      for (int q = 0; q < ITEMS; ++q) {
-        const int pos = tid + q * BLOCK;
-        if (pos < n) {
-          a.sw_out[rowoff + pos] = __uint_as_float(keys[q]);
-          a.si_out[rowoff + pos] = vals[q];
+        for (int q = 0; q < ITEMS; ++q) {
+          const int j = tid * ITEMS + q;
+          if (j < n) {
+            const float w = selection_weight(__ddiv_rn(row[j], s), a);
+            keys[q] = __float_as_uint(w);
+            vals[q] = (uint16_t)j;
+          } else {
+            keys[q] = 0u;  // pads sort after every real entry (stable)
+            vals[q] = 0xffffu;
+          }
+        }
+        __syncthreads();  // row[] is dead: its storage becomes the sort workspace
+        auto &ts = *reinterpret_cast<typename Sort::TempStorage *>(smem);
+        // Order by the top 15 value bits of W >= 0 (exponent + 7 mantissa bits;
+        // stable, so equal prefixes keep ascending j): 4 radix passes instead
+        // of 8.  The construction kernels bound the rest of a row by the
+        // prefix's upper end (taco_common.cuh: bucket_ceiling), so the scan is
+        // exact with this coarser order.
+        Sort(ts).SortDescendingBlockedToStriped(keys, vals, kSortBit, 31);
+#pragma unroll
+        for (int q = 0; q < ITEMS; ++q) {
+          const int pos = tid + q * BLOCK;
+          if (pos < n) {
+            a.sw_out[rowoff + pos] = __uint_as_float(keys[q]);
+            a.si_out[rowoff + pos] = vals[q];
+          }
         }
       }
     }
+    __syncthreads();  // row[] / sort workspace reused by the next row
   }
 }
 
 template <int BLOCK, int ITEMS>
 static int launch_row(const RowParams &a, cudaStream_t stream) {
-  size_t row_bytes = (size_t)a.n * sizeof(double);
+  size_t sort_bytes = 0;
   if constexpr (ITEMS > 0) {
     using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint16_t>;
-    if (sizeof(typename Sort::TempStorage) > row_bytes) row_bytes = sizeof(typename Sort::TempStorage);
+    sort_bytes = sizeof(typename Sort::TempStorage);
   }
-  row_bytes = (row_bytes + 15) & ~(size_t)15;
-  const size_t smem = row_bytes + 16 * (size_t)a.n_leaves + 16 * (size_t)kDepositChunk;
-  if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
+  const RowLayout lay = row_layout(a.n, a.n_leaves > 0 ? a.n_leaves : 1, sort_bytes);
+  if (lay.total > 227 * 1024) return TACO_ERR_UNSUPPORTED;
   static size_t configured = 0;  // per template instance
-  if (smem > 48 * 1024 && smem > configured) {
-    if (cudaFuncSetAttribute(k_row_update<BLOCK, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
+  static int blocks_per_sm = 0;
+  static size_t blocks_for = 0;
+  if (lay.total > 48 * 1024 && lay.total > configured) {
+    const cudaError_t e = cudaFuncSetAttribute(k_row_update<BLOCK, ITEMS>,
+                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
+    if (e != cudaSuccess) {
+      note_cuda_error(e);
       return TACO_ERR_CUDA;
-    configured = smem;
+    }
+    configured = lay.total;
   }
-  k_row_update<BLOCK, ITEMS><<<a.n, BLOCK, smem, stream>>>(a, row_bytes);
+  if (blocks_for != lay.total) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_row_update<BLOCK, ITEMS>, BLOCK,
+                                                      lay.total) != cudaSuccess ||
+        blocks_per_sm < 1)
+      blocks_per_sm = 1;
+    blocks_for = lay.total;
+  }
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int grid = a.n < sms * blocks_per_sm ? a.n : sms * blocks_per_sm;
+  k_row_update<BLOCK, ITEMS><<<grid, BLOCK, lay.total, stream>>>(a, lay);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }
@@ -320,7 +391,7 @@ extern "C" int taco_selection_table(int n, const double *p, double inv_gamma, fl
   a.ldw = ldw;
   a.sw_out = sw_out;
   a.si_out = si_out;
-  a.n_leaves = pw_num_leaves(n);
+  a.n_leaves = 0;
   return launch_variant(a, sw_out != nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -94,6 +94,18 @@ __device__ __forceinline__ uint32_t start_city(uint32_t n, uint32_t ant, uint32_
 }
 
 // ---------------------------------------------------------------------------
+// Sorted selection table.  Rows are ordered descending by the W bits above
+// kSortBit (k_row_update); entries that follow a given entry w therefore have
+// W <= bucket_ceiling(w), the largest float sharing w's sorted prefix.  The
+// pruned scan stops once bucket_ceiling(last W seen) < best score.
+// ---------------------------------------------------------------------------
+constexpr int kSortBit = 16;
+
+__device__ __forceinline__ float bucket_ceiling(float w) {
+  return __uint_as_float(__float_as_uint(w) | ((1u << kSortBit) - 1u));
+}
+
+// ---------------------------------------------------------------------------
 // status word: [0] = first failure code, [1] = smallest offending index
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void record_status(int32_t *status, int code, int index) {
@@ -229,6 +241,89 @@ __device__ inline double pw_fold(int n, const double *leaf_sum) {
       ++sp;
     }
   }
+}
+
+// ---------------------------------------------------------------------------
+// Parallel evaluation of the pairwise tree.  A plan lists the tree's internal
+// nodes grouped by height; each level is one round of independent adds
+// (left + right, numpy's operand order), so a CTA folds ~L leaves in
+// O(log L) barrier rounds instead of a serial walk.  Node ids: leaves are
+// 0..L-1, internal node q is kInternal | q.
+// ---------------------------------------------------------------------------
+constexpr uint16_t kInternal = 0x8000u;
+constexpr int kMaxPlanHeight = 40;
+
+struct PwPlan {
+  int2 *leaves;        // [L] (offset, length), left to right
+  uint16_t *left;      // [L-1] child ids of internal node q
+  uint16_t *right;     // [L-1]
+  uint16_t *order;     // [L-1] internal nodes sorted by height
+  int *level_start;    // [kMaxPlanHeight + 2]
+  int n_leaves, n_internal, height;
+};
+
+// Build the plan for length n (one thread).  `hgt` is [L-1] scratch.
+__device__ inline void pw_plan_build(int n, PwPlan &p, uint8_t *hgt) {
+  struct Frame {
+    int off, len, state, left_id, left_h;
+  };
+  Frame st[kMaxPlanHeight];
+  int sp = 0, nl = 0, ni = 0, ret_id = 0, ret_h = 0;
+  st[sp++] = Frame{0, n, 0, 0, 0};
+  while (sp) {
+    Frame &f = st[sp - 1];
+    if (f.len <= kPwBlock) {
+      p.leaves[nl] = make_int2(f.off, f.len);
+      ret_id = nl++;
+      ret_h = 0;
+      --sp;
+    } else if (f.state == 0) {
+      f.state = 1;
+      st[sp++] = Frame{f.off, pw_split(f.len), 0, 0, 0};
+    } else if (f.state == 1) {
+      f.left_id = ret_id;
+      f.left_h = ret_h;
+      f.state = 2;
+      const int n2 = pw_split(f.len);
+      st[sp++] = Frame{f.off + n2, f.len - n2, 0, 0, 0};
+    } else {
+      p.left[ni] = (uint16_t)f.left_id;
+      p.right[ni] = (uint16_t)ret_id;
+      const int h = 1 + (f.left_h > ret_h ? f.left_h : ret_h);
+      hgt[ni] = (uint8_t)h;
+      ret_id = kInternal | ni;
+      ret_h = h;
+      ++ni;
+      --sp;
+    }
+  }
+  p.n_leaves = nl;
+  p.n_internal = ni;
+  p.height = ret_h;
+  // counting sort of the internal nodes by height
+  for (int h = 0; h <= kMaxPlanHeight + 1; ++h) p.level_start[h] = 0;
+  for (int q = 0; q < ni; ++q) ++p.level_start[hgt[q] + 1];
+  for (int h = 1; h <= kMaxPlanHeight + 1; ++h) p.level_start[h] += p.level_start[h - 1];
+  int fill[kMaxPlanHeight + 1];
+  for (int h = 0; h <= kMaxPlanHeight; ++h) fill[h] = p.level_start[h];
+  for (int q = 0; q < ni; ++q) p.order[fill[hgt[q]]++] = (uint16_t)q;
+}
+
+// Fold leaf sums into the root with all threads of the CTA; returns the sum
+// in every thread.  `ival` is [L-1] scratch.  Contains __syncthreads.
+__device__ inline double pw_plan_fold(const PwPlan &p, const double *leaf_sum, double *ival) {
+  for (int h = 1; h <= p.height; ++h) {
+    const int b = p.level_start[h], e = p.level_start[h + 1];
+    for (int t = b + (int)threadIdx.x; t < e; t += blockDim.x) {
+      const int q = p.order[t];
+      const uint16_t l = p.left[q], r = p.right[q];
+      const double lv = (l & kInternal) ? ival[l & ~kInternal] : leaf_sum[l];
+      const double rv = (r & kInternal) ? ival[r & ~kInternal] : leaf_sum[r];
+      ival[q] = __dadd_rn(lv, rv);
+    }
+    __syncthreads();
+  }
+  return p.n_internal == 0 ? leaf_sum[0] : ival[p.n_internal - 1];
 }
 
 }  // namespace taco

@@ -66,7 +66,7 @@ def accumulate_increments(elites, n: int) -> np.ndarray:
     tours_t = _device.upload(tours, dev)
     costs_t = _device.upload(costs, dev)
     order = torch.arange(k, dtype=torch.int32, device=dev)
-    nbr = torch.empty((k, n, 2), dtype=torch.int32, device=dev)
+    nbr = torch.empty((n, k, 2), dtype=torch.int32, device=dev)  # city-major edge map
     inc = torch.empty(k, dtype=torch.float64, device=dev)
     _device.elite_neighbors(tours_t, order, costs_t, k, nbr, inc)
     delta = torch.empty((n, n), dtype=torch.float64, device=dev)

@@ -123,7 +123,7 @@ class Solver:
             self.tours_all, self.costs_all = self.tours_local, self.costs_local
         self.order = torch.zeros(m, dtype=torch.int32, device=dev)
         self.elite_ws = _device.EliteWorkspace(m, dev)
-        self.nbr = torch.zeros((k, n, 2), dtype=torch.int32, device=dev)
+        self.nbr = torch.zeros((n, k, 2), dtype=torch.int32, device=dev)  # city-major edge map
         self.inc = torch.zeros(k, dtype=torch.float64, device=dev)
         self.best_cost = torch.full((1,), math.inf, dtype=torch.float64, device=dev)
         self.best_tour = torch.zeros(n, dtype=torch.int32, device=dev)

@@ -134,7 +134,12 @@ def test_fast_construction_matches_restatement(n, m, gamma):
         assert np.array_equal(w, p.astype(np.float32))
     sw, si = t.sw.cpu().numpy(), t.si.cpu().numpy().astype(np.int64)
     assert np.array_equal(np.take_along_axis(w, si, axis=1), sw)
-    assert (np.diff(sw, axis=1) <= 0).all()
+    # rows descend in the W bits above bit 16, ties keep ascending column order
+    prefix = (sw.view(np.uint32) >> 16).astype(np.int64)
+    assert (np.diff(prefix, axis=1) <= 0).all()
+    same = np.diff(prefix, axis=1) == 0
+    assert (np.diff(si, axis=1)[same] > 0).all()
+    assert (np.sort(si, axis=1) == np.arange(n)).all()
     seed, it = 11, 5
     want = fastpath.build_tours(w, seed, it, np.arange(m))
     dist = _device.upload(inst.dist, t.w.device)
