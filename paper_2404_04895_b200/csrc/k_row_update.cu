@@ -45,6 +45,7 @@ struct RowParams {
 };
 
 constexpr int kDepositChunk = 512;  // elites staged in shared memory per pass
+constexpr int kBatch = 4;           // tau / eta^b loads in flight per thread
 
 // np.power(x, e) for a scalar float exponent: numpy dispatches e in
 // {-1, 0, 0.5, 1, 2} to reciprocal / ones / sqrt / copy / square (bit-exact
@@ -132,6 +133,19 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
 
   for (int i = blockIdx.x; i < n; i += gridDim.x) {
     const size_t rowoff = (size_t)i * n;
+    // tau / eta^b of this row are loaded kBatch elements per thread at a time;
+    // the first batch is issued before the deposit so it lands meanwhile
+    double tq[kBatch], eq[kBatch];
+    auto load_batch = [&](int jb) {
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int j = jb + u * BLOCK;
+        const bool in = j < n && a.tau_in != nullptr;
+        tq[u] = in ? a.tau_in[rowoff + j] : 0.0;
+        eq[u] = (in && need_sum) ? a.eta_b[rowoff + j] : 0.0;
+      }
+    };
+    load_batch(tid);
 
     // ---- delta row ---------------------------------------------------------
     if (a.nbr != nullptr) {
@@ -190,20 +204,26 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
     }
 
     // ---- tau' and unnormalized weights ---------------------------------------
-    for (int j = tid; j < n; j += BLOCK) {
-      double t = a.tau_in[rowoff + j];
-      if (a.do_evap) {
-        const double d = have_delta ? row[j] : 0.0;
-        t = __dadd_rn(__dmul_rn(a.keep, t), d);
-        t = (t < 1e-12) ? 1e-12 : t;  // np.maximum(new_tau, TAU_MIN), NaN kept
-      }
-      if (a.tau_out != nullptr) a.tau_out[rowoff + j] = t;
-      if (a.p_given) {
-        row[j] = t;
-      } else if (a.want_p) {
-        double u = __dmul_rn(numpy_scalar_power(t, a.alpha), a.eta_b[rowoff + j]);
-        if (j == i) u = 0.0;  // np.fill_diagonal(unnorm, 0.0)
-        row[j] = u;
+    for (int jb = tid; jb < n; jb += kBatch * BLOCK) {
+      if (jb != tid) load_batch(jb);
+#pragma unroll
+      for (int u = 0; u < kBatch; ++u) {
+        const int j = jb + u * BLOCK;
+        if (j >= n) break;
+        double t = tq[u];
+        if (a.do_evap) {
+          const double d = have_delta ? row[j] : 0.0;
+          t = __dadd_rn(__dmul_rn(a.keep, t), d);
+          t = (t < 1e-12) ? 1e-12 : t;  // np.maximum(new_tau, TAU_MIN), NaN kept
+        }
+        if (a.tau_out != nullptr) a.tau_out[rowoff + j] = t;
+        if (a.p_given) {
+          row[j] = t;
+        } else if (a.want_p) {
+          double v = __dmul_rn(numpy_scalar_power(t, a.alpha), eq[u]);
+          if (j == i) v = 0.0;  // np.fill_diagonal(unnorm, 0.0)
+          row[j] = v;
+        }
       }
     }
     if (!a.want_p) {
