@@ -111,14 +111,16 @@ def row_update(n, *, tau_in=None, tau_out=None, eta_b=None, nbr=None, inc=None, 
 
 
 class SelectionTables:
-    """fp32 selection table W = P^(1/gamma): dense (n x ldw) and/or sorted."""
+    """fp32 selection table W = P^(1/gamma): dense and/or row-sorted (values
+    sw + column indices si), all with row pitch ldw (multiple of 32).  The
+    sorted rows' pad columns stay W = 0 (zero-initialized, never selectable)."""
 
     def __init__(self, n: int, dev, dense: bool, sorted_: bool):
         self.n = n
         self.ldw = pad_ld(n)
         self.w = torch.empty((n, self.ldw), dtype=torch.float32, device=dev) if dense else None
-        self.sw = torch.empty((n, n), dtype=torch.float32, device=dev) if sorted_ else None
-        self.si = torch.empty((n, n), dtype=torch.uint16, device=dev) if sorted_ else None
+        self.sw = torch.zeros((n, self.ldw), dtype=torch.float32, device=dev) if sorted_ else None
+        self.si = torch.zeros((n, self.ldw), dtype=torch.uint16, device=dev) if sorted_ else None
 
 
 def selection_table_from_p(p: torch.Tensor, inv_gamma: float, tables: SelectionTables) -> None:

@@ -130,7 +130,7 @@ __device__ __forceinline__ uint32_t entry_key(float w, uint32_t j, float best, c
 //   int2   leaves[n_leaves]
 //   per ant: double leaf_buf[kPwBlock], double leaf_sum[n_leaves], uint32 vis[nwords]
 struct SortedArgs {
-  int n, m_local, ant_offset, T, nwords, n_leaves;
+  int n, m_local, ant_offset, T, nwords, n_leaves, ld;  // ld: sorted-table row pitch
   const float *sw;
   const uint16_t *si;
   const double *dist;
@@ -190,8 +190,8 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   if (HEAD) {  // stage the head of every row (written by k_row_update this iteration)
     for (int idx = threadIdx.x; idx < n * T; idx += blockDim.x) {
       const int row = idx / T, t = idx - row * T;
-      cache_w[idx] = __ldg(a.sw + (size_t)row * n + t);
-      cache_i[idx] = __ldg(a.si + (size_t)row * n + t);
+      cache_w[idx] = __ldg(a.sw + (size_t)row * a.ld + t);
+      cache_i[idx] = __ldg(a.si + (size_t)row * a.ld + t);
     }
   }
   if (threadIdx.x == 0) pw_leaves(n, leaves);
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   uint32_t cur = start;
   unsigned long long windows = 0;  // 32-entry global windows read (traffic probe)
   for (uint32_t step = 1; step < un; ++step) {
-    const uint32_t row = cur * un;
+    const uint32_t row = cur * (uint32_t)a.ld;  // < 2^32 for n <= 65535
     // first global window: issued before the row head is scored, so its L2
     // latency overlaps the shared-memory work
     uint32_t e = (uint32_t)T + lane;
@@ -279,6 +279,206 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
     if (lane == 0) a.costs[ant] = c;
   }
   if (PROBE && lane == 0) atomicAdd(a.scan_count, windows);
+}
+
+// ---------------------------------------------------------------------------
+// Lane-group construction: G lanes own one ant (32/G ants per warp) and each
+// lane scores E consecutive table entries per iteration with E independent
+// Philox chains, so one SIMT pass scores G*E entries for each of the warp's
+// ants.  Groups advance through their steps independently (a group that
+// finishes a step starts the next one in the following iteration), so a warp
+// never waits for its slowest ant within a step.  Same rule, same uniforms and
+// the same bucket-ceiling stop as k_construct_sorted: identical tours.
+// ---------------------------------------------------------------------------
+constexpr int kGroupWarps = 4;
+constexpr int kCostStack = 24;  // pairwise-fold stack depth (tree height <= ~12)
+
+struct GroupArgs {
+  int n, m_local, ant_offset, nwords, n_leaves, ld;
+  const float *sw;
+  const uint16_t *si;
+  const double *dist;
+  uint32_t iteration;
+  int32_t *tours;
+  double *costs;
+  int32_t *status;
+  unsigned long long *scan_count;  // optional traffic probe (32-entry windows)
+  PhiloxKeys ks;
+};
+
+// per-ant tour length in numpy's pairwise order, owned by the group's lane 0:
+// eight strided accumulators and the fold stack live in shared memory
+struct GroupCost {
+  double *acc;  // [8]
+  double *stk;  // [kCostStack]
+  int L, i, len, main_end, sp;
+  double res;
+
+  __device__ __forceinline__ void open(const int2 *leaves) {
+    len = leaves[L].y;
+    main_end = len >= 8 ? len - (len % 8) : 0;
+    i = 0;
+    res = 0.0;
+  }
+  __device__ __forceinline__ void push(double d, const int2 *leaves, const uint8_t *merges, int n_leaves) {
+    if (i < main_end) {
+      const int q = i & 7;
+      acc[q] = (i < 8) ? d : __dadd_rn(acc[q], d);
+    } else {
+      res = __dadd_rn(res, d);
+    }
+    if (++i == main_end)
+      res = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
+                      __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
+    if (i == len) {  // leaf complete: push it and close the tree nodes it ends
+      stk[sp++] = res;
+      for (int k = merges[L]; k > 0; --k) {
+        const double right = stk[--sp];
+        const double left = stk[--sp];
+        stk[sp++] = __dadd_rn(left, right);
+      }
+      if (++L < n_leaves) open(leaves);
+    }
+  }
+};
+
+template <int G, int E, bool PROBE>
+__global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __grid_constant__ GroupArgs a) {
+  static_assert(G == 4 || G == 8 || G == 16, "lanes per ant");
+  static_assert(E == 2 || E == 4, "entries per lane");
+  constexpr int A = 32 / G;  // ants per warp
+  constexpr int CH = G * E;  // entries scored per ant per iteration
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int n = a.n, L = a.n_leaves;
+  int2 *leaves = reinterpret_cast<int2 *>(smem);
+  uint8_t *merges = reinterpret_cast<uint8_t *>(smem + 8 * (size_t)L);
+  size_t off = (8 * (size_t)L + (size_t)L + 15) & ~(size_t)15;
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const size_t per_warp = (((size_t)4 * a.nwords * A + 15) & ~(size_t)15) + (size_t)8 * A * (8 + kCostStack);
+  unsigned char *wp = smem + off + per_warp * warp;
+  uint32_t *vis = reinterpret_cast<uint32_t *>(wp);  // [nwords][A]: conflict-free per ant
+  double *cost_mem = reinterpret_cast<double *>(wp + (((size_t)4 * a.nwords * A + 15) & ~(size_t)15));
+  if (threadIdx.x == 0) pw_leaves_merges(n, leaves, merges);
+  for (int q = lane; q < a.nwords * A; q += 32) vis[q] = 0u;
+  __syncthreads();
+
+  const int g = lane / G, gl = lane % G, gbase = g * G;
+  const int ant = (blockIdx.x * kGroupWarps + warp) * A + g;
+  bool alive = ant < a.m_local;
+  const uint32_t gant = (uint32_t)(a.ant_offset + ant);
+  const uint32_t it = a.iteration, un = (uint32_t)n, ld = (uint32_t)a.ld;
+  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, un);
+  int32_t *trow = a.tours + (size_t)ant * n;
+  GroupCost gc;
+  gc.acc = cost_mem + (size_t)g * (8 + kCostStack);
+  gc.stk = gc.acc + 8;
+  gc.L = 0;
+  gc.sp = 0;
+  const bool with_cost = a.costs != nullptr;
+  if (with_cost) gc.open(leaves);
+  double pending = 0.0;
+  if (alive && gl == 0) {
+    vis[(start >> 5) * A + g] |= 1u << (start & 31);
+    trow[0] = (int32_t)start;
+  }
+  __syncwarp();
+
+  uint32_t cur = start, step = 1, chunk = 0, bestj = 0xffffffffu;
+  float best = -1.0f;
+  unsigned long long chunks = 0;
+  while (__any_sync(kFull, alive)) {
+    if (PROBE && alive) ++chunks;
+    // ---- score this iteration's chunk: entries chunk + gl*E .. + E-1 -------
+    float w[E];
+    uint32_t j[E];
+    if (alive) {
+      const uint32_t o = cur * ld + chunk + (uint32_t)gl * E;
+      if constexpr (E == 4) {
+        const float4 wv = __ldg(reinterpret_cast<const float4 *>(a.sw + o));
+        const uint2 iv = __ldg(reinterpret_cast<const uint2 *>(a.si + o));
+        w[0] = wv.x, w[1] = wv.y, w[2] = wv.z, w[3] = wv.w;
+        j[0] = iv.x & 0xffffu, j[1] = iv.x >> 16, j[2] = iv.y & 0xffffu, j[3] = iv.y >> 16;
+      } else {
+        const float2 wv = __ldg(reinterpret_cast<const float2 *>(a.sw + o));
+        const uint32_t iv = __ldg(reinterpret_cast<const uint32_t *>(a.si + o));
+        w[0] = wv.x, w[1] = wv.y;
+        j[0] = iv & 0xffffu, j[1] = iv >> 16;
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) w[e] = 0.0f, j[e] = 0u;
+    }
+    bool cand[E];
+    bool any = false;
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      const uint32_t vw = vis[(j[e] >> 5) * A + g];
+      cand[e] = (w[e] > 0.0f) && (w[e] >= best) && !((vw >> (j[e] & 31)) & 1u);
+      any |= cand[e];
+    }
+    unsigned long long p = 0ull;  // packed (key, ~j): max = best score, lowest j
+    if (__any_sync(kFull, any)) {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const U4 r = philox4x32_10(U4{j[e] >> 2, step, gant, it}, a.ks);
+        const uint32_t key =
+            cand[e] ? __float_as_uint(__fmul_rn(w[e], bits_to_uniform(word_of(r, j[e] & 3)))) + 1u : 0u;
+        const unsigned long long pe = ((unsigned long long)key << 32) | (uint32_t)~j[e];
+        p = pe > p ? pe : p;
+      }
+    }
+#pragma unroll
+    for (int o2 = G / 2; o2 > 0; o2 >>= 1) {
+      const unsigned long long q = __shfl_xor_sync(kFull, p, o2);
+      p = q > p ? q : p;
+    }
+    const uint32_t gkey = (uint32_t)(p >> 32);
+    if (gkey != 0u) {
+      const float sc = __uint_as_float(gkey - 1u);
+      const uint32_t gj = ~(uint32_t)p;
+      if (sc > best || (sc == best && gj < bestj)) {
+        best = sc;
+        bestj = gj;
+      }
+    }
+    // entries after this chunk have W <= bucket_ceiling(chunk's last W)
+    const float wl = __shfl_sync(kFull, w[E - 1], gbase + G - 1);
+    chunk += CH;
+    const bool step_done = alive && ((bucket_ceiling(wl) < best) || (wl <= 0.0f) || (chunk >= un));
+
+    // ---- groups whose step is decided move to the next city ----------------
+    if (step_done) {
+      if (bestj == 0xffffffffu) {
+        if (gl == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
+        alive = false;
+      } else {
+        if (gl == 0) {
+          vis[(bestj >> 5) * A + g] |= 1u << (bestj & 31);
+          trow[step] = (int32_t)bestj;
+          if (with_cost) {
+            if (step > 1) gc.push(pending, leaves, merges, L);  // edge step-2
+            pending = __ldg(a.dist + (size_t)cur * n + bestj);   // edge step-1
+          }
+        }
+        cur = bestj;
+        ++step;
+        chunk = 0;
+        best = -1.0f;
+        bestj = 0xffffffffu;
+        if (step == un) {  // tour complete: close it and fold its length
+          if (gl == 0 && with_cost) {
+            gc.push(pending, leaves, merges, L);                          // edge n-2
+            gc.push(__ldg(a.dist + (size_t)cur * n + start), leaves, merges, L);  // closing edge
+            a.costs[ant] = gc.stk[0];
+          }
+          alive = false;
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (PROBE && gl == 0 && ant < a.m_local) atomicAdd(a.scan_count, (chunks * CH + 16) / 32);
 }
 
 struct DenseArgs {
@@ -486,7 +686,54 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
   const size_t leaves_bytes = ((size_t)8 * n_leaves + 15) & ~(size_t)15;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   if (variant == TACO_CONSTRUCT_SORTED) {
-    if (sw == nullptr || si == nullptr) return TACO_ERR_ARG;
+    if (sw == nullptr || si == nullptr || ldw < n || (ldw % 32) != 0) return TACO_ERR_ARG;
+    // kernel choice: lane-group kernel (G lanes x E entries per ant) or the
+    // warp-per-ant kernel; TACO_SORTED_KERNEL = warp | g4e4 | g8e4 | g4e2 |
+    // g8e2 | g16e2 overrides (tuning knob)
+    int G = 0, E = 0;
+    // Measured on B200 at n = 2392 (profiles/README.md): the warp kernel wins
+    // while it is latency-bound (<= ~48 ants per SM); beyond that the SIMT
+    // sharing of the lane-group kernel wins (m = 16384: 6.8 vs 9.8 ms).
+    if (m_local > 48 * sm_count()) G = 8, E = 2;
+    if (m_local > 200 * sm_count()) G = 4, E = 4;  // n = 5000, m = 65536: 44.9 vs 51.1 ms
+    if (const char *ev = getenv("TACO_SORTED_KERNEL")) {
+      G = 0;
+      if (ev[0] == 'g') {
+        G = atoi(ev + 1);
+        const char *pe = ev + 1;
+        while (*pe && *pe != 'e') ++pe;
+        E = *pe ? atoi(pe + 1) : 4;
+      }
+    }
+    if (G > 0) {
+      const size_t A = 32 / G;
+      const size_t per_warp = (((size_t)4 * nwords * A + 15) & ~(size_t)15) + (size_t)8 * A * (8 + kCostStack);
+      const size_t smem = ((8 * (size_t)n_leaves + (size_t)n_leaves + 15) & ~(size_t)15) + per_warp * kGroupWarps;
+      if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
+      GroupArgs ga{n, m_local, ant_offset, nwords, n_leaves, ldw, sw, si, dist, iteration,
+                   tours_out, costs_out, status, scan_count, ks};
+      const int ants_per_cta = (int)A * kGroupWarps;
+      const int grid = (m_local + ants_per_cta - 1) / ants_per_cta;
+#define TACO_GROUP_CASE(GG, EE)                                                                         \
+  if (G == GG && E == EE) {                                                                             \
+    if (scan_count != nullptr) {                                                                        \
+      if (set_smem((const void *)k_construct_group<GG, EE, true>, smem) != TACO_OK) return TACO_ERR_CUDA; \
+      k_construct_group<GG, EE, true><<<grid, kGroupWarps * 32, smem, s>>>(ga);                         \
+    } else {                                                                                            \
+      if (set_smem((const void *)k_construct_group<GG, EE, false>, smem) != TACO_OK) return TACO_ERR_CUDA; \
+      k_construct_group<GG, EE, false><<<grid, kGroupWarps * 32, smem, s>>>(ga);                        \
+    }                                                                                                   \
+    TACO_CUDA_CHECK_LAUNCH();                                                                           \
+    return TACO_OK;                                                                                     \
+  }
+      TACO_GROUP_CASE(4, 4)
+      TACO_GROUP_CASE(8, 4)
+      TACO_GROUP_CASE(4, 2)
+      TACO_GROUP_CASE(8, 2)
+      TACO_GROUP_CASE(16, 2)
+#undef TACO_GROUP_CASE
+      return TACO_ERR_ARG;
+    }
     // one CTA per SM when the colony allows it: the row-head cache is staged
     // once per CTA.  Knobs (tuning only): TACO_SORTED_WARPS, TACO_SORTED_T.
     int warps = (m_local + sm_count() - 1) / sm_count();
@@ -509,7 +756,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     if (T < 0 || T > 32 || T >= n) return TACO_ERR_ARG;
     const size_t smem = (((size_t)6 * n * T + 15) & ~(size_t)15) + fixed;
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
-    SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, sw, si, dist, iteration,
+    SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, ldw, sw, si, dist, iteration,
                  tours_out, costs_out, status, scan_count, ks};
     const int grid = (m_local + warps - 1) / warps;
     const void *fn = T > 0 ? (scan_count ? (const void *)k_construct_sorted<true, true>

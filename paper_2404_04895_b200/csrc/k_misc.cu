@@ -45,17 +45,28 @@ __global__ void __launch_bounds__(WARPS * 32)
 // shared memory; one thread per ant.  Exact np.argsort(kind="stable").
 constexpr int kRankMaxM = 16384;
 
-__global__ void __launch_bounds__(256) k_elite_rank(int m, const double *__restrict__ costs, int32_t *order) {
+constexpr int kRankWarps = 8;
+constexpr int kRankAntsPerWarp = 4;
+
+// one warp ranks kRankAntsPerWarp ants: lanes split the comparison range,
+// redux.sync adds the partial counts
+__global__ void __launch_bounds__(kRankWarps * 32)
+    k_elite_rank(int m, const double *__restrict__ costs, int32_t *order) {
   extern __shared__ unsigned long long keys[];
   for (int b = threadIdx.x; b < m; b += blockDim.x) keys[b] = (unsigned long long)__double_as_longlong(costs[b]);
   __syncthreads();
-  const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a >= m) return;
-  const unsigned long long ka = keys[a];
-  int rank = 0;
-  for (int b = 0; b < a; ++b) rank += keys[b] <= ka;  // earlier ants win ties
-  for (int b = a + 1; b < m; ++b) rank += keys[b] < ka;
-  order[rank] = a;
+  const int lane = threadIdx.x & 31;
+  const int first = (blockIdx.x * kRankWarps + (threadIdx.x >> 5)) * kRankAntsPerWarp;
+  for (int a = first; a < first + kRankAntsPerWarp && a < m; ++a) {
+    const unsigned long long ka = keys[a];
+    unsigned cnt = 0;
+    for (int b = lane; b < m; b += 32) {
+      const unsigned long long kb = keys[b];
+      cnt += (kb < ka) || (kb == ka && b < a);  // earlier ants win ties
+    }
+    const unsigned rank = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) order[rank] = a;
+  }
 }
 
 __global__ void k_cost_keys(int m, const double *costs, unsigned long long *keys, int32_t *vals) {
@@ -164,7 +175,8 @@ extern "C" int taco_elite_order(int m, const double *costs, int32_t *order_out, 
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(k_elite_rank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return TACO_ERR_CUDA;
-    k_elite_rank<<<(m + 255) / 256, 256, smem, st>>>(m, costs, order_out);
+    constexpr int per_cta = kRankWarps * kRankAntsPerWarp;
+    k_elite_rank<<<(m + per_cta - 1) / per_cta, kRankWarps * 32, smem, st>>>(m, costs, order_out);
     TACO_CUDA_CHECK_LAUNCH();
     return TACO_OK;
   }

@@ -289,8 +289,8 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
         for (int q = 0; q < ITEMS; ++q) {
           const int pos = tid + q * BLOCK;
           if (pos < n) {
-            a.sw_out[rowoff + pos] = __uint_as_float(keys[q]);
-            a.si_out[rowoff + pos] = vals[q];
+            a.sw_out[(size_t)i * a.ldw + pos] = __uint_as_float(keys[q]);
+            a.si_out[(size_t)i * a.ldw + pos] = vals[q];
           }
         }
       }
@@ -363,7 +363,7 @@ extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, con
   if (nbr != nullptr && (inc == nullptr || k < 1)) return TACO_ERR_ARG;
   if (nbr != nullptr && delta_in != nullptr) return TACO_ERR_ARG;
   if (want_p && eta_b == nullptr) return TACO_ERR_ARG;
-  if (w_out != nullptr && ldw < n) return TACO_ERR_ARG;
+  if ((w_out != nullptr || sw_out != nullptr) && (ldw < n || (ldw % 32) != 0)) return TACO_ERR_ARG;
   if ((sw_out == nullptr) != (si_out == nullptr)) return TACO_ERR_ARG;
   if ((sw_out != nullptr || w_out != nullptr || p_out != nullptr) && !want_p) return TACO_ERR_ARG;
   RowParams a;
@@ -397,7 +397,7 @@ extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, con
 extern "C" int taco_selection_table(int n, const double *p, double inv_gamma, float *w_out, int ldw,
                                     float *sw_out, uint16_t *si_out, void *stream) {
   if (n < 3 || n > 65535 || p == nullptr) return TACO_ERR_ARG;
-  if (w_out != nullptr && ldw < n) return TACO_ERR_ARG;
+  if ((w_out != nullptr || sw_out != nullptr) && (ldw < n || (ldw % 32) != 0)) return TACO_ERR_ARG;
   if ((sw_out == nullptr) != (si_out == nullptr)) return TACO_ERR_ARG;
   RowParams a = {};
   a.n = n;

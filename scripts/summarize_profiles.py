@@ -1,0 +1,79 @@
+"""Summarize an ncu round into profiles/ (tracked): launch-list shares and the
+key counters of each full capture.
+
+usage: python scripts/summarize_profiles.py <tag> [gpurun_out dir]
+writes profiles/<tag>_launches.csv, profiles/<tag>_kernels.csv,
+profiles/<tag>_hotlines.txt
+"""
+import collections
+import csv
+import io
+import os
+import subprocess
+import sys
+
+tag = sys.argv[1]
+src = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
+root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+out_dir = os.path.join(root, "profiles")
+os.makedirs(out_dir, exist_ok=True)
+
+# ---- launch list -------------------------------------------------------------
+rows = list(csv.reader(open(os.path.join(src, f"launches_{tag}.csv"))))
+hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+h = rows[hi]
+ki, vi = h.index("Kernel Name"), h.index("Metric Value")
+agg, cnt = collections.OrderedDict(), collections.Counter()
+for r in rows[hi + 1:]:
+    name = r[ki].split("(")[0].replace("void ", "")
+    agg[name] = agg.get(name, 0.0) + float(r[vi].replace(",", "")) / 1e3
+    cnt[name] += 1
+total = sum(agg.values())
+with open(os.path.join(out_dir, f"{tag}_launches.csv"), "w", newline="") as f:
+    w = csv.writer(f)
+    w.writerow(["kernel", "launches", "total_us", "mean_us", "share"])
+    for k, v in sorted(agg.items(), key=lambda x: -x[1]):
+        w.writerow([k, cnt[k], f"{v:.1f}", f"{v / cnt[k]:.1f}", f"{v / total:.4f}"])
+
+# ---- full captures ----------------------------------------------------------------
+METRICS = [
+    "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sector_hit_rate.pct",
+    "lts__throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+]
+reps = sorted(f for f in os.listdir(src) if f.startswith("prof_") and f.endswith(f"_{tag}.ncu-rep"))
+kern_rows = []
+hot = []
+for rep in reps:
+    path = os.path.join(src, rep)
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(raw)))
+    if len(r) < 3:
+        continue
+    hh, uu, vv = r[0], r[1], r[2]
+    rec = {"report": rep, "kernel": vv[hh.index("Kernel Name")].split("(")[0] if "Kernel Name" in hh else ""}
+    for m in METRICS:
+        if m in hh:
+            rec[m] = f"{vv[hh.index(m)]} {uu[hh.index(m)]}".strip()
+    kern_rows.append(rec)
+    lines = subprocess.run([sys.executable, os.path.join(root, "scripts", "ncu_lines.py"), path, "12"],
+                           capture_output=True, text=True).stdout
+    hot.append(f"== {rep}\n{lines}")
+with open(os.path.join(out_dir, f"{tag}_kernels.csv"), "w", newline="") as f:
+    cols = ["report", "kernel"] + METRICS
+    w = csv.DictWriter(f, fieldnames=cols)
+    w.writeheader()
+    for rec in kern_rows:
+        w.writerow(rec)
+with open(os.path.join(out_dir, f"{tag}_hotlines.txt"), "w") as f:
+    f.write("\n".join(hot))
+print(open(os.path.join(out_dir, f"{tag}_launches.csv")).read())
+for rec in kern_rows:
+    print(rec["report"], rec.get("gpu__time_duration.sum"), rec.get("dram__bytes_read.sum"),
+          rec.get("dram__bytes_write.sum"), rec.get("lts__t_sector_hit_rate.pct"),
+          rec.get("smsp__issue_active.avg.pct_of_peak_sustained_active"))

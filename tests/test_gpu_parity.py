@@ -132,7 +132,8 @@ def test_fast_construction_matches_restatement(n, m, gamma):
     # the tables hold exactly fp32(P^(1/gamma)), row-sorted descending
     if gamma == 1.0:
         assert np.array_equal(w, p.astype(np.float32))
-    sw, si = t.sw.cpu().numpy(), t.si.cpu().numpy().astype(np.int64)
+    sw, si = t.sw[:, :n].cpu().numpy(), t.si[:, :n].cpu().numpy().astype(np.int64)
+    assert (t.sw[:, n:] == 0).all()  # pad columns are never selectable
     assert np.array_equal(np.take_along_axis(w, si, axis=1), sw)
     # rows descend in the W bits above bit 16, ties keep ascending column order
     prefix = (sw.view(np.uint32) >> 16).astype(np.int64)
