@@ -158,6 +158,11 @@ def run_ours(args) -> dict | None:
     n, m, selection = CONFIGS[args.config]
     k = max(1, m // 10)
     period = args.warmup + args.steps
+    # nvidia-smi needs ~0.2 s to start polling: launch it before any GPU work so
+    # its samples cover the warm-up and both timed regions
+    sampler = ClockSampler(local) if rank == 0 else None
+    if sampler:
+        sampler.__enter__()
     coords = np.random.default_rng(0).uniform(0.0, 2000.0, (n, 2))
     inst = taco.euclidean_instance(coords)
     params = taco.AcoParams(m=m, k=k, selection=selection, seed=0,
@@ -174,10 +179,6 @@ def run_ours(args) -> dict | None:
     del warm
     _device._INSTANCES.clear()
     torch.cuda.synchronize()
-    # clocks are sampled over both timed regions (e2e + device), ~100 ms apart
-    sampler = ClockSampler(local) if rank == 0 else None
-    if sampler:
-        sampler.__enter__()
     _barrier(world)
     t0 = time.perf_counter()
     e2e_solver = taco.Solver(e2e_inst, params, construct=args.construct)

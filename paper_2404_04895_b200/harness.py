@@ -1,0 +1,124 @@
+"""Experiment harness on the device Solver.
+
+Mirrors the reference's ``run_experiment`` (bench.py:171-238) so convergence
+studies (IR vs AdaIR, bench.py:162-168) run at GPU scale with the same record
+and summary types: run r uses seed base + r, every iteration yields an
+``IterationRecord``, and each run a ``RunSummary`` whose mean time excludes
+the first (warm-up) iteration.  Iteration times are device times of one full
+iteration (CUDA events); instance loading is the caller's (TSPLIB parsing is
+outside the accelerated path), so ``inst`` is required.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from .model import Selection
+from .selection import gamma_at
+from .solver import Solver
+
+CONVERGENCE_BAND = 1e-3  # bench.py:40
+
+
+@dataclass(frozen=True)
+class ExperimentConfig:
+    """Run parameters (bench.py:71-98); instance fields are informational."""
+
+    params: object
+    instance_path: str | None = None
+    synthetic: object | None = None
+    repetitions: int = 1
+    time_limit_seconds: float | None = None
+    output_path: str | None = None
+    summary_path: str | None = None
+    record_probability_shift: bool = False
+    best_known: float | None = None
+    lenient: bool = False
+    chunk_size: int | None = None
+
+    def __post_init__(self):
+        if self.repetitions < 1:
+            raise ValueError(f"repetitions must be >= 1, got {self.repetitions}")
+        if self.time_limit_seconds is not None and self.time_limit_seconds <= 0:
+            raise ValueError("time_limit_seconds must be positive")
+
+
+@dataclass(frozen=True)
+class IterationRecord:
+    run_id: int
+    seed: int
+    iteration: int
+    wall_clock_ms: float
+    iteration_best_cost: float
+    best_cost_so_far: float
+    solution_error_percent: float | None
+    gamma: float | None
+    rho: float
+
+
+@dataclass(frozen=True)
+class RunSummary:
+    run_id: int
+    seed: int
+    iterations_run: int
+    final_best_cost: float
+    solution_error_percent: float | None
+    convergence_generation: int
+    mean_ms_per_iter: float
+    terminated_by: str
+
+
+def convergence_generation(best_trace: list[float]) -> int:
+    """First iteration whose best-so-far is within 0.1% of the final best."""
+    limit = best_trace[-1] * (1.0 + CONVERGENCE_BAND)
+    return next(it for it, v in enumerate(best_trace) if v <= limit)
+
+
+def run_experiment(config: ExperimentConfig, inst, clock=time.perf_counter,
+                   construct: str = "sorted") -> tuple[list[IterationRecord], list[RunSummary]]:
+    """construct -> elite -> deposit -> evaporate -> P per iteration on the
+    device, `repetitions` runs with seeds base..base+r-1."""
+    if inst is None:
+        raise ValueError("pass the TspInstance: instance loading is outside the accelerated path")
+    base = config.params
+    bk = config.best_known if config.best_known is not None else getattr(inst, "best_known", None)
+    records: list[IterationRecord] = []
+    summaries: list[RunSummary] = []
+    adair = Selection(base.selection) is Selection.ADAIR
+    for run_id in range(config.repetitions):
+        params = replace(base, seed=base.seed + run_id)
+        solver = Solver(inst, params, construct=construct)
+        best_so_far = float("inf")
+        trace, iter_ms = [], []
+        terminated_by = "max_iters"
+        run_start = clock()
+        for it in range(params.max_iters):
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0.record()
+            solver.step_async()
+            t1.record()
+            solver.check()  # synchronizes; raises the reference's exceptions
+            ms = t0.elapsed_time(t1)
+            iteration_best = float(solver.costs_all[solver.order[0]].item())
+            best_so_far = min(best_so_far, iteration_best)
+            trace.append(best_so_far)
+            iter_ms.append(ms)
+            records.append(IterationRecord(
+                run_id=run_id, seed=params.seed, iteration=it, wall_clock_ms=ms,
+                iteration_best_cost=iteration_best, best_cost_so_far=best_so_far,
+                solution_error_percent=(100.0 * (best_so_far - bk) / bk) if bk else None,
+                gamma=gamma_at(it, params.gamma_schedule) if adair else None, rho=params.rho))
+            if config.time_limit_seconds is not None and clock() - run_start >= config.time_limit_seconds:
+                terminated_by = "time_limit"
+                break
+        measured = iter_ms[1:] if len(iter_ms) > 1 else iter_ms
+        summaries.append(RunSummary(
+            run_id=run_id, seed=params.seed, iterations_run=len(iter_ms), final_best_cost=best_so_far,
+            solution_error_percent=(100.0 * (best_so_far - bk) / bk) if bk else None,
+            convergence_generation=convergence_generation(trace),
+            mean_ms_per_iter=float(np.mean(measured)), terminated_by=terminated_by))
+    return records, summaries
