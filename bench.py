@@ -63,7 +63,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+              "clocks_event_reasons.sw_power_cap,utilization.gpu")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
@@ -74,7 +74,7 @@ class ClockSampler:
     def _reader(self):
         for line in self._proc.stdout:
             parts = [c.strip() for c in line.split(",")]
-            if len(parts) >= 7:
+            if len(parts) >= 8:
                 self.rows.append(parts)
 
     def __enter__(self):
@@ -102,13 +102,22 @@ class ClockSampler:
     def summary(self) -> dict:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        smax = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+
+        # samples taken while kernels ran (the sampler also sees the idle gaps
+        # between the timed regions)
+        busy = [r for r in self.rows if (num(r[7]) or 0.0) >= 50.0] or self.rows
+        sm = [num(r[0]) for r in busy if num(r[0]) is not None]
+        smax = [num(r[1]) for r in self.rows if num(r[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower().startswith("active")})
+        reasons = sorted({names[i] for r in busy for i in range(4) if r[3 + i].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(busy)}
 
 
 # ---------------------------------------------------------------------------

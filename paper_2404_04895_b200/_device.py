@@ -118,7 +118,8 @@ class SelectionTables:
     def __init__(self, n: int, dev, dense: bool, sorted_: bool):
         self.n = n
         self.ldw = pad_ld(n)
-        self.w = torch.empty((n, self.ldw), dtype=torch.float32, device=dev) if dense else None
+        # the sorted table is built from the dense one, so sorted implies dense
+        self.w = torch.empty((n, self.ldw), dtype=torch.float32, device=dev) if dense or sorted_ else None
         self.sw = torch.zeros((n, self.ldw), dtype=torch.float32, device=dev) if sorted_ else None
         self.si = torch.zeros((n, self.ldw), dtype=torch.uint16, device=dev) if sorted_ else None
 

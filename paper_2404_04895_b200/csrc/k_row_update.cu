@@ -86,7 +86,7 @@ __host__ __device__ inline RowLayout row_layout(int n, int L, size_t sort_bytes)
   return l;
 }
 
-template <int BLOCK, int ITEMS>
+template <int BLOCK>
 __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay) {
   extern __shared__ __align__(16) unsigned char smem[];
   double *row = reinterpret_cast<double *>(smem);
@@ -259,60 +259,31 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
         for (int j = n + tid; j < a.ldw; j += BLOCK) a.w_out[(size_t)i * a.ldw + j] = 0.0f;
     }
 
-    // ---- row-sorted selection table ------------------------------------------
-    if constexpr (ITEMS > 0) {
-      if (a.sw_out != nullptr) {
-        using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint16_t>;
-        uint32_t keys[ITEMS];
-        uint16_t vals[ITEMS];
-#pragma unroll
-        for (int q = 0; q < ITEMS; ++q) {
-          const int j = tid * ITEMS + q;
-          if (j < n) {
-            const float w = selection_weight(__ddiv_rn(row[j], s), a);
-            keys[q] = __float_as_uint(w);
-            vals[q] = (uint16_t)j;
-          } else {
-            keys[q] = 0u;  // pads sort after every real entry (stable)
-            vals[q] = 0xffffu;
-          }
-        }
-        __syncthreads();  // row[] is dead: its storage becomes the sort workspace
-        auto &ts = *reinterpret_cast<typename Sort::TempStorage *>(smem);
-        // Order by the top 15 value bits of W >= 0 (exponent + 7 mantissa bits;
-        // stable, so equal prefixes keep ascending j): 4 radix passes instead
-        // of 8.  The construction kernels bound the rest of a row by the
-        // prefix's upper end (taco_common.cuh: bucket_ceiling), so the scan is
-        // exact with this coarser order.
-        Sort(ts).SortDescendingBlockedToStriped(keys, vals, kSortBit, 31);
-#pragma unroll
-        for (int q = 0; q < ITEMS; ++q) {
-          const int pos = tid + q * BLOCK;
-          if (pos < n) {
-            a.sw_out[(size_t)i * a.ldw + pos] = __uint_as_float(keys[q]);
-            a.si_out[(size_t)i * a.ldw + pos] = vals[q];
-          }
-        }
-      }
-    }
-    __syncthreads();  // row[] / sort workspace reused by the next row
+    __syncthreads();  // row[] is reused by the next row
   }
 }
 
-template <int BLOCK, int ITEMS>
-static int launch_row(const RowParams &a, cudaStream_t stream) {
-  size_t sort_bytes = 0;
-  if constexpr (ITEMS > 0) {
-    using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, uint16_t>;
-    sort_bytes = sizeof(typename Sort::TempStorage);
+static int sm_count_row() {
+  static int cached = 0;
+  if (cached == 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
+      cached = 148;
   }
-  const RowLayout lay = row_layout(a.n, a.n_leaves > 0 ? a.n_leaves : 1, sort_bytes);
+  return cached;
+}
+
+constexpr int kRowBlock = 256;
+
+static int launch_row(const RowParams &a, cudaStream_t stream) {
+  const RowLayout lay = row_layout(a.n, a.n_leaves > 0 ? a.n_leaves : 1, 0);
   if (lay.total > 227 * 1024) return TACO_ERR_UNSUPPORTED;
-  static size_t configured = 0;  // per template instance
+  static size_t configured = 0;
   static int blocks_per_sm = 0;
   static size_t blocks_for = 0;
   if (lay.total > 48 * 1024 && lay.total > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(k_row_update<BLOCK, ITEMS>,
+    const cudaError_t e = cudaFuncSetAttribute(k_row_update<kRowBlock>,
                                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
     if (e != cudaSuccess) {
       note_cuda_error(e);
@@ -321,18 +292,93 @@ static int launch_row(const RowParams &a, cudaStream_t stream) {
     configured = lay.total;
   }
   if (blocks_for != lay.total) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_row_update<BLOCK, ITEMS>, BLOCK,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_row_update<kRowBlock>, kRowBlock,
                                                       lay.total) != cudaSuccess ||
         blocks_per_sm < 1)
       blocks_per_sm = 1;
     blocks_for = lay.total;
   }
-  int dev = 0, sms = 148;
-  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int sms = sm_count_row();
   const int grid = a.n < sms * blocks_per_sm ? a.n : sms * blocks_per_sm;
-  k_row_update<BLOCK, ITEMS><<<grid, BLOCK, lay.total, stream>>>(a, lay);
+  k_row_update<kRowBlock><<<grid, kRowBlock, lay.total, stream>>>(a, lay);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Row sort of the selection table: sw/si[i, :] = row i of W in descending
+// order of the W bits above kSortBit, stable in the column index.  Keys are
+// packed (W prefix << 16 | j) so a single 32-bit register per item carries
+// both; the exact W is gathered back from a shared copy of the row.  Entries
+// past n sort last (prefix 0, larger position) and are not written.
+// ---------------------------------------------------------------------------
+template <int BLOCK, int ITEMS>
+__global__ void __launch_bounds__(BLOCK) k_row_sort(int n, int ldw, const float *__restrict__ w,
+                                                    float *__restrict__ sw, uint16_t *__restrict__ si) {
+  using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  auto &ts = *reinterpret_cast<typename Sort::TempStorage *>(smem);
+  float *wrow = reinterpret_cast<float *>(smem + ((sizeof(typename Sort::TempStorage) + 15) & ~(size_t)15));
+  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+    const float *src = w + (size_t)i * ldw;
+    for (int j = threadIdx.x; j < n; j += BLOCK) wrow[j] = src[j];
+    __syncthreads();
+    uint32_t keys[ITEMS];
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int j = threadIdx.x * ITEMS + q;
+      keys[q] = j < n ? ((__float_as_uint(wrow[j]) & ~((1u << kSortBit) - 1u)) | (uint32_t)j) : 0xffffu;
+    }
+    Sort(ts).SortDescendingBlockedToStriped(keys, kSortBit, 31);
+#pragma unroll
+    for (int q = 0; q < ITEMS; ++q) {
+      const int pos = threadIdx.x + q * BLOCK;
+      if (pos < n) {
+        const uint32_t j = keys[q] & 0xffffu;
+        sw[(size_t)i * ldw + pos] = wrow[j];
+        si[(size_t)i * ldw + pos] = (uint16_t)j;
+      }
+    }
+    __syncthreads();  // wrow / sort storage reused by the next row
+  }
+}
+
+template <int BLOCK, int ITEMS>
+static int launch_sort_t(int n, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t stream) {
+  using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS>;
+  const size_t smem = ((sizeof(typename Sort::TempStorage) + 15) & ~(size_t)15) + (size_t)4 * n;
+  if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
+  static int blocks_per_sm = 0;
+  static size_t configured = 0;
+  if (configured != smem) {
+    if (smem > 48 * 1024) {
+      const cudaError_t e =
+          cudaFuncSetAttribute(k_row_sort<BLOCK, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) {
+        note_cuda_error(e);
+        return TACO_ERR_CUDA;
+      }
+    }
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_row_sort<BLOCK, ITEMS>, BLOCK, smem) !=
+            cudaSuccess ||
+        blocks_per_sm < 1)
+      blocks_per_sm = 1;
+    configured = smem;
+  }
+  const int sms = sm_count_row();
+  const int grid = n < sms * blocks_per_sm ? n : sms * blocks_per_sm;
+  k_row_sort<BLOCK, ITEMS><<<grid, BLOCK, smem, stream>>>(n, ldw, w, sw, si);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+static int launch_sort(int n, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t s) {
+  if (n <= 1024) return launch_sort_t<128, 8>(n, ldw, w, sw, si, s);
+  if (n <= 2560) return launch_sort_t<256, 10>(n, ldw, w, sw, si, s);
+  if (n <= 5120) return launch_sort_t<512, 10>(n, ldw, w, sw, si, s);
+  if (n <= 10240) return launch_sort_t<512, 20>(n, ldw, w, sw, si, s);
+  if (n <= 20480) return launch_sort_t<1024, 20>(n, ldw, w, sw, si, s);
+  return TACO_ERR_UNSUPPORTED;
 }
 
 }  // namespace taco
@@ -342,14 +388,9 @@ using namespace taco;
 extern "C" int taco_max_sorted_n(void) { return 20480; }
 
 static int launch_variant(RowParams &a, bool sorted, cudaStream_t s) {
-  if (!sorted) return launch_row<256, 0>(a, s);
-  const int n = a.n;
-  if (n <= 1024) return launch_row<128, 8>(a, s);
-  if (n <= 2560) return launch_row<256, 10>(a, s);
-  if (n <= 5120) return launch_row<512, 10>(a, s);
-  if (n <= 10240) return launch_row<512, 20>(a, s);
-  if (n <= 20480) return launch_row<1024, 20>(a, s);
-  return TACO_ERR_UNSUPPORTED;
+  const int rc = launch_row(a, s);
+  if (rc != TACO_OK || !sorted) return rc;
+  return launch_sort(a.n, a.ldw, a.w_out, a.sw_out, a.si_out, s);
 }
 
 extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, const double *eta_b,
@@ -365,6 +406,7 @@ extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, con
   if (want_p && eta_b == nullptr) return TACO_ERR_ARG;
   if ((w_out != nullptr || sw_out != nullptr) && (ldw < n || (ldw % 32) != 0)) return TACO_ERR_ARG;
   if ((sw_out == nullptr) != (si_out == nullptr)) return TACO_ERR_ARG;
+  if (sw_out != nullptr && w_out == nullptr) return TACO_ERR_ARG;  // the sort reads the dense table
   if ((sw_out != nullptr || w_out != nullptr || p_out != nullptr) && !want_p) return TACO_ERR_ARG;
   RowParams a;
   a.n = n;
@@ -399,6 +441,7 @@ extern "C" int taco_selection_table(int n, const double *p, double inv_gamma, fl
   if (n < 3 || n > 65535 || p == nullptr) return TACO_ERR_ARG;
   if ((w_out != nullptr || sw_out != nullptr) && (ldw < n || (ldw % 32) != 0)) return TACO_ERR_ARG;
   if ((sw_out == nullptr) != (si_out == nullptr)) return TACO_ERR_ARG;
+  if (sw_out != nullptr && w_out == nullptr) return TACO_ERR_ARG;  // the sort reads the dense table
   RowParams a = {};
   a.n = n;
   a.tau_in = p;
