@@ -63,7 +63,7 @@ class ClockSampler:
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap,utilization.gpu")
+              "clocks_event_reasons.sw_power_cap,utilization.gpu,clocks_event_reasons.gpu_idle")
 
     def __init__(self, gpu: int):
         self.gpu = gpu
@@ -74,7 +74,7 @@ class ClockSampler:
     def _reader(self):
         for line in self._proc.stdout:
             parts = [c.strip() for c in line.split(",")]
-            if len(parts) >= 8:
+            if len(parts) >= 9:
                 self.rows.append(parts)
 
     def __enter__(self):
@@ -109,9 +109,9 @@ class ClockSampler:
             except ValueError:
                 return None
 
-        # samples taken while kernels ran (the sampler also sees the idle gaps
-        # between the timed regions)
-        busy = [r for r in self.rows if (num(r[7]) or 0.0) >= 50.0] or self.rows
+        # samples taken while kernels ran: the sampler also sees the host-side
+        # gaps (instance setup, syncs) where the GPU idles at low clocks
+        busy = [r for r in self.rows if not r[8].lower().startswith("active")] or self.rows
         sm = [num(r[0]) for r in busy if num(r[0]) is not None]
         smax = [num(r[1]) for r in self.rows if num(r[1]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]

@@ -531,7 +531,10 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
     for (int q = lane; q < nq; q += 32) {
       const float4 wv = __ldg(row + q);
       const uint32_t nib = (vis[q >> 3] >> ((q & 7) * 4)) & 0xfu;
-      const bool any = (nib != 0xfu) && (wv.x > 0.0f || wv.y > 0.0f || wv.z > 0.0f || wv.w > 0.0f);
+      // a score is w * u < w, so a group whose largest W cannot reach this
+      // lane's running best (key - 1 as float) cannot change the argmax
+      const float wmax = fmaxf(fmaxf(wv.x, wv.y), fmaxf(wv.z, wv.w));
+      const bool any = (nib != 0xfu) && wmax > 0.0f && (lkey == 0u || wmax >= __uint_as_float(lkey - 1u));
       if (any) {
         const U4 r = philox4x32_10(U4{(uint32_t)q, (uint32_t)step, gant, it}, a.ks);
         const float wc[4] = {wv.x, wv.y, wv.z, wv.w};
