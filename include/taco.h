@@ -150,6 +150,23 @@ int taco_select_parity(int n, int m, int step, const double *logw,
                        uint8_t *visited, int64_t *tours,
                        int32_t *status, void *stream);
 
+/*
+ * Reference-stream replay: the same round as
+ * taco_select_parity, but the step's (m, n) Exp(1) block of
+ * Generator(Philox(SeedSequence(seed, spawn_key=(0, it, step))))
+ * .standard_exponential (rng.py:42-49) is regenerated on the device from the
+ * step's Philox4x64 key (key0, key1 = SeedSequence.generate_state(2, uint64),
+ * computed by the host) with numpy's ziggurat, decoded in parallel.
+ * flags_out (2 device words, zeroed by the caller): [0] counts wedge tests
+ * closer than 4 ulp (CUDA vs glibc exp could disagree), [1] is set if the
+ * replay window overflowed; either makes the round unreliable.
+ */
+size_t taco_replay_workspace_bytes(int m, int n);
+int taco_select_replay(int n, int m, int step, uint64_t key0, uint64_t key1,
+                       const double *logw, int64_t *current, uint8_t *visited,
+                       int64_t *tours, void *workspace, size_t ws_bytes,
+                       unsigned *flags_out, int32_t *status, void *stream);
+
 /* logw = log(p)/gamma, -inf where p == 0 (selection.py:62-75). */
 int taco_log_weights(int64_t count, const double *p, double gamma,
                      double *logw_out, void *stream);

@@ -87,10 +87,15 @@ def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = No
 
     stream="device" (default): keyed on-chip Philox4x32-10 uniforms and the
     product-form rule argmax(W * u) — the fast path.
-    stream="numpy": reference-stream replay — the reference's own keyed numpy
-    deviates, start cities and log-weight table (rng.py:42-68,
-    selection.py:62-75) are produced on the host and the device runs the n-1
-    log-domain argmax rounds; tours equal the reference's bit for bit.
+    stream="replay": the reference's own stream, regenerated on the device —
+    the per-step Philox4x64 keys of SeedSequence(seed, spawn_key=(0, it, step))
+    come from the host, and the (m, n) Exp(1) blocks are decoded from them on
+    the device with numpy's ziggurat (k_numpy_stream.cu); tours equal the
+    reference's bit for bit at GPU speed.
+    stream="numpy": the same, with the deviate blocks produced by numpy on the
+    host and uploaded step by step (slow; the replay's cross-check).
+    In both reference-stream modes the start cities and the log-weight table
+    are numpy's own (rng.py:65-68, selection.py:62-75).
     ``chunk_size`` is accepted and has no effect (chunking is bit-invisible in
     the reference too, colony.py:119-124); ``probe`` is not supported.
     variant: "sorted" (pruned scan of the row-sorted table) or "dense" (full
@@ -105,14 +110,15 @@ def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = No
     di = _device.device_instance(inst)
     dev = di.dev
     p_host = np.asarray(p.p, dtype=np.float64)
-    if stream == "numpy":
-        tours_t = _construct_reference_stream(p_host, n, m, params.seed, iteration, gamma, dev)
+    if stream in ("numpy", "replay"):
+        tours_t = _construct_reference_stream(p_host, n, m, params.seed, iteration, gamma, dev,
+                                              replay=(stream == "replay"))
         costs_t = _device.tour_cost(tours_t, di.dist)
     elif stream == "device":
         tours_t, costs_t = _construct_device_stream(p_host, n, m, params.seed, iteration, gamma, dev,
                                                     variant, di.dist)
     else:
-        raise ValueError(f"stream must be 'device' or 'numpy', got {stream!r}")
+        raise ValueError(f"stream must be 'device', 'replay' or 'numpy', got {stream!r}")
     return TourBatch(tours=_device.download(tours_t).astype(np.int64, copy=False),
                      costs=_device.download(costs_t))
 
@@ -140,7 +146,12 @@ def _raise_construct_status(status: torch.Tensor) -> None:
         raise AssertionError("selector chose a visited city")
 
 
-def _construct_reference_stream(p_host, n, m, seed, iteration, gamma, dev) -> torch.Tensor:
+class ReplayUnreliable(RuntimeError):
+    """A replayed ziggurat comparison was too close to call with CUDA's exp
+    (or the replay window overflowed); use stream="numpy" for that call."""
+
+
+def _construct_reference_stream(p_host, n, m, seed, iteration, gamma, dev, replay: bool) -> torch.Tensor:
     # log-weight table with the reference's numpy arithmetic (selection.py:72-74)
     logw = np.full(p_host.shape, -np.inf)
     np.log(p_host, out=logw, where=p_host > 0)
@@ -154,11 +165,26 @@ def _construct_reference_stream(p_host, n, m, seed, iteration, gamma, dev) -> to
     tours[:, 0] = current
     status = _device.new_status(dev)
     lib = _lib.load()
-    for step in range(1, n):
-        e_t = _device.upload(_rng.step_exponentials(seed, iteration, step, m, n), dev)
-        _lib.check(lib.taco_select_parity(n, m, step, logw_t.data_ptr(), e_t.data_ptr(), current.data_ptr(),
-                                          visited.data_ptr(), tours.data_ptr(), status.data_ptr(),
-                                          _device.stream_handle()), "taco_select_parity")
+    stream = _device.stream_handle()
+    if replay:
+        keys = _rng.step_keys(seed, iteration, n)
+        ws_bytes = int(lib.taco_replay_workspace_bytes(m, n))
+        ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+        flags = torch.zeros(2, dtype=torch.int32, device=dev)
+        for step in range(1, n):
+            k0, k1 = (int(v) for v in keys[step - 1])
+            _lib.check(lib.taco_select_replay(n, m, step, k0, k1, logw_t.data_ptr(), current.data_ptr(),
+                                              visited.data_ptr(), tours.data_ptr(), ws.data_ptr(), ws_bytes,
+                                              flags.data_ptr(), status.data_ptr(), stream), "taco_select_replay")
+        ambiguous, overflow = (int(v) for v in flags.cpu().tolist())
+        if ambiguous or overflow:
+            raise ReplayUnreliable(f"replay flags: {ambiguous} close wedge tests, overflow={overflow}")
+    else:
+        for step in range(1, n):
+            e_t = _device.upload(_rng.step_exponentials(seed, iteration, step, m, n), dev)
+            _lib.check(lib.taco_select_parity(n, m, step, logw_t.data_ptr(), e_t.data_ptr(), current.data_ptr(),
+                                              visited.data_ptr(), tours.data_ptr(), status.data_ptr(), stream),
+                       "taco_select_parity")
     _raise_construct_status(status)
     return tours
 

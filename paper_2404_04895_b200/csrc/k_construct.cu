@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
 
   if (HEAD) {  // stage the head of every row (written by k_row_update this iteration)
     for (int idx = threadIdx.x; idx < n * T; idx += blockDim.x) {
-      const int row = idx / T, t = idx - row * T;
+      const int row = idx / (T > 0 ? T : 1), t = idx - row * T;
       cache_w[idx] = __ldg(a.sw + (size_t)row * a.ld + t);
       cache_i[idx] = __ldg(a.si + (size_t)row * a.ld + t);
     }

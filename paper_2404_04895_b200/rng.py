@@ -36,6 +36,14 @@ def step_exponentials(seed: int, iteration: int, step: int, m: int, n: int) -> n
     return stream(seed, DOMAIN_CONSTRUCT, iteration, step).standard_exponential((m, n))
 
 
+def step_keys(seed: int, iteration: int, n: int) -> np.ndarray:
+    """Philox4x64 keys of the construction steps 1..n-1 of one iteration: the
+    state SeedSequence(seed, spawn_key=(0, it, step)) hands to numpy's Philox
+    (rng.py:33-39).  Shape (n-1, 2) uint64; the device replays the streams."""
+    return np.stack([np.random.SeedSequence(entropy=seed, spawn_key=(DOMAIN_CONSTRUCT, iteration, step))
+                     .generate_state(2, np.uint64) for step in range(1, n)])
+
+
 def start_cities(seed: int, iteration: int, m: int, n: int) -> np.ndarray:
     """Reference start city per ant (rng.py:65-68)."""
     return stream(seed, DOMAIN_START, iteration).integers(0, n, size=m, dtype=np.int64)

@@ -77,11 +77,17 @@ class Solver:
     ``AcoParams.for_instance`` (alpha, beta, rho, n_ants / m, k, selection,
     seed, gamma_schedule, q0_tau, max_iters).
     construct: "sorted" (pruned scan, default) or "dense" (full-row stream).
+    stream: "device" (default, the on-chip Philox4x32 stream) or "replay":
+    every iteration replays the reference's own numpy streams on the device
+    (colony.construct_tours(stream="replay")) with the reference's log-domain
+    rule, so a run reproduces antbatch's run_experiment bit for bit (tours,
+    pheromone, best lengths) — the parity mode, one GPU only.
     group: torch.distributed group to shard ants over (default: the world
     group when initialized with more than one rank).
     """
 
-    def __init__(self, instance, params=None, *, construct: str = "sorted", group=None, **overrides):
+    def __init__(self, instance, params=None, *, construct: str = "sorted", stream: str = "device",
+                 group=None, **overrides):
         self.inst = _as_instance(instance)
         self.n = n = int(self.inst.n)
         self.params = p = _as_params(params, n, overrides)
@@ -93,6 +99,9 @@ class Solver:
             construct = "dense"
         self.construct = construct
         self._variant = _lib.CONSTRUCT_SORTED if construct == "sorted" else _lib.CONSTRUCT_DENSE
+        if stream not in ("device", "replay"):
+            raise ValueError(f"stream must be 'device' or 'replay', got {stream!r}")
+        self.stream = stream
 
         self.group = group
         if group is None and tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1:
@@ -100,6 +109,8 @@ class Solver:
         world = tdist.get_world_size(self.group) if self.group is not None else 1
         rank = tdist.get_rank(self.group) if self.group is not None else 0
         self.shard: AntShard = shard_ants(p.m, rank, world)
+        if stream == "replay" and world > 1:
+            raise ValueError("the reference-stream replay runs on one GPU")
 
         self.di = _device.device_instance(self.inst)
         dev = self.dev = self.di.dev
@@ -107,8 +118,18 @@ class Solver:
         self.eta_b = self.di.eta_beta(p.beta)
         self.tau = torch.full((n, n), float(p.q0_tau), dtype=torch.float64, device=dev)
         self.tau.fill_diagonal_(0.0)
-        self.tables = _device.SelectionTables(n, dev, dense=(construct == "dense"),
-                                              sorted_=(construct == "sorted"))
+        replay = stream == "replay"
+        self.tables = _device.SelectionTables(n, dev, dense=(construct == "dense" and not replay),
+                                              sorted_=(construct == "sorted" and not replay))
+        if replay:  # reference-stream state: P, the numpy log table, lockstep buffers
+            self.p = torch.empty((n, n), dtype=torch.float64, device=dev)
+            self.logw = torch.empty((n, n), dtype=torch.float64, device=dev)
+            self.tours64 = torch.zeros((m, n), dtype=torch.int64, device=dev)
+            self.visited = torch.zeros((m, n), dtype=torch.uint8, device=dev)
+            self.current = torch.zeros(m, dtype=torch.int64, device=dev)
+            self.replay_ws_bytes = int(lib.taco_replay_workspace_bytes(m, n))
+            self.replay_ws = torch.empty(self.replay_ws_bytes, dtype=torch.uint8, device=dev)
+            self.replay_flags = torch.zeros(2, dtype=torch.int32, device=dev)
         sh = self.shard
         # zero-initialized so a failed construction never leaves out-of-range cities
         self.tours_local = torch.zeros((sh.per_rank, n), dtype=torch.int32, device=dev)
@@ -138,6 +159,13 @@ class Solver:
     # ------------------------------------------------------------------
     def _rebuild_tables(self, evaporate: bool, gamma_next: float) -> None:
         t = self.tables
+        if self.stream == "replay":  # P itself is the next iteration's input
+            _device.row_update(
+                self.n, tau_in=self.tau, tau_out=self.tau if evaporate else None, eta_b=self.eta_b,
+                nbr=self.nbr if evaporate else None, inc=self.inc if evaporate else None,
+                k=self.params.k if evaporate else 0, do_evap=evaporate, keep=self.keep, want_p=True,
+                alpha=float(self.params.alpha), p_out=self.p, rowsum_out=self.rowsum, status=self.status)
+            return
         _device.row_update(
             self.n, tau_in=self.tau, tau_out=self.tau if evaporate else None, eta_b=self.eta_b,
             nbr=self.nbr if evaporate else None, inc=self.inc if evaporate else None,
@@ -157,9 +185,12 @@ class Solver:
         lib = _lib.load()
         ev = _Timer(timers)
         ev.start("construct")
-        _device.construct(self.n, sh.count, sh.offset, self._variant, self.tables, p.seed, it,
-                          self.tours_local, self.status, scan_count, dist=self.di.dist,
-                          costs_out=self.costs_local)
+        if self.stream == "replay":
+            self._construct_replay(it)
+        else:
+            _device.construct(self.n, sh.count, sh.offset, self._variant, self.tables, p.seed, it,
+                              self.tours_local, self.status, scan_count, dist=self.di.dist,
+                              costs_out=self.costs_local)
         ev.stop("construct")
         if sh.world > 1:
             gather_colony(self.tours_local, self.costs_local, sh, self.tours_all, self.costs_all,
@@ -174,6 +205,40 @@ class Solver:
         self._rebuild_tables(evaporate=True, gamma_next=construction_gamma(p, it + 1))
         ev.stop("update")
         self.iteration = it + 1
+
+    def _construct_replay(self, it: int) -> None:
+        """Lockstep construction on the reference's streams (colony.py:101-152):
+        numpy's start cities and log table (host), the step deviates replayed
+        on the device from numpy's Philox keys."""
+        from . import rng as _rng
+        from .colony import ReplayUnreliable
+
+        n, p, lib = self.n, self.params, _lib.load()
+        gamma = construction_gamma(p, it)
+        ph = _device.download(self.p)
+        logw = np.full(ph.shape, -np.inf)
+        np.log(ph, out=logw, where=ph > 0)  # selection.py:72-74, numpy's own log
+        np.divide(logw, gamma, out=logw)
+        self.logw.copy_(torch.from_numpy(logw))
+        starts = torch.from_numpy(_rng.start_cities(p.seed, it, p.m, n)).to(self.dev)
+        self.current.copy_(starts)
+        self.visited.zero_()
+        self.visited[torch.arange(p.m, device=self.dev), starts] = 1
+        self.tours64[:, 0] = starts
+        keys = _rng.step_keys(p.seed, it, n)
+        stream = _device.stream_handle()
+        for step in range(1, n):
+            k0, k1 = (int(v) for v in keys[step - 1])
+            _lib.check(lib.taco_select_replay(n, p.m, step, k0, k1, self.logw.data_ptr(), self.current.data_ptr(),
+                                              self.visited.data_ptr(), self.tours64.data_ptr(),
+                                              self.replay_ws.data_ptr(), self.replay_ws_bytes,
+                                              self.replay_flags.data_ptr(), self.status.data_ptr(), stream),
+                       "taco_select_replay")
+        self.tours_local.copy_(self.tours64)
+        _device.tour_cost(self.tours64, self.di.dist, self.costs_local)
+        ambiguous, overflow = (int(v) for v in self.replay_flags.cpu().tolist())
+        if ambiguous or overflow:
+            raise ReplayUnreliable(f"replay flags: {ambiguous} close wedge tests, overflow={overflow}")
 
     def check(self) -> None:
         """Raise the reference's exception for any failure recorded so far."""

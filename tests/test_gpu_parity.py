@@ -64,8 +64,9 @@ def test_device_uniforms_and_starts_match_restatement():
 # ---------------------------------------------------------------------------
 # drop-ins against the reference's golden pipeline
 # ---------------------------------------------------------------------------
+@pytest.mark.parametrize("stream", ["numpy", "replay"])
 @pytest.mark.parametrize("name", ["int12_ir", "int12_adair", "euc23_adair", "euc17_ab"])
-def test_dropin_pipeline_matches_reference_golden(golden, name):
+def test_dropin_pipeline_matches_reference_golden(golden, name, stream):
     inst = _inst(golden, name)
     for seed in golden[f"{name}/seeds"].tolist():
         params, iters = _params(golden, name, seed)
@@ -79,7 +80,7 @@ def test_dropin_pipeline_matches_reference_golden(golden, name):
                 np.testing.assert_allclose(prob.p, golden[f"{key}/p"], rtol=1e-12, atol=0)
             # reference-stream replay: feed the golden P so tours are comparable bitwise
             batch = taco.construct_tours(taco.ProbabilityMatrix(golden[f"{key}/p"]), inst, params, it,
-                                         stream="numpy")
+                                         stream=stream)
             assert np.array_equal(batch.tours, golden[f"{key}/tours"])
             assert np.array_equal(batch.costs, golden[f"{key}/costs"])
             elites = taco.select_elite(batch, params.k)
@@ -92,9 +93,10 @@ def test_dropin_pipeline_matches_reference_golden(golden, name):
             prob = taco.compute_probability_matrix(tau, inst, params)
 
 
+@pytest.mark.parametrize("stream", ["numpy", "replay"])
 @pytest.mark.parametrize("mech", ["ir", "adair"])
 @pytest.mark.parametrize("n,m", [(5, 1), (10, 7), (51, 64)])
-def test_reference_stream_tours_bit_exact(mech, n, m):
+def test_reference_stream_tours_bit_exact(mech, n, m, stream):
     inst = euclid(n + m, n)
     for seed in range(3):
         params = taco.AcoParams(m=m, k=1, selection=mech, seed=seed,
@@ -102,10 +104,26 @@ def test_reference_stream_tours_bit_exact(mech, n, m):
         tau = ref.initial_tau(n, 1.0)
         p = ref.transition(tau, inst.eta, 1.0, 2.0)
         for it in (0, 3):
-            got = taco.construct_tours(taco.ProbabilityMatrix(p), inst, params, it, stream="numpy")
+            got = taco.construct_tours(taco.ProbabilityMatrix(p), inst, params, it, stream=stream)
             want = ref.build_tours(p, m, seed, it, ref.gamma(it, 1.5, 1.0, 7) if mech == "adair" else 1.0)
             assert np.array_equal(got.tours, want)
             assert np.array_equal(got.costs, ref.lengths(want, inst.dist))
+
+
+@pytest.mark.parametrize("n,m", [(257, 300), (600, 512)])
+def test_device_replay_of_reference_stream_at_scale(n, m):
+    # 77k / 307k deviates per step decoded on the device from numpy's Philox
+    # keys (slow ziggurat paths included): the reference's tours exactly
+    inst = euclid(n, n)
+    g = np.random.default_rng(n)
+    tau = g.uniform(0.05, 3.0, (n, n))
+    p = ref.transition((tau + tau.T) / 2, inst.eta, 1.0, 2.0)
+    params = taco.AcoParams(m=m, k=1, selection="adair", seed=99,
+                            gamma_schedule=taco.GammaSchedule(1.5, 1.0, 10))
+    got = taco.construct_tours(taco.ProbabilityMatrix(p), inst, params, 3, stream="replay")
+    want = ref.build_tours(p, m, 99, 3, ref.gamma(3, 1.5, 1.0, 10))
+    assert np.array_equal(got.tours, want)
+    assert np.array_equal(got.costs, ref.lengths(want, inst.dist))
 
 
 # ---------------------------------------------------------------------------
@@ -312,3 +330,21 @@ def test_solver_quality_matches_reference_statistically():
     assert abs(ours.mean() - theirs.mean()) / theirs.mean() < 0.03
     se = np.sqrt(ours.var(ddof=1) / 10 + theirs.var(ddof=1) / 10)
     assert abs(ours.mean() - theirs.mean()) <= 3 * se + 1e-9 * theirs.mean()
+
+
+@pytest.mark.parametrize("name", ["int12_ir", "int12_adair", "euc23_adair"])
+def test_solver_replay_reproduces_reference_runs(golden, name):
+    # full runs on the reference's own streams: every iteration's tours, lengths
+    # and pheromone equal antbatch's run (golden vectors) bit for bit
+    inst = _inst(golden, name)
+    for seed in golden[f"{name}/seeds"].tolist():
+        params, iters = _params(golden, name, seed)
+        s = taco.Solver(inst, params, stream="replay")
+        for it in range(iters):
+            key = f"{name}/s{seed}/it{it}"
+            tour, length = s.step()
+            b = s.last_batch()
+            assert np.array_equal(b.tours, golden[f"{key}/tours"])
+            assert np.array_equal(b.costs, golden[f"{key}/costs"])
+            assert np.array_equal(s.pheromone().tau, golden[f"{key}/tau"])
+            assert length == min(golden[f"{name}/s{seed}/it{i}/costs"].min() for i in range(it + 1))
