@@ -299,7 +299,9 @@ def run_ours(args) -> dict | None:
                 "d2h_bytes_per_step": n * 4 + 8 + 16,
                 "what": "Solver(host instance: dist+eta H2D) + K x step() returning best tour/length (D2H)"},
         "gpu_launches": args.steps * 6,
-        "gpu_launches_note": "6 libtaco kernels per iteration + CUB radix-sort kernels of the elite sort",
+        "gpu_launches_note": ("6 libtaco kernels per iteration: k_construct_sorted (or the lane-group "
+                              "variant), k_elite_rank, k_track_best, k_elite_neighbors, k_row_update, "
+                              "k_row_sort (CUB radix sort only for m > 16384)"),
         "best_length": best_len,
     }
     if dense_ms is not None:

@@ -72,9 +72,18 @@ __device__ __forceinline__ bool np_fast(uint64_t w) {
   return ri < kZigKe[(w >> 3) & 0xff];
 }
 
-// Decode one sample starting at word p: returns the value, writes the number
-// of words consumed; counts wedge tests too close to call.
-__device__ double np_sample(uint64_t p, uint64_t w, uint64_t k0, uint64_t k1, int &len, unsigned *ambiguous) {
+// word source: the step's words materialized by k_np_len (positions < P),
+// recomputed from the key past the replay window
+struct NpWords {
+  const uint64_t *buf;
+  uint64_t P, k0, k1;
+  __device__ __forceinline__ uint64_t operator()(uint64_t p) const { return p < P ? buf[p] : np_word(p, k0, k1); }
+};
+
+// Decode one sample starting at word p (first word w): returns the value,
+// writes the number of words consumed; counts wedge tests too close to call.
+template <typename Words>
+__device__ double np_sample(uint64_t p, uint64_t w, const Words &word, int &len, unsigned *ambiguous) {
   len = 0;
   for (;;) {
     uint64_t ri = w >> 3;
@@ -85,7 +94,7 @@ __device__ double np_sample(uint64_t p, uint64_t w, uint64_t k0, uint64_t k1, in
       len += 1;
       return x;
     }
-    const double u = np_double(np_word(p + 1, k0, k1));
+    const double u = np_double(word(p + 1));
     len += 2;
     if (idx == 0) return __dsub_rn(kZigExpR, log1p(-u));
     const double fe_i = __longlong_as_double((long long)kZigFeBits[idx]);
@@ -97,11 +106,17 @@ __device__ double np_sample(uint64_t p, uint64_t w, uint64_t k0, uint64_t k1, in
     if (ambiguous != nullptr && fabs(lhs - rhs) <= 4.0 * 0x1p-52 * rhs) atomicAdd(ambiguous, 1u);
     if (lhs < rhs) return x;
     p += 2;  // rejected: the retry starts at the next unused word
-    w = np_word(p, k0, k1);
+    w = word(p);
   }
 }
 
+struct KeyWords {  // words straight from the key (used while filling the buffer)
+  uint64_t k0, k1;
+  __device__ __forceinline__ uint64_t operator()(uint64_t p) const { return np_word(p, k0, k1); }
+};
+
 struct ReplayWs {
+  uint64_t *words;  // [P] the step's Philox4x64 words
   uint32_t *slow;   // [P/32] slow-path bit per position
   uint8_t *lens;    // [P] words consumed by a sample starting at a slow position
   uint32_t *cov;    // [P/32] positions consumed by a previous sample
@@ -112,18 +127,22 @@ struct ReplayWs {
   uint64_t P;       // positions replayed (multiple of 128)
 };
 
-__global__ void k_np_len(uint64_t P, uint64_t k0, uint64_t k1, uint32_t *slow, uint8_t *lens, unsigned *flags) {
+__global__ void k_np_len(uint64_t P, uint64_t k0, uint64_t k1, uint64_t *words, uint32_t *slow, uint8_t *lens,
+                         unsigned *flags) {
   const uint64_t b = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (4 * b >= P) return;
   const U64x4 blk = philox4x64_10(b + 1, k0, k1);
   const uint64_t ws[4] = {blk.x, blk.y, blk.z, blk.w};
+  reinterpret_cast<ulonglong2 *>(words + 4 * b)[0] = make_ulonglong2(blk.x, blk.y);
+  reinterpret_cast<ulonglong2 *>(words + 4 * b)[1] = make_ulonglong2(blk.z, blk.w);
+  const KeyWords kw{k0, k1};
   uint32_t bits = 0;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     if (!np_fast(ws[q])) {
       const uint64_t p = 4 * b + q;
       int len;
-      np_sample(p, ws[q], k0, k1, len, flags);
+      np_sample(p, ws[q], kw, len, flags);
       if (len > kMaxSlowLen) atomicOr(flags + 1, 1u);
       lens[p] = (uint8_t)(len > 255 ? 255 : len);
       bits |= 1u << q;
@@ -138,6 +157,25 @@ __device__ __forceinline__ uint64_t step_len(const uint32_t *slow, const uint8_t
   return bit(slow, s) ? lens[s] : 1;
 }
 
+// first slow position >= s (or `limit` if none before it)
+__device__ __forceinline__ uint64_t next_slow(const uint32_t *slow, uint64_t s, uint64_t limit) {
+  uint64_t w = s >> 5;
+  uint32_t bits = slow[w] & (0xffffffffu << (s & 31));
+  while (!bits) {
+    if (++w * 32 >= limit) return limit;
+    bits = slow[w];
+  }
+  const uint64_t q = w * 32 + (__ffs(bits) - 1);
+  return q < limit ? q : limit;
+}
+
+// does any slow position q in [lo, a) reach past a (q + L(q) > a)?
+__device__ __forceinline__ bool reaches_past(const uint32_t *slow, const uint8_t *lens, uint64_t lo, uint64_t a) {
+  for (uint64_t q = next_slow(slow, lo, a); q < a; q = next_slow(slow, q + 1, a))
+    if (q + lens[q] > a) return true;
+  return false;
+}
+
 // thread per 32-position word of the slow bitmap
 __global__ void k_np_cover(uint64_t P, const uint32_t *slow, const uint8_t *lens, uint32_t *cov) {
   const uint64_t wi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -149,17 +187,12 @@ __global__ void k_np_cover(uint64_t P, const uint32_t *slow, const uint8_t *lens
     const uint64_t p = wi * 32 + b;
     // anchor: a position no slow sample before it can reach past is a start
     uint64_t a = p > (uint64_t)kMaxSlowLen ? p - kMaxSlowLen : 0;
-    for (;;) {
-      if (a == 0) break;
-      bool safe = true;
-      const uint64_t lo = a > (uint64_t)kMaxSlowLen ? a - kMaxSlowLen : 0;
-      for (uint64_t q = lo; q < a && safe; ++q)
-        if (bit(slow, q) && q + lens[q] > a) safe = false;
-      if (safe) break;
+    while (a > 0 && reaches_past(slow, lens, a > (uint64_t)kMaxSlowLen ? a - kMaxSlowLen : 0, a))
       a = a > (uint64_t)kMaxSlowLen ? a - kMaxSlowLen : 0;
-    }
+    // walk the sample starts from the anchor: fast runs are skipped in one
+    // jump (each fast position is a start that consumes one word)
     uint64_t s = a;
-    while (s < p) s += step_len(slow, lens, s);
+    while (s < p) s = bit(slow, s) ? s + lens[s] : next_slow(slow, s, p);
     if (s == p)
       for (uint64_t c = p + 1; c < p + lens[p] && c < P; ++c) atomicOr(cov + (c >> 5), 1u << (c & 31));
   }
@@ -212,7 +245,8 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int j = base + lane;
     if (j < n) {
       int len;
-      const double e = np_sample(my, np_word(my, k0, k1), k0, k1, len, nullptr);
+      const NpWords word{ws.words, ws.P, k0, k1};
+      const double e = np_sample(my, word(my), word, len, nullptr);
       // np.take -> np.subtract -> np.copyto(-inf, where=visited)  (selection.py:152-154)
       const double s = vr[j] ? -INFINITY : __dsub_rn(lr[j], e);
       if (s > best) {
@@ -258,6 +292,8 @@ static ReplayWs carve(void *ws, int m, int n) {
   r.P = replay_positions(m, n);
   const uint64_t words = r.P / 32;
   unsigned char *p = reinterpret_cast<unsigned char *>(ws);
+  r.words = reinterpret_cast<uint64_t *>(p);
+  p += al256(r.P * 8);
   r.slow = reinterpret_cast<uint32_t *>(p);
   p += al256(words * 4);
   r.cov = reinterpret_cast<uint32_t *>(p);
@@ -279,7 +315,7 @@ using namespace taco;
 extern "C" size_t taco_replay_workspace_bytes(int m, int n) {
   if (m < 1 || n < 1) return 0;
   const uint64_t P = replay_positions(m, n), words = P / 32;
-  return 3 * al256(words * 4) + al256(P) + al256(scan_bytes(words));
+  return al256(P * 8) + 3 * al256(words * 4) + al256(P) + al256(scan_bytes(words));
 }
 
 extern "C" int taco_select_replay(int n, int m, int step, uint64_t key0, uint64_t key1, const double *logw,
@@ -294,7 +330,8 @@ extern "C" int taco_select_replay(int n, int m, int step, uint64_t key0, uint64_
   if (cudaMemsetAsync(r.slow, 0, words * 4, s) != cudaSuccess ||
       cudaMemsetAsync(r.cov, 0, words * 4, s) != cudaSuccess)
     return TACO_ERR_CUDA;
-  k_np_len<<<(unsigned)((r.P / 4 + 255) / 256), 256, 0, s>>>(r.P, key0, key1, r.slow, r.lens, flags_out);
+  k_np_len<<<(unsigned)((r.P / 4 + 255) / 256), 256, 0, s>>>(r.P, key0, key1, r.words, r.slow, r.lens,
+                                                              flags_out);
   TACO_CUDA_CHECK_LAUNCH();
   k_np_cover<<<(unsigned)((words + 255) / 256), 256, 0, s>>>(r.P, r.slow, r.lens, r.cov);
   TACO_CUDA_CHECK_LAUNCH();
