@@ -11,7 +11,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "libtaco.so")
+LIB_PATH = os.environ.get("TACO_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                           "libtaco.so")
 
 TACO_OK = 0
 TACO_UNDERFLOW = 1

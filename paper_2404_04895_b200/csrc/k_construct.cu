@@ -144,6 +144,25 @@ struct SortedArgs {
 
 constexpr int kSortedMaxWarps = 28;
 
+// Pull the first global window (entries off..off+31) of row j into L1: the
+// lanes holding the row head's top entries issue this right after loading
+// them, so when one of them wins the step the next step's window is an L1 hit
+// instead of an L2 round trip on the serial step chain.
+__device__ __forceinline__ void prefetch_window(const float *sw, const uint16_t *si, uint32_t j, uint32_t ld,
+                                                uint32_t off) {
+  const float *pw = sw + (size_t)j * ld + off;
+  const uint16_t *pi = si + (size_t)j * ld + off;
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(pw));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(pw + 31));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(pi));
+  asm volatile("prefetch.global.L1 [%0];" ::"l"(pi + 31));
+}
+
+#ifdef TACO_STEP_PROFILE
+// per-step latency phases of ant 0 (head window, global windows, bookkeeping)
+__device__ unsigned long long g_step_prof[8];
+#endif
+
 // Score the 32-entry window (w, j) of the sorted row against the running
 // (best, bestj).  Warp-uniform control flow: the Philox chain runs once per
 // window for all lanes iff any lane holds a candidate (unvisited, W > 0,
@@ -169,7 +188,7 @@ __device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t
   }
 }
 
-template <bool HEAD, bool PROBE>
+template <bool HEAD, bool PROBE, bool PREFETCH = true>
 __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const __grid_constant__ SortedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
@@ -217,6 +236,9 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   uint32_t cur = start;
   unsigned long long windows = 0;  // 32-entry global windows read (traffic probe)
   for (uint32_t step = 1; step < un; ++step) {
+#ifdef TACO_STEP_PROFILE
+    const long long t0 = clock64();
+#endif
     const uint32_t row = cur * (uint32_t)a.ld;  // < 2^32 for n <= 65535
     // first global window: issued before the row head is scored, so its L2
     // latency overlaps the shared-memory work
@@ -236,13 +258,42 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
       if (lane < T) {
         w = cache_w[cur * T + lane];
         j = cache_i[cur * T + lane];
+        if (PREFETCH && w > 0.0f) prefetch_window(sw, si, j, (uint32_t)a.ld, (uint32_t)T);
       }
+#ifdef TACO_STEP_PROFILE
+      {
+        const uint32_t vw = vis[j >> 5];
+        const bool cand = (w > 0.0f) && !((vw >> (j & 31)) & 1u);
+        const long long ta = clock64();
+        const U4 r = philox4x32_10(U4{j >> 2, step, gant, it}, a.ks);
+        const uint32_t key = cand ? __float_as_uint(__fmul_rn(w, bits_to_uniform(word_of(r, j & 3)))) + 1u : 0u;
+        const long long tb = clock64();
+        const uint32_t mkey = __reduce_max_sync(kFull, key);
+        const long long tc = clock64();
+        const uint32_t jmin = __reduce_min_sync(kFull, key == mkey ? j : 0xffffffffu);
+        const long long td = clock64();
+        if (ant == 0 && lane == 0 && mkey + jmin != 7u) {
+          g_step_prof[5] += ta - t0;
+          g_step_prof[6] += tb - ta;
+          g_step_prof[7] += (tc - tb) + ((td - tc) << 32);
+        }
+      }
+#endif
       score_window(w, j, vis, step, gant, it, a.ks, best, bestj);
       const float wl = __shfl_sync(kFull, w, T - 1);
       done = (bucket_ceiling(wl) < best) || (wl <= 0.0f);
     }
+#ifdef TACO_STEP_PROFILE
+    const long long t1 = clock64();
+    int nwin = 0;
+#endif
     uint32_t base = (uint32_t)T;
     while (!done) {
+#ifdef TACO_STEP_PROFILE
+      ++nwin;
+#endif
+      if (PREFETCH && !HEAD && base == 0 && lane < 8 && wg > 0.0f)
+        prefetch_window(sw, si, jg, (uint32_t)a.ld, 0u);
       score_window(wg, jg, vis, step, gant, it, a.ks, best, bestj);
       if (PROBE) ++windows;
       // entries after this window have W <= bucket_ceiling(window's last W)
@@ -259,6 +310,9 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
         }
       }
     }
+#ifdef TACO_STEP_PROFILE
+    const long long t2 = clock64();
+#endif
     if (bestj == 0xffffffffu) {
       if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
       return;
@@ -269,6 +323,16 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
     __syncwarp();
     tw.put((int)step, (int32_t)bestj);
     cur = bestj;
+#ifdef TACO_STEP_PROFILE
+    const long long t3 = clock64();
+    if (ant == 0 && lane == 0) {
+      g_step_prof[0] += t1 - t0;
+      g_step_prof[1] += t2 - t1;
+      g_step_prof[2] += t3 - t2;
+      g_step_prof[3] += 1;
+      g_step_prof[4] += nwin;
+    }
+#endif
   }
   tw.flush();
   if (lc.active) {
@@ -675,6 +739,13 @@ static int set_smem(const void *fn, size_t bytes) {
 
 constexpr size_t kSmemBudget = 200 * 1024;
 
+template <bool HEAD, bool PROBE, bool PF>
+static int launch_sorted(const SortedArgs &a, int grid, int threads, size_t smem, cudaStream_t s) {
+  if (set_smem((const void *)k_construct_sorted<HEAD, PROBE, PF>, smem) != TACO_OK) return TACO_ERR_CUDA;
+  k_construct_sorted<HEAD, PROBE, PF><<<grid, threads, smem, s>>>(a);
+  return TACO_OK;
+}
+
 extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, const float *w, int ldw,
                               const float *sw, const uint16_t *si, uint64_t seed, uint32_t iteration,
                               const double *dist, int32_t *tours_out, double *costs_out, int32_t *status,
@@ -762,18 +833,24 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, ldw, sw, si, dist, iteration,
                  tours_out, costs_out, status, scan_count, ks};
     const int grid = (m_local + warps - 1) / warps;
-    const void *fn = T > 0 ? (scan_count ? (const void *)k_construct_sorted<true, true>
-                                         : (const void *)k_construct_sorted<true, false>)
-                           : (scan_count ? (const void *)k_construct_sorted<false, true>
-                                         : (const void *)k_construct_sorted<false, false>);
-    if (set_smem(fn, smem) != TACO_OK) return TACO_ERR_CUDA;
-    if (T > 0) {
-      if (scan_count) k_construct_sorted<true, true><<<grid, warps * 32, smem, s>>>(a);
-      else k_construct_sorted<true, false><<<grid, warps * 32, smem, s>>>(a);
-    } else {
-      if (scan_count) k_construct_sorted<false, true><<<grid, warps * 32, smem, s>>>(a);
-      else k_construct_sorted<false, false><<<grid, warps * 32, smem, s>>>(a);
+    // L1 prefetch of the top candidates' next windows: measured slower on B200
+    // (2.68 vs 2.48 ms at m = 4096; the extra issue slots and L1 pollution
+    // cost more than the L2 latency they hide), so off unless asked for
+    bool prefetch = false;
+    if (const char *ev = getenv("TACO_PREFETCH")) prefetch = atoi(ev) != 0;  // tuning knob
+    const int code = (T > 0 ? 4 : 0) | (scan_count ? 2 : 0) | (prefetch ? 1 : 0);
+    int rc = TACO_ERR_ARG;
+    switch (code) {
+      case 0: rc = launch_sorted<false, false, false>(a, grid, warps * 32, smem, s); break;
+      case 1: rc = launch_sorted<false, false, true>(a, grid, warps * 32, smem, s); break;
+      case 2: rc = launch_sorted<false, true, false>(a, grid, warps * 32, smem, s); break;
+      case 3: rc = launch_sorted<false, true, true>(a, grid, warps * 32, smem, s); break;
+      case 4: rc = launch_sorted<true, false, false>(a, grid, warps * 32, smem, s); break;
+      case 5: rc = launch_sorted<true, false, true>(a, grid, warps * 32, smem, s); break;
+      case 6: rc = launch_sorted<true, true, false>(a, grid, warps * 32, smem, s); break;
+      case 7: rc = launch_sorted<true, true, true>(a, grid, warps * 32, smem, s); break;
     }
+    if (rc != TACO_OK) return rc;
   } else if (variant == TACO_CONSTRUCT_DENSE) {
     if (w == nullptr || ldw < n || (ldw % 4) != 0) return TACO_ERR_ARG;
     if ((reinterpret_cast<uintptr_t>(w) & 15u) != 0) return TACO_ERR_ARG;
@@ -789,6 +866,18 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }
+
+#ifdef TACO_STEP_PROFILE
+extern "C" int taco_step_profile(unsigned long long *host_out, int reset) {
+  if (cudaMemcpyFromSymbol(host_out, g_step_prof, sizeof(unsigned long long) * 8) != cudaSuccess)
+    return TACO_ERR_CUDA;
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_step_prof, z, sizeof(z));
+  }
+  return TACO_OK;
+}
+#endif
 
 extern "C" int taco_starts(int n, int m_local, int ant_offset, uint64_t seed, uint32_t iteration,
                            int32_t *starts_out, void *stream) {
