@@ -7,6 +7,7 @@ without libtaco.so the calls raise.
 
 from __future__ import annotations
 
+import warnings
 import weakref
 
 import numpy as np
@@ -43,7 +44,12 @@ def read_status(status: torch.Tensor) -> tuple[int, int]:
 
 
 def upload(a: np.ndarray, dev, dtype=None) -> torch.Tensor:
-    t = torch.from_numpy(np.ascontiguousarray(a))
+    """Host array -> new device tensor.  The reference's value objects are
+    read-only numpy arrays; they are only read here (copied to the device), so
+    torch's non-writable-array warning does not apply."""
+    with warnings.catch_warnings():
+        warnings.filterwarnings("ignore", message="The given NumPy array is not writable")
+        t = torch.from_numpy(np.ascontiguousarray(a))
     if dtype is not None:
         t = t.to(dtype)
     return t.to(dev, non_blocking=False)
