@@ -38,6 +38,7 @@ extern "C" {
 #define TACO_OK 0
 #define TACO_UNDERFLOW 1          /* colony.py:63-68  NumericalUnderflow          */
 #define TACO_NO_CANDIDATE 2       /* colony.py:149   "selector chose a visited city" */
+#define TACO_DEGENERATE 3         /* model.py:86-91  DegenerateInstance (status[1] = row) */
 #define TACO_ERR_ARG (-1)         /* bad argument (ValueError on the Python side)  */
 #define TACO_ERR_CUDA (-2)        /* CUDA launch / runtime error                  */
 #define TACO_ERR_UNSUPPORTED (-3) /* size outside the compiled kernel variants    */
@@ -166,6 +167,25 @@ int taco_select_replay(int n, int m, int step, uint64_t key0, uint64_t key1,
                        const double *logw, int64_t *current, uint8_t *visited,
                        int64_t *tours, void *workspace, size_t ws_bytes,
                        unsigned *flags_out, int32_t *status, void *stream);
+
+/* edge-weight conventions for taco_coord_instance */
+#define TACO_EDGE_EXACT 0   /* sqrt(dx*dx+dy*dy), unrounded: euclidean_instance model.py:124-134 */
+#define TACO_EDGE_EUC_2D 1  /* TSPLIB EUC_2D  int(sqrt+0.5)   tsplib.py:207-208 */
+#define TACO_EDGE_CEIL_2D 2 /* TSPLIB CEIL_2D ceil(sqrt)      tsplib.py:209-210 */
+#define TACO_EDGE_ATT 3     /* TSPLIB ATT pseudo-Euclidean    tsplib.py:211-214 */
+
+/*
+ * Instance on the device from (n, 2) f64 coordinates:
+ * dist under `edge_weight` and eta = 1/dist off the diagonal, bit-exact with
+ * euclidean_instance (model.py:124-134) / build_instance (model.py:98-119)
+ * through _instance_from_dist (model.py:82-97).  Replaces the host's n^2
+ * Python loop and the 16n^2-byte upload.  A zero off-diagonal distance records
+ * TACO_DEGENERATE with status[1] = smallest such row, unless lenient (then
+ * eta = 1/1e-10 there).  3 <= n <= 65535.
+ */
+int taco_coord_instance(int n, const double *coords, int edge_weight,
+                        double *dist_out, double *eta_out, int lenient,
+                        int32_t *status, void *stream);
 
 /* logw = log(p)/gamma, -inf where p == 0 (selection.py:62-75). */
 int taco_log_weights(int64_t count, const double *p, double gamma,

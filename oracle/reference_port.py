@@ -198,3 +198,45 @@ def instance_arrays(coords: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
     eta = np.zeros_like(dist)
     np.divide(1.0, dist, out=eta, where=off)
     return dist, eta
+
+
+class Degenerate(ValueError):
+    """A zero off-diagonal distance (model.py:22-23, raised at model.py:86-91)."""
+
+
+def _tsplib_weight(dx: float, dy: float, kind: str) -> float:
+    """tsplib.distance (tsplib.py:198-215), scalar Python floats."""
+    if kind == "EUC_2D":
+        return float(int(math.sqrt(dx * dx + dy * dy) + 0.5))
+    if kind == "CEIL_2D":
+        return float(math.ceil(math.sqrt(dx * dx + dy * dy)))
+    if kind == "ATT":
+        r = math.sqrt((dx * dx + dy * dy) / 10.0)
+        t = int(r + 0.5)
+        return float(t + 1 if t < r else t)
+    raise ValueError(f"edge weight type {kind!r} not supported")
+
+
+def coord_instance(coords: np.ndarray, kind: str = "EXACT", lenient: bool = False):
+    """dist/eta from coordinates: "EXACT" = euclidean_instance (model.py:124-134),
+    else build_instance's pair loop (model.py:110-116) under a TSPLIB rule;
+    then _instance_from_dist's eta / zero policy (model.py:82-97)."""
+    pts = np.asarray(coords, dtype=np.float64)
+    n = len(pts)
+    if kind == "EXACT":
+        diff = pts[:, None, :] - pts[None, :, :]
+        dist = np.sqrt((diff * diff).sum(axis=2))
+    else:
+        dist = np.zeros((n, n))
+        for i in range(n):
+            for j in range(i + 1, n):
+                dist[i, j] = dist[j, i] = _tsplib_weight(float(pts[i, 0] - pts[j, 0]),
+                                                         float(pts[i, 1] - pts[j, 1]), kind)
+    off = ~np.eye(n, dtype=bool)
+    zero = (dist == 0.0) & off
+    if zero.any() and not lenient:
+        i, j = np.argwhere(zero)[0]
+        raise Degenerate(f"cities {i} and {j} are at distance 0 (duplicate coordinates)")
+    eta = np.zeros_like(dist)
+    np.divide(1.0, np.where(zero, 1e-10, dist), out=eta, where=off)
+    return dist, eta

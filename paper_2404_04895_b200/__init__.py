@@ -44,6 +44,9 @@ from .pheromone import (
 )
 from .selection import AllZeroWeights, gamma_at, scaled_log_weights
 from .solver import Solver
+from ._device import DeviceInstance, UnsupportedEdgeWeightType, device_build_instance
+
+device_euclidean_instance = DeviceInstance.from_coords
 
 __version__ = "0.1.0"
 
@@ -53,5 +56,6 @@ __all__ = [
     "TourBatch", "TspInstance", "accumulate_increments", "apply_update", "batch_costs",
     "compute_probability_matrix", "construct_tours", "edge_index_matrix", "euclidean_instance",
     "gamma_at", "increment_matrix", "init_starts", "instance_from_distances", "scaled_log_weights",
-    "select_elite", "tour_cost",
+    "select_elite", "tour_cost", "DeviceInstance", "device_euclidean_instance",
+    "device_build_instance", "UnsupportedEdgeWeightType",
 ]

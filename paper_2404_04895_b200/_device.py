@@ -67,13 +67,62 @@ def pad_ld(n: int) -> int:
 # ---------------------------------------------------------------------------
 # per-instance device cache (dist, eta, eta^beta), keyed by object identity
 # ---------------------------------------------------------------------------
+class UnsupportedEdgeWeightType(ValueError):
+    """Edge-weight convention outside EXACT / EUC_2D / CEIL_2D / ATT
+    (tsplib.py:45-46, raised by tsplib.distance tsplib.py:215)."""
+
+
 class DeviceInstance:
+    """dist / eta (and eta^beta per beta) resident on the device."""
+
     def __init__(self, inst, dev):
         self.n = int(inst.n)
         self.dev = dev
+        self.best_known = getattr(inst, "best_known", None)
+        self.name = getattr(inst, "name", "")
         self.dist = upload(np.asarray(inst.dist, dtype=np.float64), dev)
         self.eta = upload(np.asarray(inst.eta, dtype=np.float64), dev)
         self._eta_b: dict[float, torch.Tensor] = {}
+
+    @classmethod
+    def from_coords(cls, coords, edge_weight_type: str = "EXACT", lenient: bool = False,
+                    best_known: float | None = None, name: str = "") -> "DeviceInstance":
+        """Instance built on the device from (n, 2) coordinates, bit-exact with
+        the host builders: ``"EXACT"`` = euclidean_instance (model.py:124-134),
+        ``"EUC_2D"`` / ``"CEIL_2D"`` / ``"ATT"`` = build_instance's TSPLIB
+        conventions (model.py:98-119, tsplib.py:198-215).  Only the 16n bytes of
+        coordinates cross PCIe; the host never holds the n^2 matrices."""
+        from .model import DegenerateInstance
+
+        kind = _lib.EDGE_WEIGHT_TYPES.get(str(edge_weight_type))
+        if kind is None:
+            raise UnsupportedEdgeWeightType(f"edge weight type {edge_weight_type!r} not supported")
+        xy = np.ascontiguousarray(np.asarray(coords, dtype=np.float64))
+        if xy.ndim != 2 or xy.shape[1] != 2:
+            raise ValueError(f"coords must have shape (n, 2), got {xy.shape}")
+        n = xy.shape[0]
+        if n < 3:
+            raise DegenerateInstance(f"need at least 3 cities, got {n}")
+        if n > 65535:
+            raise ValueError(f"n = {n} exceeds the engine's 65535-city limit")
+        dev = device()
+        obj = cls.__new__(cls)
+        obj.n, obj.dev, obj._eta_b = n, dev, {}
+        obj.best_known, obj.name = best_known, name
+        obj.dist = torch.empty((n, n), dtype=torch.float64, device=dev)
+        obj.eta = torch.empty((n, n), dtype=torch.float64, device=dev)
+        status = new_status(dev)
+        check(_lib.load().taco_coord_instance(n, ptr(upload(xy, dev)), kind, ptr(obj.dist), ptr(obj.eta),
+                                              int(bool(lenient)), ptr(status), stream_handle()),
+              "taco_coord_instance")
+        code, row = read_status(status)
+        if code == _lib.TACO_DEGENERATE:
+            # the first row-major zero off the diagonal lies in the smallest such row
+            d = download(obj.dist[row])
+            d[row] = 1.0
+            col = int(np.flatnonzero(d == 0.0)[0])
+            raise DegenerateInstance(f"cities {row} and {col} are at distance 0 (duplicate coordinates)")
+        return obj
 
     def eta_beta(self, beta: float) -> torch.Tensor:
         beta = float(beta)
@@ -84,6 +133,19 @@ class DeviceInstance:
                   "taco_eta_power")
             self._eta_b[beta] = t
         return t
+
+
+def device_build_instance(raw, best_known: float | None = None, lenient: bool = False) -> DeviceInstance:
+    """build_instance (model.py:98-119) on the device from a parsed TSPLIB file:
+    any object with ``dimension``, ``node_coords`` ((id, x, y) triples),
+    ``edge_weight_type`` and ``name`` (the reference's RawTspFile).  The
+    reference's bundled best-known table is not consulted (TSPLIB data is out
+    of scope): pass ``best_known``."""
+    coords = np.array([(float(x), float(y)) for _, x, y in raw.node_coords], dtype=np.float64).reshape(-1, 2)
+    if coords.shape[0] != int(raw.dimension):
+        raise ValueError(f"DIMENSION {raw.dimension} but {coords.shape[0]} coordinates")
+    return DeviceInstance.from_coords(coords, raw.edge_weight_type, lenient=lenient, best_known=best_known,
+                                      name=getattr(raw, "name", ""))
 
 
 _INSTANCES: "weakref.WeakKeyDictionary" = weakref.WeakKeyDictionary()

@@ -17,6 +17,8 @@ LIB_PATH = os.environ.get("TACO_LIB_PATH") or os.path.join(os.path.dirname(os.pa
 TACO_OK = 0
 TACO_UNDERFLOW = 1
 TACO_NO_CANDIDATE = 2
+TACO_DEGENERATE = 3
+EDGE_WEIGHT_TYPES = {"EXACT": 0, "EUC_2D": 1, "CEIL_2D": 2, "ATT": 3}
 TACO_ERR_ARG = -1
 TACO_ERR_CUDA = -2
 TACO_ERR_UNSUPPORTED = -3
@@ -52,6 +54,7 @@ SIGNATURES = {
     "taco_replay_workspace_bytes": (_c_size, [_c_int, _c_int]),
     "taco_select_replay": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u64, _p, _p, _p, _p, _p, _c_size, _p, _p,
                                     _p]),
+    "taco_coord_instance": (_c_int, [_c_int, _p, _c_int, _p, _p, _c_int, _p, _p]),
     "taco_log_weights": (_c_int, [_c_i64, _p, _c_f64, _p, _p]),
     "taco_tour_cost": (_c_int, [_c_int, _c_int, _p, _c_int, _p, _p, _p]),
     "taco_elite_workspace_bytes": (_c_size, [_c_int]),

@@ -123,6 +123,60 @@ __global__ void k_log_weights(int64_t count, const double *p, double gamma, doub
   }
 }
 
+// dist / eta of an unrounded Euclidean instance from (n, 2) coordinates, with
+// numpy's operation order (model.py:124-134 -> _instance_from_dist 82-97):
+// d = sqrt(dx*dx + dy*dy) (two products, one sum, IEEE sqrt), eta = 1.0 / d
+// off the diagonal (1e-10 stands in for a zero distance when lenient).
+// Edge weight of one city pair under the instance builders' conventions:
+//   TACO_EDGE_EXACT  sqrt(dx*dx + dy*dy)           euclidean_instance model.py:124-134
+//   TACO_EDGE_EUC_2D int(sqrt(..) + 0.5)            tsplib.distance tsplib.py:207-208
+//   TACO_EDGE_CEIL_2D ceil(sqrt(..))                tsplib.py:209-210
+//   TACO_EDGE_ATT    r = sqrt(../10); t = int(r+.5); t + (t < r)   tsplib.py:211-214
+// All roundings explicit (no FMA contraction), so the f64 results are the
+// host's bit for bit.  x >= 0 everywhere, so int() truncation == floor.
+__device__ __forceinline__ double edge_weight(double dx, double dy, int kind) {
+  const double ss = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  switch (kind) {
+    case TACO_EDGE_EUC_2D:
+      return trunc(__dadd_rn(__dsqrt_rn(ss), 0.5));
+    case TACO_EDGE_CEIL_2D:
+      return ceil(__dsqrt_rn(ss));
+    case TACO_EDGE_ATT: {
+      const double r = __dsqrt_rn(__ddiv_rn(ss, 10.0));
+      const double t = trunc(__dadd_rn(r, 0.5));
+      return t < r ? __dadd_rn(t, 1.0) : t;
+    }
+    default:
+      return __dsqrt_rn(ss);
+  }
+}
+
+// One grid row per city i (blockIdx.y), columns j across x.  dist/eta follow
+// _instance_from_dist (model.py:82-97): eta = 1/d off the diagonal, 0 on it;
+// a zero off-diagonal distance is DegenerateInstance unless lenient (then
+// eta = 1/1e-10).  status[1] = smallest row holding such a zero (the first
+// row-major zero lies in that row, so the host finds its column).
+__global__ void k_coord_instance(int n, const double *__restrict__ xy, int kind, double *dist, double *eta,
+                                 int lenient, int32_t *status) {
+  const int i = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const size_t t = (size_t)i * n + j;
+  if (i == j) {
+    dist[t] = 0.0;
+    eta[t] = 0.0;
+    return;
+  }
+  const double d = edge_weight(__dsub_rn(xy[2 * i], xy[2 * j]), __dsub_rn(xy[2 * i + 1], xy[2 * j + 1]), kind);
+  dist[t] = d;
+  if (d == 0.0) {
+    if (!lenient) record_status(status, TACO_DEGENERATE, i);
+    eta[t] = __ddiv_rn(1.0, 1e-10);
+  } else {
+    eta[t] = __ddiv_rn(1.0, d);
+  }
+}
+
 static size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static size_t cub_temp_bytes(int m) {
@@ -246,6 +300,17 @@ extern "C" const char *taco_last_cuda_error(void) {
   return taco::g_last_cuda_error == cudaSuccess ? "" : cudaGetErrorString(taco::g_last_cuda_error);
 }
 
+extern "C" int taco_coord_instance(int n, const double *coords, int edge_weight, double *dist_out,
+                                   double *eta_out, int lenient, int32_t *status, void *stream) {
+  if (n < 3 || n > 65535 || coords == nullptr || dist_out == nullptr || eta_out == nullptr) return TACO_ERR_ARG;
+  if (edge_weight < TACO_EDGE_EXACT || edge_weight > TACO_EDGE_ATT) return TACO_ERR_ARG;
+  const dim3 grid((unsigned)((n + 255) / 256), (unsigned)n);
+  k_coord_instance<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(n, coords, edge_weight, dist_out,
+                                                                              eta_out, lenient, status);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
 extern "C" int taco_abi_version(void) { return TACO_ABI_VERSION; }
 
 extern "C" const char *taco_status_string(int code) {
@@ -256,6 +321,8 @@ extern "C" const char *taco_status_string(int code) {
       return "transition-matrix row normalizer is zero or non-finite";
     case TACO_NO_CANDIDATE:
       return "selector chose a visited city";
+    case TACO_DEGENERATE:
+      return "two cities are at distance 0";
     case TACO_ERR_ARG:
       return "invalid argument";
     case TACO_ERR_CUDA:

@@ -5,8 +5,10 @@ studies (IR vs AdaIR, bench.py:162-168) run at GPU scale with the same record
 and summary types: run r uses seed base + r, every iteration yields an
 ``IterationRecord``, and each run a ``RunSummary`` whose mean time excludes
 the first (warm-up) iteration.  Iteration times are device times of one full
-iteration (CUDA events); instance loading is the caller's (TSPLIB parsing is
-outside the accelerated path), so ``inst`` is required.
+iteration (CUDA events).  Synthetic instances (bench.py:127-150) are built
+on the device (``load_instance``); TSPLIB parsing is outside the accelerated
+path, so for ``instance_path`` the caller passes the instance (or
+``device_build_instance(raw)``).
 """
 
 from __future__ import annotations
@@ -17,11 +19,54 @@ from dataclasses import dataclass, replace
 import numpy as np
 import torch
 
+from ._device import DeviceInstance
 from .model import Selection
 from .selection import gamma_at
 from .solver import Solver
 
 CONVERGENCE_BAND = 1e-3  # bench.py:40
+
+
+@dataclass(frozen=True)
+class SyntheticSpec:
+    """Deterministic synthetic instance: n cities, layout kind, coordinate
+    seed (bench.py:55-69)."""
+
+    n: int
+    seed: int = 0
+    kind: str = "clustered"
+    name: str = ""
+
+    def __post_init__(self):
+        if self.kind not in ("clustered", "uniform"):
+            raise ValueError(f"kind must be clustered or uniform, got {self.kind!r}")
+        if not self.name:
+            object.__setattr__(self, "name", f"rnd{self.n}")
+
+
+def synthetic_coords(spec: SyntheticSpec) -> np.ndarray:
+    """The coordinates make_synthetic_instance (bench.py:127-150) writes: the
+    same Generator draws, rounded to one decimal; distances are EUC_2D."""
+    g = np.random.default_rng(spec.seed)
+    if spec.kind == "clustered":
+        n_centers = max(2, spec.n // 25)
+        centers = g.uniform(0.0, 2000.0, size=(n_centers, 2))
+        which = g.integers(0, n_centers, size=spec.n)
+        pts = centers[which] + g.normal(0.0, 60.0, size=(spec.n, 2))
+    else:
+        pts = g.uniform(0.0, 2000.0, size=(spec.n, 2))
+    return np.round(pts, 1)
+
+
+def load_instance(config: "ExperimentConfig") -> DeviceInstance:
+    """load_instance (bench.py:152-159) for synthetic specs, built on the
+    device (EUC_2D).  TSPLIB files are parsed by the caller."""
+    if config.synthetic is None:
+        raise NotImplementedError("TSPLIB parsing is outside the accelerated path: parse the file and pass "
+                                  "the instance (or device_build_instance(raw)) to run_experiment")
+    spec = config.synthetic
+    return DeviceInstance.from_coords(synthetic_coords(spec), "EUC_2D", lenient=config.lenient,
+                                      best_known=config.best_known, name=spec.name)
 
 
 @dataclass(frozen=True)
@@ -78,12 +123,12 @@ def convergence_generation(best_trace: list[float]) -> int:
     return next(it for it, v in enumerate(best_trace) if v <= limit)
 
 
-def run_experiment(config: ExperimentConfig, inst, clock=time.perf_counter,
+def run_experiment(config: ExperimentConfig, inst=None, clock=time.perf_counter,
                    construct: str = "sorted") -> tuple[list[IterationRecord], list[RunSummary]]:
     """construct -> elite -> deposit -> evaporate -> P per iteration on the
     device, `repetitions` runs with seeds base..base+r-1."""
     if inst is None:
-        raise ValueError("pass the TspInstance: instance loading is outside the accelerated path")
+        inst = load_instance(config)
     base = config.params
     bk = config.best_known if config.best_known is not None else getattr(inst, "best_known", None)
     records: list[IterationRecord] = []

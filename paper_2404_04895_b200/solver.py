@@ -72,8 +72,8 @@ class _Timer:
 class Solver:
     """TensorACO on one B200, or sharded over the ranks of a process group.
 
-    instance: a TspInstance (this package's or the reference's) or an (n, n)
-    distance matrix.  params: an AcoParams, or keyword overrides of
+    instance: a TspInstance (this package's or the reference's), an (n, n)
+    distance matrix, or a device instance (``device_euclidean_instance``).  params: an AcoParams, or keyword overrides of
     ``AcoParams.for_instance`` (alpha, beta, rho, n_ants / m, k, selection,
     seed, gamma_schedule, q0_tau, max_iters).
     construct: "sorted" (pruned scan, default) or "dense" (full-row stream).
@@ -88,8 +88,11 @@ class Solver:
 
     def __init__(self, instance, params=None, *, construct: str = "sorted", stream: str = "device",
                  group=None, **overrides):
-        self.inst = _as_instance(instance)
-        self.n = n = int(self.inst.n)
+        if isinstance(instance, _device.DeviceInstance):  # built on the device (from_coords)
+            self.inst, device_inst = None, instance
+        else:
+            self.inst, device_inst = _as_instance(instance), None
+        self.n = n = int(device_inst.n if device_inst is not None else self.inst.n)
         self.params = p = _as_params(params, n, overrides)
         construction_gamma(p, 0)  # validates the mechanism (RW is out of scope)
         if construct not in ("sorted", "dense"):
@@ -112,7 +115,7 @@ class Solver:
         if stream == "replay" and world > 1:
             raise ValueError("the reference-stream replay runs on one GPU")
 
-        self.di = _device.device_instance(self.inst)
+        self.di = device_inst if device_inst is not None else _device.device_instance(self.inst)
         dev = self.dev = self.di.dev
         m, k = p.m, p.k
         self.eta_b = self.di.eta_beta(p.beta)

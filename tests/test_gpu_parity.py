@@ -7,6 +7,8 @@ numpy's exact power set) else <= 1e-12 relative (tolerance well inside the
 1e-6 the north star allows); tour lengths bit-exact (pairwise order).
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -348,3 +350,68 @@ def test_solver_replay_reproduces_reference_runs(golden, name):
             assert np.array_equal(b.costs, golden[f"{key}/costs"])
             assert np.array_equal(s.pheromone().tau, golden[f"{key}/tau"])
             assert length == min(golden[f"{name}/s{seed}/it{i}/costs"].min() for i in range(it + 1))
+
+
+def _golden_instances():
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_instances.npz"))
+
+
+@pytest.mark.parametrize("kind", ["EXACT", "EUC_2D", "CEIL_2D", "ATT"])
+def test_device_instance_matches_reference_builders(kind):
+    """f4: dist/eta built on the device == the reference builders' (golden), bitwise."""
+    z = _golden_instances()
+    dev = taco.device_euclidean_instance(z["conv/coords"], kind)
+    assert np.array_equal(dev.dist.cpu().numpy(), z[f"conv/{kind}/dist"])
+    assert np.array_equal(dev.eta.cpu().numpy(), z[f"conv/{kind}/eta"])
+
+
+def test_device_instance_degenerate_and_lenient():
+    z = _golden_instances()
+    for kind in ("EUC_2D", "EXACT"):
+        with pytest.raises(taco.DegenerateInstance) as e:
+            taco.device_euclidean_instance(z["degen/coords"], kind)
+        assert str(e.value) == str(z[f"degen/{kind}/message"])
+        dev = taco.device_euclidean_instance(z["degen/coords"], kind, lenient=True)
+        assert np.array_equal(dev.dist.cpu().numpy(), z[f"degen/{kind}/dist"])
+        assert np.array_equal(dev.eta.cpu().numpy(), z[f"degen/{kind}/eta"])
+    with pytest.raises(taco.UnsupportedEdgeWeightType):
+        taco.device_euclidean_instance(z["degen/coords"], "EXPLICIT")
+
+
+def test_device_instance_large_and_synthetic():
+    from paper_2404_04895_b200.harness import ExperimentConfig, SyntheticSpec, load_instance
+
+    z = _golden_instances()
+    for key in [k for k in z.files if k.startswith("syn_") and k.endswith("/spec")]:
+        tag = key[: -len("/spec")]
+        n, seed = (int(v) for v in z[key])
+        kind = "clustered" if "clustered" in tag else "uniform"
+        cfg = ExperimentConfig(params=taco.AcoParams(m=4, k=1), synthetic=SyntheticSpec(n=n, seed=seed, kind=kind))
+        inst = load_instance(cfg)
+        assert inst.name == f"rnd{n}"
+        assert np.array_equal(inst.dist.cpu().numpy(), z[f"{tag}/dist"])
+        assert np.array_equal(inst.eta.cpu().numpy(), z[f"{tag}/eta"])
+    g = np.random.default_rng(3)
+    coords = g.uniform(0.0, 2000.0, (3001, 2))  # multi-block rows, n not a multiple of 256
+    host = taco.euclidean_instance(coords)
+    dev = taco.device_euclidean_instance(coords)
+    assert np.array_equal(dev.dist.cpu().numpy(), host.dist)
+    assert np.array_equal(dev.eta.cpu().numpy(), host.eta)
+    # a Solver on the device instance runs exactly like one on the host instance
+    coords = g.uniform(0.0, 2000.0, (90, 2))
+    params = taco.AcoParams(m=20, k=2, selection="ir", seed=2)
+    a = taco.Solver(taco.device_euclidean_instance(coords), params).run(5)
+    b = taco.Solver(taco.euclidean_instance(coords), params).run(5)
+    assert a[1] == b[1] and np.array_equal(a[0], b[0])
+
+
+def test_device_build_instance_from_raw_tsplib_record():
+    from types import SimpleNamespace
+
+    z = _golden_instances()
+    coords = z["conv/coords"]
+    raw = SimpleNamespace(name="x37", dimension=len(coords), edge_weight_type="ATT",
+                          node_coords=tuple((i + 1, float(x), float(y)) for i, (x, y) in enumerate(coords)))
+    inst = taco.device_build_instance(raw, best_known=123.0)
+    assert inst.name == "x37" and inst.best_known == 123.0
+    assert np.array_equal(inst.dist.cpu().numpy(), z["conv/ATT/dist"])

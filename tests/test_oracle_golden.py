@@ -6,6 +6,8 @@
   vectors, and its pairwise-sum restatement equals numpy's ndarray.sum.
 """
 
+import os
+
 import numpy as np
 import pytest
 
@@ -137,3 +139,42 @@ def test_product_rule_agrees_with_log_rule_on_shared_uniforms():
     a = fastpath.build_tours(w, 2, 0, np.arange(32))
     b = fastpath.log_rule_tours(p, 1.0, 2, 0, np.arange(32))
     assert (a != b).sum() == 0
+
+
+# ---------------------------------------------------------------------------
+# instance builders, pinned on tests/golden/reference_instances.npz
+# ---------------------------------------------------------------------------
+def _instances():
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "reference_instances.npz"))
+
+
+@pytest.mark.parametrize("kind", ["EXACT", "EUC_2D", "CEIL_2D", "ATT"])
+def test_oracle_coord_instance_matches_reference(kind):
+    z = _instances()
+    dist, eta = ref.coord_instance(z["conv/coords"], kind)
+    assert np.array_equal(dist, z[f"conv/{kind}/dist"])
+    assert np.array_equal(eta, z[f"conv/{kind}/eta"])
+
+
+def test_oracle_degenerate_instance_matches_reference():
+    z = _instances()
+    for kind in ("EUC_2D", "EXACT"):
+        with pytest.raises(ref.Degenerate) as e:
+            ref.coord_instance(z["degen/coords"], kind)
+        assert str(e.value) == str(z[f"degen/{kind}/message"])
+        dist, eta = ref.coord_instance(z["degen/coords"], kind, lenient=True)
+        assert np.array_equal(dist, z[f"degen/{kind}/dist"]) and np.array_equal(eta, z[f"degen/{kind}/eta"])
+
+
+def test_synthetic_coords_match_reference():
+    from paper_2404_04895_b200.harness import SyntheticSpec, synthetic_coords
+
+    z = _instances()
+    for kind in ("clustered", "uniform"):
+        key = [k for k in z.files if k.startswith(f"syn_{kind}") and k.endswith("/spec")][0]
+        tag = key[: -len("/spec")]
+        n, seed = (int(v) for v in z[key])
+        coords = synthetic_coords(SyntheticSpec(n=n, seed=seed, kind=kind))
+        assert np.array_equal(coords, z[f"{tag}/coords"])
+        dist, eta = ref.coord_instance(coords, "EUC_2D")
+        assert np.array_equal(dist, z[f"{tag}/dist"]) and np.array_equal(eta, z[f"{tag}/eta"])
