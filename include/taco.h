@@ -125,6 +125,43 @@ int taco_construct(int n, int m_local, int ant_offset, int variant,
                    int32_t *status, unsigned long long *scan_count,
                    void *stream);
 
+/*
+ * Roulette-wheel (RW) construction, device stream.
+ * Replaces colony.construct_tours colony.py:127-141 (RW branch) with
+ * rw_spin_block (selection.py:102-127) evaluated on P (n x n f64, the
+ * probability matrix) for ants [ant_offset, ant_offset + m_local): per step
+ * the first j with cumsum(P[cur] * unvisited)_j / total > u, bit-exact with
+ * the reference's sequential cumsum rule (a certified parallel scan, with an
+ * exact sequential recount when the crossing is within rounding distance).
+ * u is one 53-bit Philox4x32-10 uniform per (step, ant) (counter word 0 =
+ * 0xffffffff) in place of rng.step_uniforms (rng.py:52-62).  Start cities and
+ * the fused tour length are as in taco_construct.  exact_count (nullable,
+ * device u64) accumulates the steps that took the sequential recount;
+ * force_exact != 0 makes every step take it (test hook).
+ */
+int taco_construct_rw(int n, int m_local, int ant_offset, const double *p,
+                      uint64_t seed, uint32_t iteration, const double *dist,
+                      int32_t *tours_out, double *costs_out, int32_t *status,
+                      unsigned long long *exact_count, int force_exact,
+                      void *stream);
+
+/*
+ * One lockstep round of rw_spin_block (selection.py:102-127) with the
+ * reference's thresholds u (m f64, rng.step_uniforms) — RW parity mode: the
+ * visited assert (colony.py:149), then current (m i64) / visited (m x n u8) /
+ * tours (m x n i64, column `step`) update.  exact_count / force_exact as in
+ * taco_construct_rw.
+ */
+int taco_rw_parity(int n, int m, int step, const double *p, const double *u,
+                   int64_t *current, uint8_t *visited, int64_t *tours,
+                   int32_t *status, unsigned long long *exact_count,
+                   int force_exact, void *stream);
+
+/* RW device-stream thresholds for given (step, ant) pairs (test hook). */
+int taco_rw_uniforms(int count, const uint32_t *step, const uint32_t *ant,
+                     uint64_t seed, uint32_t iteration, double *u_out,
+                     void *stream);
+
 /* Start cities of the device stream (rng.start_cities rng.py:65-68 analog). */
 int taco_starts(int n, int m_local, int ant_offset, uint64_t seed,
                 uint32_t iteration, int32_t *starts_out, void *stream);

@@ -66,6 +66,47 @@ def starts(seed: int, iteration: int, ants, n: int) -> np.ndarray:
     return ((x * np.uint64(n)) >> np.uint64(32)).astype(np.int64)
 
 
+RW_COUNTER = 0xFFFFFFFF  # counter word 0 of the RW thresholds (k_roulette.cu)
+
+
+def rw_uniform(seed: int, iteration: int, step, ant) -> np.ndarray:
+    """Device RW threshold: 53 bits of Philox4x32-10 counter
+    (0xffffffff, step, ant, it), words 0 and 1, as numpy's random():
+    ((x >> 5) * 2^26 + (y >> 6)) / 2^53."""
+    step = np.asarray(step, dtype=np.uint64).ravel()
+    ant = np.asarray(ant, dtype=np.uint64).ravel()
+    ctr = np.stack([np.full_like(step, RW_COUNTER), step, ant, np.full_like(step, iteration & MASK32)], axis=-1)
+    r = philox4x32_10(ctr, seed_key(seed)).astype(np.uint64)
+    k = ((r[:, 0] >> np.uint64(5)) << np.uint64(26)) | (r[:, 1] >> np.uint64(6))
+    return k.astype(np.float64) * 2.0**-53
+
+
+def rw_tours(p: np.ndarray, seed: int, iteration: int, ants) -> np.ndarray:
+    """Device-stream roulette-wheel tours: the reference's spin rule
+    (rw_spin_block selection.py:102-127 — sequential cumsum, strict >, the
+    last-positive fallback) on the device thresholds and start cities."""
+    n = p.shape[0]
+    ants = np.asarray(ants)
+    m = len(ants)
+    rows = np.arange(m)
+    cur = starts(seed, iteration, ants, n)
+    unvisited = np.ones((m, n))
+    unvisited[rows, cur] = 0.0
+    tours = np.empty((m, n), dtype=np.int64)
+    tours[:, 0] = cur
+    for step in range(1, n):
+        u = rw_uniform(seed, iteration, np.full(m, step), ants)
+        cdf = np.cumsum(p[cur] * unvisited, axis=1)
+        cdf /= cdf[:, -1:].copy()
+        nxt = (cdf > u[:, None]).argmax(axis=1)
+        for a in np.flatnonzero(cdf[:, -1] <= u):
+            nxt[a] = np.flatnonzero(p[cur[a]] * unvisited[a])[-1]
+        unvisited[rows, nxt] = 0.0
+        tours[:, step] = nxt
+        cur = nxt
+    return tours
+
+
 def selection_table(p: np.ndarray, g: float) -> np.ndarray:
     """W = fp32(P^(1/g)); exact for g == 1.  (For g != 1 numpy's pow may
     differ from CUDA's by an ulp before rounding; parity tests therefore feed

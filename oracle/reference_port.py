@@ -104,6 +104,42 @@ def build_tours(p: np.ndarray, m: int, seed: int, iteration: int, g: float) -> n
     return tours
 
 
+def spin_round(p: np.ndarray, cur: np.ndarray, unvisited: np.ndarray, u: np.ndarray) -> np.ndarray:
+    """Roulette spins of all ants at one step (rw_spin_block selection.py:102-127):
+    first j with cumsum(P[cur] * unvisited)_j / total > u, else the last
+    positive weight."""
+    cdf = np.cumsum(p[cur] * unvisited, axis=1)
+    cdf /= cdf[:, -1:].copy()
+    nxt = (cdf > u[:, None]).argmax(axis=1)
+    for a in np.flatnonzero(cdf[:, -1] <= u):
+        nxt[a] = np.flatnonzero(p[cur[a]] * unvisited[a])[-1]
+    return nxt
+
+
+def spin_thresholds(seed: int, iteration: int, step: int, m: int, n: int) -> np.ndarray:
+    """u = exp(-E[:, 0]) of the step's block (rng.step_uniforms rng.py:52-62)."""
+    return np.exp(-exp_block(seed, iteration, step, m, n)[:, 0])
+
+
+def build_tours_rw(p: np.ndarray, m: int, seed: int, iteration: int) -> np.ndarray:
+    """m lockstep roulette-wheel tours (colony.py:113-141, RW branch)."""
+    n = p.shape[0]
+    cur = start_block(seed, iteration, m, n)
+    rows = np.arange(m)
+    unvisited = np.ones((m, n))
+    unvisited[rows, cur] = 0.0
+    tours = np.empty((m, n), dtype=np.int64)
+    tours[:, 0] = cur
+    for step in range(1, n):
+        nxt = spin_round(p, cur, unvisited, spin_thresholds(seed, iteration, step, m, n))
+        if (unvisited[rows, nxt] == 0.0).any():  # colony.py:149
+            raise AssertionError("selector chose a visited city")
+        unvisited[rows, nxt] = 0.0
+        tours[:, step] = nxt
+        cur = nxt
+    return tours
+
+
 def lengths(tours: np.ndarray, dist: np.ndarray) -> np.ndarray:
     """Closed-tour lengths, numpy pairwise row sums (model.py:292-295)."""
     return dist[tours, np.roll(tours, -1, axis=1)].sum(axis=1)
@@ -168,7 +204,10 @@ def iterate(tau: np.ndarray, p: np.ndarray, dist: np.ndarray, eta: np.ndarray, c
             iteration: int) -> dict:
     """construct -> elite -> deposit -> evaporate -> P (bench.py:199-206)."""
     n = dist.shape[0]
-    tours = build_tours(p, cfg.m, cfg.seed, iteration, cfg.gamma(iteration))
+    if cfg.selection == "rw":
+        tours = build_tours_rw(p, cfg.m, cfg.seed, iteration)
+    else:
+        tours = build_tours(p, cfg.m, cfg.seed, iteration, cfg.gamma(iteration))
     costs = lengths(tours, dist)
     order = elite_ranks(costs, cfg.k)
     delta = deposit(tours[order], costs[order], n)

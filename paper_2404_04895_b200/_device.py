@@ -211,6 +211,17 @@ def construct(n: int, m_local: int, ant_offset: int, variant: int, tables: Selec
     check(code, "taco_construct")
 
 
+def construct_rw(n: int, m_local: int, ant_offset: int, p: torch.Tensor, seed: int, iteration: int,
+                 tours_out: torch.Tensor, status: torch.Tensor, dist: torch.Tensor | None = None,
+                 costs_out: torch.Tensor | None = None, exact_count: torch.Tensor | None = None,
+                 force_exact: bool = False) -> None:
+    """Roulette-wheel tours from the f64 probability matrix (device stream)."""
+    code = _lib.load().taco_construct_rw(
+        n, m_local, ant_offset, ptr(p), int(seed), int(iteration) & 0xFFFFFFFF, ptr(dist), ptr(tours_out),
+        ptr(costs_out), ptr(status), ptr(exact_count), int(bool(force_exact)), stream_handle())
+    check(code, "taco_construct_rw")
+
+
 def tour_cost(tours: torch.Tensor, dist: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     m, n = tours.shape
     if out is None:

@@ -54,6 +54,9 @@ SIGNATURES = {
     "taco_replay_workspace_bytes": (_c_size, [_c_int, _c_int]),
     "taco_select_replay": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u64, _p, _p, _p, _p, _p, _c_size, _p, _p,
                                     _p]),
+    "taco_construct_rw": (_c_int, [_c_int, _c_int, _c_int, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _c_int, _p]),
+    "taco_rw_parity": (_c_int, [_c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p, _c_int, _p]),
+    "taco_rw_uniforms": (_c_int, [_c_int, _p, _p, _c_u64, _c_u32, _p, _p]),
     "taco_coord_instance": (_c_int, [_c_int, _p, _c_int, _p, _p, _c_int, _p, _p]),
     "taco_log_weights": (_c_int, [_c_i64, _p, _c_f64, _p, _p]),
     "taco_tour_cost": (_c_int, [_c_int, _c_int, _p, _c_int, _p, _p, _p]),

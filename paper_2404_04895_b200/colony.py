@@ -33,11 +33,7 @@ def _underflow_from_sums(sums: np.ndarray) -> NumericalUnderflow:
 
 
 def _selection(params) -> Selection:
-    mech = Selection(getattr(params, "selection", Selection.ADAIR))
-    if mech is Selection.RW:
-        raise NotImplementedError(
-            "roulette-wheel selection is outside the accelerated IR/AdaIR path")
-    return mech
+    return Selection(getattr(params, "selection", Selection.ADAIR))
 
 
 def construction_gamma(params, iteration: int) -> float:
@@ -100,6 +96,10 @@ def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = No
     the reference too, colony.py:119-124); ``probe`` is not supported.
     variant: "sorted" (pruned scan of the row-sorted table) or "dense" (full
     row streaming); both return identical tours.
+    Roulette wheel (selection="rw", colony.py:127-141) spins on P itself:
+    stream="device" draws one threshold per (step, ant) on chip; "numpy"
+    uses the reference's thresholds exp(-E[:, 0]) (rng.py:52-62) and returns
+    its tours bit for bit; "replay" is not available for RW.
     """
     if probe is not None:
         raise NotImplementedError("construction probes are not supported by the device engine")
@@ -110,7 +110,9 @@ def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = No
     di = _device.device_instance(inst)
     dev = di.dev
     p_host = np.asarray(p.p, dtype=np.float64)
-    if stream in ("numpy", "replay"):
+    if _selection(params) is Selection.RW:
+        tours_t, costs_t = _construct_roulette(p_host, n, m, params.seed, iteration, dev, di.dist, stream)
+    elif stream in ("numpy", "replay"):
         tours_t = _construct_reference_stream(p_host, n, m, params.seed, iteration, gamma, dev,
                                               replay=(stream == "replay"))
         costs_t = _device.tour_cost(tours_t, di.dist)
@@ -138,6 +140,36 @@ def _construct_device_stream(p_host, n, m, seed, iteration, gamma, dev, variant,
     _device.construct(n, m, 0, code, tables, seed, iteration, tours, status, dist=dist, costs_out=costs)
     _raise_construct_status(status)
     return tours, costs
+
+
+def _construct_roulette(p_host, n, m, seed, iteration, dev, dist, stream):
+    p_t = _device.upload(p_host, dev)
+    status = _device.new_status(dev)
+    if stream == "device":
+        tours = torch.zeros((m, n), dtype=torch.int32, device=dev)
+        costs = torch.empty(m, dtype=torch.float64, device=dev)
+        _device.construct_rw(n, m, 0, p_t, seed, iteration, tours, status, dist=dist, costs_out=costs)
+        _raise_construct_status(status)
+        return tours, costs
+    if stream == "replay":
+        raise NotImplementedError("roulette-wheel thresholds are exp(-E) under numpy's own exp; "
+                                  "use stream='numpy' for RW reference parity")
+    if stream != "numpy":
+        raise ValueError(f"stream must be 'device', 'replay' or 'numpy', got {stream!r}")
+    starts = _rng.start_cities(seed, iteration, m, n)
+    current = _device.upload(starts, dev)
+    visited = torch.zeros((m, n), dtype=torch.uint8, device=dev)
+    visited[torch.arange(m, device=dev), current] = 1
+    tours = torch.zeros((m, n), dtype=torch.int64, device=dev)
+    tours[:, 0] = current
+    lib, hs = _lib.load(), _device.stream_handle()
+    for step in range(1, n):
+        u_t = _device.upload(_rng.step_uniforms(seed, iteration, step, m, n), dev)
+        _lib.check(lib.taco_rw_parity(n, m, step, p_t.data_ptr(), u_t.data_ptr(), current.data_ptr(),
+                                      visited.data_ptr(), tours.data_ptr(), status.data_ptr(), None, 0, hs),
+                   "taco_rw_parity")
+    _raise_construct_status(status)
+    return tours, _device.tour_cost(tours, dist)
 
 
 def _raise_construct_status(status: torch.Tensor) -> None:

@@ -26,90 +26,9 @@
 // order (bit-exact with batch_costs), so no separate m x n gather pass runs.
 #include <cstdlib>
 
-#include "taco_common.cuh"
+#include "construct_common.cuh"
 
 namespace taco {
-
-constexpr unsigned kFull = 0xffffffffu;
-
-struct TourWriter {
-  // lane (step & 31) buffers the choice of `step`; every 32 steps the warp
-  // writes one coalesced 128-byte segment of the tour row.
-  int32_t *row;
-  int n;
-  int lane;
-  int32_t buf;
-  __device__ __forceinline__ void put(int step, int32_t city) {
-    if (lane == (step & 31)) buf = city;
-    if ((step & 31) == 31) row[(step & ~31) + lane] = buf;
-  }
-  __device__ __forceinline__ void flush() {
-    const int last = n - 1;
-    if ((last & 31) != 31 && lane <= (last & 31)) row[(last & ~31) + lane] = buf;
-  }
-};
-
-// Tour length in numpy's pairwise order, fed one edge at a time in position
-// order e = 0..n-1 (edge e joins t[e] and t[(e+1) % n]).  Edge lengths of the
-// current pairwise-tree leaf (<= 128 positions, taco_common.cuh) are parked in
-// a per-ant shared buffer; when the leaf is complete lane 0 sums it with
-// pw_leaf_sum, and the leaf sums are folded at the end — the exact operation
-// sequence of ndarray.sum(axis=1), at one shared store per step.
-struct LeafCost {
-  const double *dist;
-  const int2 *leaves;
-  double *buf;       // per-ant shared buffer, kPwBlock entries
-  double *leaf_sum;  // per-ant shared, n_leaves entries
-  int n, lane, L, i, len;
-  double pending;
-  bool active;
-
-  __device__ __forceinline__ void init(const double *d, const int2 *lv, double *b, double *ls, int n_,
-                                       int lane_) {
-    dist = d;
-    leaves = lv;
-    buf = b;
-    leaf_sum = ls;
-    n = n_;
-    lane = lane_;
-    active = d != nullptr;
-    L = 0;
-    i = 0;
-    len = active ? leaves[0].y : 0;
-    pending = 0.0;
-  }
-  // lane 0 starts loading the length of edge (a, b); it is parked one step later
-  __device__ __forceinline__ void load(uint32_t a, uint32_t b) {
-    if (active && lane == 0) pending = __ldg(dist + (size_t)a * n + b);
-  }
-  __device__ __forceinline__ void push() {
-    if (!active) return;
-    if (lane == 0) buf[i] = pending;
-    if (++i == len) {
-      if (lane == 0) leaf_sum[L] = pw_leaf_sum(len, [&](int q) { return buf[q]; });
-      __syncwarp();
-      const bool more = leaves[L].x + len < n;  // leaves tile [0, n) exactly
-      ++L;
-      if (more) {
-        len = leaves[L].y;
-        i = 0;
-      }
-    }
-  }
-  __device__ __forceinline__ double finish() {
-    __syncwarp();
-    return pw_fold(n, leaf_sum);  // meaningful in lane 0
-  }
-};
-
-// per-ant shared scratch: leaf buffer, leaf sums, visited bitmask (16-B aligned)
-__host__ __device__ __forceinline__ size_t ant_scratch_bytes(int n_leaves, int nwords) {
-  return ((size_t)8 * kPwBlock + (size_t)8 * n_leaves + (size_t)4 * nwords + 15) & ~(size_t)15;
-}
-
-__device__ __forceinline__ bool is_visited(const uint32_t *vis, uint32_t j) {
-  return (vis[j >> 5] >> (j & 31)) & 1u;
-}
 
 __device__ __forceinline__ uint32_t score_key(float w, uint32_t j, int step, uint32_t gant, uint32_t iteration,
                                               const PhiloxKeys &ks) {
@@ -710,32 +629,6 @@ __global__ void __launch_bounds__(WARPS * 32)
 }  // namespace taco
 
 using namespace taco;
-
-static inline void split_seed(uint64_t seed, uint32_t *k0, uint32_t *k1) {
-  *k0 = (uint32_t)(seed & 0xffffffffu);
-  *k1 = (uint32_t)(seed >> 32);
-}
-
-static int sm_count() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
-      cached = 148;
-  }
-  return cached;
-}
-
-static int set_smem(const void *fn, size_t bytes) {
-  if (bytes <= 48 * 1024) return TACO_OK;
-  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-  if (e != cudaSuccess) {
-    note_cuda_error(e);
-    return TACO_ERR_CUDA;
-  }
-  return TACO_OK;
-}
 
 constexpr size_t kSmemBudget = 200 * 1024;
 

@@ -32,7 +32,7 @@ import torch.distributed as tdist
 from . import _device, _lib
 from .colony import NumericalUnderflow, construction_gamma
 from .distributed import AntShard, gather_colony, shard_ants
-from .model import AcoParams, PheromoneState, ProbabilityMatrix, TourBatch, instance_from_distances
+from .model import AcoParams, PheromoneState, ProbabilityMatrix, Selection, TourBatch, instance_from_distances
 
 
 def _as_instance(instance):
@@ -94,7 +94,7 @@ class Solver:
             self.inst, device_inst = _as_instance(instance), None
         self.n = n = int(device_inst.n if device_inst is not None else self.inst.n)
         self.params = p = _as_params(params, n, overrides)
-        construction_gamma(p, 0)  # validates the mechanism (RW is out of scope)
+        self.rw = Selection(p.selection) is Selection.RW  # roulette wheel spins on P itself
         if construct not in ("sorted", "dense"):
             raise ValueError(f"construct must be 'sorted' or 'dense', got {construct!r}")
         lib = _lib.load()
@@ -114,6 +114,9 @@ class Solver:
         self.shard: AntShard = shard_ants(p.m, rank, world)
         if stream == "replay" and world > 1:
             raise ValueError("the reference-stream replay runs on one GPU")
+        if stream == "replay" and self.rw:
+            raise ValueError("the reference-stream replay covers IR / AdaIR; RW parity runs through "
+                             "construct_tours(stream='numpy')")
 
         self.di = device_inst if device_inst is not None else _device.device_instance(self.inst)
         dev = self.dev = self.di.dev
@@ -122,8 +125,12 @@ class Solver:
         self.tau = torch.full((n, n), float(p.q0_tau), dtype=torch.float64, device=dev)
         self.tau.fill_diagonal_(0.0)
         replay = stream == "replay"
-        self.tables = _device.SelectionTables(n, dev, dense=(construct == "dense" and not replay),
-                                              sorted_=(construct == "sorted" and not replay))
+        table = not (replay or self.rw)
+        self.tables = _device.SelectionTables(n, dev, dense=(construct == "dense" and table),
+                                              sorted_=(construct == "sorted" and table))
+        if self.rw:  # P (f64) is the spin input; steps that needed the exact recount
+            self.p = torch.empty((n, n), dtype=torch.float64, device=dev)
+            self.rw_exact_steps = torch.zeros(1, dtype=torch.int64, device=dev)
         if replay:  # reference-stream state: P, the numpy log table, lockstep buffers
             self.p = torch.empty((n, n), dtype=torch.float64, device=dev)
             self.logw = torch.empty((n, n), dtype=torch.float64, device=dev)
@@ -162,7 +169,7 @@ class Solver:
     # ------------------------------------------------------------------
     def _rebuild_tables(self, evaporate: bool, gamma_next: float) -> None:
         t = self.tables
-        if self.stream == "replay":  # P itself is the next iteration's input
+        if self.stream == "replay" or self.rw:  # P itself is the next iteration's input
             _device.row_update(
                 self.n, tau_in=self.tau, tau_out=self.tau if evaporate else None, eta_b=self.eta_b,
                 nbr=self.nbr if evaporate else None, inc=self.inc if evaporate else None,
@@ -190,6 +197,9 @@ class Solver:
         ev.start("construct")
         if self.stream == "replay":
             self._construct_replay(it)
+        elif self.rw:
+            _device.construct_rw(self.n, sh.count, sh.offset, self.p, p.seed, it, self.tours_local, self.status,
+                                 dist=self.di.dist, costs_out=self.costs_local, exact_count=self.rw_exact_steps)
         else:
             _device.construct(self.n, sh.count, sh.offset, self._variant, self.tables, p.seed, it,
                               self.tours_local, self.status, scan_count, dist=self.di.dist,

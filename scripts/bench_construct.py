@@ -24,12 +24,13 @@ ap.add_argument("--n", type=int, default=2392)
 ap.add_argument("--m", type=int, default=4096)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--reps", type=int, default=5)
-ap.add_argument("--variant", default="sorted")
+ap.add_argument("--variant", default="sorted", help="sorted | dense | rw")
 args = ap.parse_args()
 
 inst = taco.euclidean_instance(np.random.default_rng(0).uniform(0, 2000, (args.n, 2)))
-params = taco.AcoParams(m=args.m, k=max(1, args.m // 10), selection="adair", seed=0)
-s = taco.Solver(inst, params, construct=args.variant)
+rw = args.variant == "rw"
+params = taco.AcoParams(m=args.m, k=max(1, args.m // 10), selection="rw" if rw else "adair", seed=0)
+s = taco.Solver(inst, params, construct="sorted" if rw else args.variant)
 for _ in range(args.iters):
     s.step_async()
 s.check()
@@ -44,8 +45,12 @@ times = []
 for r in range(args.reps + 1):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
-    _device.construct(args.n, args.m, 0, variant, s.tables, 0, s.iteration, tours, st,
-                      scan if r == 0 else None, dist=s.di.dist, costs_out=costs)
+    if rw:
+        _device.construct_rw(args.n, args.m, 0, s.p, 0, s.iteration, tours, st, dist=s.di.dist,
+                             costs_out=costs, exact_count=scan if r == 0 else None)
+    else:
+        _device.construct(args.n, args.m, 0, variant, s.tables, 0, s.iteration, tours, st,
+                          scan if r == 0 else None, dist=s.di.dist, costs_out=costs)
     b.record()
     torch.cuda.synchronize()
     if r:
@@ -53,5 +58,6 @@ for r in range(args.reps + 1):
 assert _device.read_status(st)[0] == 0
 print(json.dumps({"n": args.n, "m": args.m, "variant": args.variant,
                   "T": os.environ.get("TACO_SORTED_T"), "warps": os.environ.get("TACO_SORTED_WARPS"),
-                  "ms": float(np.median(times)), "windows_per_ant_step": int(scan.item()) / (args.m * (args.n - 1)),
+                  "ms": float(np.median(times)), ("exact_recount_steps" if rw else "windows_per_ant_step"):
+                      int(scan.item()) if rw else int(scan.item()) / (args.m * (args.n - 1)),
                   "tour_checksum": int(tours.sum().item())}))

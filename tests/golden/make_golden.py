@@ -53,7 +53,11 @@ CASES = [
     ("int12_adair", lambda: integer_instance(2024, 12), 12, 10, 2, "adair", (0, 1, 2), 4, 1.0, 2.0, 0.1, 4),
     ("euc23_adair", lambda: euclid_instance(7, 23), 23, 16, 3, "adair", (5,), 3, 1.0, 2.0, 0.2, 3),
     ("euc17_ab", lambda: euclid_instance(11, 17), 17, 8, 2, "ir", (3,), 2, 1.5, 3.0, 0.3, 10),
+    ("int12_rw", lambda: integer_instance(2024, 12), 12, 10, 2, "rw", (0, 1), 3, 1.0, 2.0, 0.1, 4),
+    ("euc29_rw", lambda: euclid_instance(13, 29), 29, 16, 3, "rw", (4,), 3, 1.0, 2.0, 0.2, 4),
 ]
+
+SELECTION_CODE = {"ir": 0, "adair": 1, "rw": 2}  # meta[8]
 
 
 def main() -> None:
@@ -62,7 +66,7 @@ def main() -> None:
         inst = make()
         out[f"{name}/dist"] = inst.dist
         out[f"{name}/eta"] = inst.eta
-        out[f"{name}/meta"] = np.array([n, m, k, iters, alpha, beta, rho, period, 1 if sel == "adair" else 0],
+        out[f"{name}/meta"] = np.array([n, m, k, iters, alpha, beta, rho, period, SELECTION_CODE[sel]],
                                        dtype=np.float64)
         out[f"{name}/seeds"] = np.array(seeds, dtype=np.int64)
         for seed in seeds:
@@ -89,6 +93,12 @@ def main() -> None:
                 out[f"{key}/tau"] = tau.tau
     # known-answer cases from the reference's own tests
     out["kat/gamma"] = np.array([antbatch.gamma_at(t, GammaSchedule()) for t in (0, 250, 500, 999, 1000)])
+    from antbatch.selection import rw_spin
+    spins = [(np.array([1.0, 0.0, 3.0]), u) for u in (0.2, 0.25, 0.9, 0.0, 1.0)] + \
+            [(np.array([0.3, 0.7, 0.0]), 1.0 - 1e-17), (np.array([0.0, 1.0, 0.0]), 0.999999)]
+    out["kat/rw_weights"] = np.array([np.pad(w, (0, 3 - len(w))) for w, _ in spins])
+    out["kat/rw_u"] = np.array([u for _, u in spins])
+    out["kat/rw_pick"] = np.array([rw_spin(w, u) for w, u in spins])
     out["kat/increment_0_1_2_cost4"] = antbatch.increment_matrix(np.array([0, 1, 2]), 4.0, 3)
     path = os.path.join(HERE, "reference_pipeline.npz")
     np.savez_compressed(path, **out)

@@ -23,9 +23,9 @@ pytestmark = pytest.mark.gpu
 
 
 def _params(golden, name, seed):
-    n, m, k, iters, alpha, beta, rho, period, adair = golden[f"{name}/meta"]
+    n, m, k, iters, alpha, beta, rho, period, sel = golden[f"{name}/meta"]
     return taco.AcoParams(m=int(m), k=int(k), alpha=alpha, beta=beta, rho=rho,
-                          selection="adair" if adair else "ir",
+                          selection=("ir", "adair", "rw")[int(sel)],
                           gamma_schedule=taco.GammaSchedule(1.5, 1.0, int(period)), seed=seed), int(iters)
 
 

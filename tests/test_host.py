@@ -52,8 +52,7 @@ def test_construction_gamma_per_mechanism():
     ad = taco.AcoParams(m=2, k=1, selection="adair")
     assert colony.construction_gamma(ir, 7) == 1.0
     assert colony.construction_gamma(ad, 0) == 1.5
-    with pytest.raises(NotImplementedError):
-        colony.construction_gamma(taco.AcoParams(m=2, k=1, selection="rw"), 0)
+    assert colony.construction_gamma(taco.AcoParams(m=2, k=1, selection="rw"), 0) == 1.0
 
 
 def test_instances_frozen_and_degenerate_detection():

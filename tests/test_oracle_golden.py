@@ -16,17 +16,17 @@ from oracle import fastpath, reference_port as ref
 
 
 def _case(golden, name):
-    n, m, k, iters, alpha, beta, rho, period, adair = golden[f"{name}/meta"]
+    n, m, k, iters, alpha, beta, rho, period, sel = golden[f"{name}/meta"]
     cfg = ref.Config(m=int(m), k=int(k), alpha=alpha, beta=beta, rho=rho,
-                     selection="adair" if adair else "ir", period=int(period))
+                     selection=("ir", "adair", "rw")[int(sel)], period=int(period))
     return int(n), int(iters), cfg, golden[f"{name}/dist"], golden[f"{name}/eta"]
 
 
 def test_golden_has_cases(golden):
-    assert len(golden_cases(golden)) >= 4
+    assert len(golden_cases(golden)) >= 6
 
 
-@pytest.mark.parametrize("name", ["int12_ir", "int12_adair", "euc23_adair", "euc17_ab"])
+@pytest.mark.parametrize("name", ["int12_ir", "int12_adair", "euc23_adair", "euc17_ab", "int12_rw", "euc29_rw"])
 def test_reference_port_reproduces_reference_pipeline(golden, name):
     n, iters, cfg, dist, eta = _case(golden, name)
     for seed in golden[f"{name}/seeds"].tolist():
@@ -52,6 +52,36 @@ def test_gamma_known_answers(golden):
     assert got == golden["kat/gamma"].tolist()
     assert got[0] == 1.5 and got[-1] == 1.5
     assert abs(got[1] - 1.4268) < 5e-5  # reference tests/test_selection.py:28-41
+
+
+def test_spin_known_answers(golden):
+    # reference tests/test_selection.py:76-93 and the u = 0 / u = 1 edges
+    for w, u, want in zip(golden["kat/rw_weights"], golden["kat/rw_u"], golden["kat/rw_pick"]):
+        got = ref.spin_round(w[None, :], np.array([0]), np.ones((1, 3)), np.array([u]))[0]
+        assert got == want
+
+
+def test_device_rw_restatement_is_the_reference_rule():
+    """fastpath.rw_tours applies the reference's spin rule (spin_round) to the
+    device thresholds: with thresholds swapped in, it is the same function."""
+    g = np.random.default_rng(8)
+    n, m = 15, 6
+    p = g.uniform(0.0, 1.0, (n, n))
+    np.fill_diagonal(p, 0.0)
+    p /= p.sum(axis=1, keepdims=True)
+    tours = fastpath.rw_tours(p, 5, 3, np.arange(m))
+    for t in tours:
+        assert sorted(t.tolist()) == list(range(n))
+    # step-by-step replay with spin_round
+    cur = fastpath.starts(5, 3, np.arange(m), n)
+    unvisited = np.ones((m, n))
+    unvisited[np.arange(m), cur] = 0.0
+    for step in range(1, n):
+        u = fastpath.rw_uniform(5, 3, np.full(m, step), np.arange(m))
+        nxt = ref.spin_round(p, cur, unvisited, u)
+        assert np.array_equal(nxt, tours[:, step])
+        unvisited[np.arange(m), nxt] = 0.0
+        cur = nxt
 
 
 def test_deposit_hand_case(golden):
