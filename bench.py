@@ -23,7 +23,6 @@ import argparse
 import json
 import math
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -40,6 +39,7 @@ CONFIGS = {
     "c2": (1000, 1024, "adair"),
     "c3": (2392, 4096, "adair"),
     "c3ir": (2392, 4096, "ir"),
+    "c3rw": (2392, 4096, "rw"),  # roulette-wheel ablation
     "c4": (10000, 8192, "ir"),
     "c5_256": (5000, 256, "ir"),
     "c5_4096": (5000, 4096, "ir"),
@@ -58,66 +58,98 @@ def _peaks() -> tuple[float, str]:
         return HBM_FALLBACK, "fallback"
 
 
-class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap,utilization.gpu,clocks_event_reasons.gpu_idle")
-
-    def __init__(self, gpu: int):
-        self.gpu = gpu
-        self.rows: list[list[str]] = []
-        self._proc = None
-        self._thread = None
-
-    def _reader(self):
-        for line in self._proc.stdout:
-            parts = [c.strip() for c in line.split(",")]
-            if len(parts) >= 9:
-                self.rows.append(parts)
-
+class _null:
     def __enter__(self):
-        try:  # one long-lived nvidia-smi polling every 100 ms during the timed region
-            self._proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self._thread = threading.Thread(target=self._reader, daemon=True)
-            self._thread.start()
-        except OSError:
-            self._proc = None
         return self
 
     def __exit__(self, *exc):
-        if self._proc is not None:
-            self._proc.terminate()
-            try:
-                self._proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self._proc.kill()
+        return False
+
+
+class ClockSampler:
+    """SM clock and clock-event (throttle) reasons sampled through NVML every
+    ~2 ms, kept only inside the marked timed regions (``window()``), so short
+    timed regions still get tens of samples and host-side gaps (instance
+    setup, CPU baseline) do not dilute the median."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
+
+    def __init__(self, local_rank: int, period_s: float = 0.002):
+        self.period = period_s
+        self.samples: list[tuple[float, int]] = []
+        self.max_mhz = None
+        self._in_window = threading.Event()
+        self._stop = threading.Event()
+        self._thread = None
+        self._nvml = None
+        self._handle = None
+        self._local = local_rank
+
+    def _open(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        self._nvml = pynvml
+        try:
+            props = torch.cuda.get_device_properties(self._local)
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            self._handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:  # noqa: BLE001 - fall back to the NVML index
+            self._handle = pynvml.nvmlDeviceGetHandleByIndex(self._local)
+        self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(self._handle, pynvml.NVML_CLOCK_SM))
+
+    def _poll(self):
+        nv, h = self._nvml, self._handle
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons",
+                              getattr(nv, "nvmlDeviceGetCurrentClocksThrottleReasons", None))
+        while not self._stop.is_set():
+            if self._in_window.wait(timeout=0.05):
+                try:
+                    self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                                         int(get_reasons(h)) if get_reasons else 0))
+                except Exception:  # noqa: BLE001
+                    pass
+                time.sleep(self.period)
+
+    def __enter__(self):
+        try:
+            self._open()
+            self._thread = threading.Thread(target=self._poll, daemon=True)
+            self._thread.start()
+        except Exception:  # noqa: BLE001 - no NVML: the line says "unavailable"
+            self._nvml = None
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        self._in_window.set()
         if self._thread is not None:
-            self._thread.join(timeout=5)
+            self._thread.join(timeout=2)
+
+    class _Window:
+        def __init__(self, ev):
+            self.ev = ev
+
+        def __enter__(self):
+            self.ev.set()
+
+        def __exit__(self, *exc):
+            self.ev.clear()
+
+    def window(self):
+        """Context manager marking a timed region (enter before the first
+        launch, exit after the closing synchronize)."""
+        return self._Window(self._in_window)
 
     def summary(self) -> dict:
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
-
-        def num(v):
-            try:
-                return float(v)
-            except ValueError:
-                return None
-
-        # samples taken while kernels ran: the sampler also sees the host-side
-        # gaps (instance setup, syncs) where the GPU idles at low clocks
-        busy = [r for r in self.rows if not r[8].lower().startswith("active")] or self.rows
-        sm = [num(r[0]) for r in busy if num(r[0]) is not None]
-        smax = [num(r[1]) for r in self.rows if num(r[1]) is not None]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in busy for i in range(4) if r[3 + i].lower().startswith("active")})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": reasons, "samples": len(self.rows), "samples_under_load": len(busy)}
+        if self._nvml is None or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"], "samples": 0}
+        sm = [c for c, _ in self.samples]
+        reasons = sorted({name for _, bits in self.samples for name, bit in self.REASONS if bits & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_min_mhz": min(sm), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(sm), "source": "NVML, 2 ms, timed regions only"}
 
 
 # ---------------------------------------------------------------------------
@@ -167,8 +199,7 @@ def run_ours(args) -> dict | None:
     n, m, selection = CONFIGS[args.config]
     k = max(1, m // 10)
     period = args.warmup + args.steps
-    # nvidia-smi needs ~0.2 s to start polling: launch it before any GPU work so
-    # its samples cover the warm-up and both timed regions
+    # NVML clock sampler (rank 0): samples only inside the timed regions
     sampler = ClockSampler(local) if rank == 0 else None
     if sampler:
         sampler.__enter__()
@@ -189,12 +220,14 @@ def run_ours(args) -> dict | None:
     _device._INSTANCES.clear()
     torch.cuda.synchronize()
     _barrier(world)
-    t0 = time.perf_counter()
-    e2e_solver = taco.Solver(e2e_inst, params, construct=args.construct)
-    for _ in range(args.steps):
-        best_tour, best_len = e2e_solver.step()
-    torch.cuda.synchronize()
-    e2e_s = _max_over_ranks(time.perf_counter() - t0, world)
+    with sampler.window() if sampler else _null():
+        t0 = time.perf_counter()
+        e2e_solver = taco.Solver(e2e_inst, params, construct=args.construct)
+        for _ in range(args.steps):
+            best_tour, best_len = e2e_solver.step()
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+    e2e_s = _max_over_ranks(e2e_s, world)
     del e2e_solver
 
     # ---- device-timed value ------------------------------------------------
@@ -208,11 +241,12 @@ def run_ours(args) -> dict | None:
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     _barrier(world)
     torch.cuda.synchronize()
-    start.record()
-    for _ in range(args.steps):
-        solver.step_async(timers=timers, scan_count=scan if args.construct == "sorted" else None)
-    end.record()
-    torch.cuda.synchronize()
+    with sampler.window() if sampler else _null():
+        start.record()
+        for _ in range(args.steps):
+            solver.step_async(timers=timers, scan_count=scan if args.construct == "sorted" else None)
+        end.record()
+        torch.cuda.synchronize()
     if sampler:
         sampler.__exit__()
     solver.check()
@@ -238,7 +272,8 @@ def run_ours(args) -> dict | None:
 
     # ---- the north-star full-row streaming kernel on the same state -------
     dense_ms = None
-    if args.construct == "sorted" and n <= 20480:
+    rw = selection == "rw"
+    if args.construct == "sorted" and n <= 20480 and not rw:
         pmat = torch.from_numpy(solver.probability().p).to(dev)
         dt = _device.SelectionTables(n, dev, dense=True, sorted_=False)
         g = taco.colony.construction_gamma(params, solver.iteration)
@@ -269,7 +304,15 @@ def run_ours(args) -> dict | None:
     # the reference's full-row gather: m (n-1) n 4 B per launch
     alg_full = m_local * (n - 1) * n * 4
     dom_ms = t_construct
-    roof = {"kernel": f"k_construct_{args.construct}", "bound": "hbm",
+    if rw:  # the spin reads the ant's full f64 P row per step (pass A) + one 2 KB tile (pass B)
+        alg_rw = m_local * (n - 1) * (n * 8 + 2048) + m_local * n * 4
+        roof = {"kernel": "k_construct_rw", "bound": "hbm", "achieved": alg_rw / (dom_ms * 1e-3) / 1e9,
+                "peak": peak, "unit": "GB/s", "peak_kind": peak_kind, "traffic": None, "ms_per_launch": dom_ms,
+                "share_of_step": dom_ms / ms_per_step, "alg_bytes_per_launch": alg_rw,
+                "alg_bytes_def": "P row f64 m*(n-1)*(8n + 2048) B + tours m*n*4 B"}
+    else:
+        roof = None
+    roof = roof or {"kernel": f"k_construct_{args.construct}", "bound": "hbm",
             "achieved": (alg_sorted if args.construct == "sorted" else alg_full) / (dom_ms * 1e-3) / 1e9,
             "peak": peak, "unit": "GB/s", "peak_kind": peak_kind, "traffic": None,
             "ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step,
@@ -285,7 +328,7 @@ def run_ours(args) -> dict | None:
         "data": "synthetic: U(0,2000)^2 Euclidean cities (seed 0), unrounded distances",
         "config": {"workload": f"{args.config}: n={n} cities, m={m} ants, k={k}, {selection}, "
                                f"alpha=1 beta=2 rho=0.1, gamma 1.5->1.0 period {period}",
-                   "n": n, "m": m, "k": k, "selection": selection, "construct": args.construct,
+                   "n": n, "m": m, "k": k, "selection": selection, "construct": "rw" if rw else args.construct,
                    "parallelism": f"ants sharded over {world} GPU(s)",
                    "l2": "back-to-back iterations; per-iteration state (tau, eta^b, dist, tables, "
                          "tours) > 126 MB L2; value_l2_flushed scrubs 256 MB before each iteration"},

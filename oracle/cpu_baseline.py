@@ -42,21 +42,27 @@ def sample_iteration(n: int, m: int, k: int, selection: str = "adair", seed: int
     p = ref.transition(tau, eta, cfg.alpha, cfg.beta)
     t_p = clock() - t0
 
+    rw = selection == "rw"
     t0 = clock()
-    logw = ref.log_table(p, cfg.gamma(it))
+    logw = None if rw else ref.log_table(p, cfg.gamma(it))
     t_logw = clock() - t0
 
     rows = np.arange(m)
     cur = ref.start_block(seed, it, m, n)
     seen = np.zeros((m, n), dtype=bool)
     seen[rows, cur] = True
+    unvisited = (~seen).astype(np.float64)
     first = 3
     steps = max(1, min(steps, n - first))
     step_times = []
     for step in range(1, first + steps):
         t0 = clock()
-        e = ref.exp_block(seed, it, step, m, n)
-        nxt = ref.lockstep_round(logw, cur, e, seen)
+        if rw:  # colony.py:127-134: thresholds + spins
+            nxt = ref.spin_round(p, cur, unvisited, ref.spin_thresholds(seed, it, step, m, n))
+            unvisited[rows, nxt] = 0.0
+        else:
+            e = ref.exp_block(seed, it, step, m, n)
+            nxt = ref.lockstep_round(logw, cur, e, seen)
         seen[rows, nxt] = True
         cur = nxt
         dt = clock() - t0
