@@ -63,20 +63,6 @@ struct SortedArgs {
 
 constexpr int kSortedMaxWarps = 28;
 
-// Pull the first global window (entries off..off+31) of row j into L1: the
-// lanes holding the row head's top entries issue this right after loading
-// them, so when one of them wins the step the next step's window is an L1 hit
-// instead of an L2 round trip on the serial step chain.
-__device__ __forceinline__ void prefetch_window(const float *sw, const uint16_t *si, uint32_t j, uint32_t ld,
-                                                uint32_t off) {
-  const float *pw = sw + (size_t)j * ld + off;
-  const uint16_t *pi = si + (size_t)j * ld + off;
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(pw));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(pw + 31));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(pi));
-  asm volatile("prefetch.global.L1 [%0];" ::"l"(pi + 31));
-}
-
 #ifdef TACO_STEP_PROFILE
 // per-step latency phases of ant 0 (head window, global windows, bookkeeping)
 __device__ unsigned long long g_step_prof[8];
@@ -107,7 +93,10 @@ __device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t
   }
 }
 
-template <bool HEAD, bool PROBE, bool PREFETCH = true>
+// LAZY (with HEAD): the first global window is loaded only when the shared
+// row head did not decide the step; otherwise it is issued before the head is
+// scored so its L2 latency overlaps the shared-memory work.
+template <bool HEAD, bool PROBE, bool LAZY>
 __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const __grid_constant__ SortedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
@@ -160,11 +149,11 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
 #endif
     const uint32_t row = cur * (uint32_t)a.ld;  // < 2^32 for n <= 65535
     // first global window: issued before the row head is scored, so its L2
-    // latency overlaps the shared-memory work
+    // latency overlaps the shared-memory work (unless LAZY)
     uint32_t e = (uint32_t)T + lane;
     float wg = 0.0f;
     uint32_t jg = 0;
-    if (e < un) {
+    if (!(HEAD && LAZY) && e < un) {
       wg = __ldg(sw + (row + e));
       jg = __ldg(si + (row + e));
     }
@@ -177,7 +166,6 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
       if (lane < T) {
         w = cache_w[cur * T + lane];
         j = cache_i[cur * T + lane];
-        if (PREFETCH && w > 0.0f) prefetch_window(sw, si, j, (uint32_t)a.ld, (uint32_t)T);
       }
 #ifdef TACO_STEP_PROFILE
       {
@@ -201,6 +189,10 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
       score_window(w, j, vis, step, gant, it, a.ks, best, bestj);
       const float wl = __shfl_sync(kFull, w, T - 1);
       done = (bucket_ceiling(wl) < best) || (wl <= 0.0f);
+      if (LAZY && !done && e < un) {
+        wg = __ldg(sw + (row + e));
+        jg = __ldg(si + (row + e));
+      }
     }
 #ifdef TACO_STEP_PROFILE
     const long long t1 = clock64();
@@ -211,8 +203,6 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
 #ifdef TACO_STEP_PROFILE
       ++nwin;
 #endif
-      if (PREFETCH && !HEAD && base == 0 && lane < 8 && wg > 0.0f)
-        prefetch_window(sw, si, jg, (uint32_t)a.ld, 0u);
       score_window(wg, jg, vis, step, gant, it, a.ks, best, bestj);
       if (PROBE) ++windows;
       // entries after this window have W <= bucket_ceiling(window's last W)
@@ -726,12 +716,11 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, ldw, sw, si, dist, iteration,
                  tours_out, costs_out, status, scan_count, ks};
     const int grid = (m_local + warps - 1) / warps;
-    // L1 prefetch of the top candidates' next windows: measured slower on B200
-    // (2.68 vs 2.48 ms at m = 4096; the extra issue slots and L1 pollution
-    // cost more than the L2 latency they hide), so off unless asked for
-    bool prefetch = false;
-    if (const char *ev = getenv("TACO_PREFETCH")) prefetch = atoi(ev) != 0;  // tuning knob
-    const int code = (T > 0 ? 4 : 0) | (scan_count ? 2 : 0) | (prefetch ? 1 : 0);
+    // (An L1 prefetch of the top candidates' next windows was measured slower
+    // on B200, 2.68 vs 2.48 ms at m = 4096, and removed.)
+    bool lazy = false;
+    if (const char *ev = getenv("TACO_LAZY")) lazy = atoi(ev) != 0;  // tuning knob
+    const int code = (T > 0 ? 4 : 0) | (scan_count ? 2 : 0) | (lazy && T > 0 ? 1 : 0);
     int rc = TACO_ERR_ARG;
     switch (code) {
       case 0: rc = launch_sorted<false, false, false>(a, grid, warps * 32, smem, s); break;

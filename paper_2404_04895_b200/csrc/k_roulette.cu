@@ -20,10 +20,12 @@
 // certified (probability ~ n * 2^-50 per step) the warp recomputes the exact
 // sequential cumsum — the bit-exact answer either way.
 //
-// Layout: one warp per ant; a row is read in tiles of 256 doubles, lane l
-// owning the 8 contiguous columns [t*256 + 8l, +8) (double2 loads when rows
-// are 16-B aligned).  Pass A writes one total per tile to shared memory; pass
-// B re-reads only the crossing tile.  Device stream: one 53-bit uniform per
+// Layout: one warp per ant; a row is read in tiles of 256 doubles.  Pass A
+// streams the row with coalesced 16-B pair loads (lane l: pairs l, l+32, l+64,
+// l+96 of each tile, all four in flight before any is used), parks per-lane tile
+// partials in shared memory and folds them per tile afterwards, so no
+// cross-lane dependency stalls the loads.  Pass B re-reads only the crossing
+// tile with lane l owning the 8 contiguous columns [t*256 + 8l, +8).  Device stream: one 53-bit uniform per
 // (step, ant) from Philox4x32-10 counter (0xffffffff, step, ant, iteration) —
 // a counter word the IR/AdaIR stream never uses (its word 0 is j/4 < 16384).
 #include "construct_common.cuh"
@@ -31,6 +33,12 @@
 namespace taco {
 
 constexpr int kRwTile = 256;
+constexpr int kRwChunk = 32;  // tiles per pass-A chunk
+
+// per-warp lane partials of one chunk (rows padded to 33 against bank conflicts)
+__host__ __device__ __forceinline__ size_t rw_part_bytes(int ntiles) {
+  return (size_t)8 * 33 * (ntiles < kRwChunk ? ntiles : kRwChunk);
+}
 constexpr uint32_t kRwCounter = 0xffffffffu;
 
 __device__ __forceinline__ double rw_uniform(uint32_t step, uint32_t gant, uint32_t it, const PhiloxKeys &ks) {
@@ -87,6 +95,38 @@ struct BitmaskRow {
     for (int v = 0; v < 8; ++v)
       if ((mask >> v) & 1u) x[v] = 0.0;
   }
+  // masked sum of the four column pairs (j, j+1), j = base + 64h (base even):
+  // all loads are issued before any is consumed.  FULL: the whole tile lies
+  // inside the row (no bounds logic); otherwise addresses are clamped into the
+  // row and out-of-row pairs zeroed afterwards.
+  template <bool VEC, bool FULL>
+  __device__ __forceinline__ double quad_pair_sum(int base) const {
+    double x[8];
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int j = base + 64 * h;
+      const int jc = (FULL || j < n) ? j : 0;
+      if (VEC) {  // n even and rows 16-B aligned
+        const double2 d = __ldg(reinterpret_cast<const double2 *>(row + jc));
+        x[2 * h] = d.x;
+        x[2 * h + 1] = d.y;
+      } else {
+        x[2 * h] = __ldg(row + jc);
+        x[2 * h + 1] = __ldg(row + ((FULL || jc + 1 < n) ? jc + 1 : jc));
+      }
+    }
+    double s[2] = {0.0, 0.0};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      const int j = base + 64 * h;
+      const uint32_t bits = (FULL || j < n) ? (vis[j >> 5] >> (j & 31)) & 3u : 3u;  // j even: one word
+      const bool tail = !FULL && !VEC && j + 1 >= n;
+      const double a0 = (bits & 1u) ? 0.0 : x[2 * h];
+      const double a1 = ((bits & 2u) || tail) ? 0.0 : x[2 * h + 1];
+      s[h & 1] = __dadd_rn(s[h & 1], __dadd_rn(a0, a1));
+    }
+    return __dadd_rn(s[0], s[1]);
+  }
 };
 
 // Masked row of the parity hook: P row + the reference's (m, n) visited bytes.
@@ -99,6 +139,17 @@ struct ByteMaskRow {
   __device__ __forceinline__ void load8(int j0, double x[8]) const {
 #pragma unroll
     for (int v = 0; v < 8; ++v) x[v] = (j0 + v < n && !vis[j0 + v]) ? row[j0 + v] : 0.0;
+  }
+  template <bool VEC, bool FULL>
+  __device__ __forceinline__ double quad_pair_sum(int base) const {
+    double s = 0.0;
+    for (int h = 0; h < 4; ++h) {
+      const int j = base + 64 * h;
+      const double x0 = (j < n && !vis[j]) ? row[j] : 0.0;
+      const double x1 = (j + 1 < n && !vis[j + 1]) ? row[j + 1] : 0.0;
+      s = __dadd_rn(s, __dadd_rn(x0, x1));
+    }
+    return s;
   }
 };
 
@@ -137,18 +188,30 @@ __device__ int rw_exact(const Row &r, int n, double u, int lane) {
 // scratch of ntiles doubles.  *exact is set when the certified fast answer was
 // unavailable (or force_exact) and the sequential path ran.
 template <bool VEC, class Row>
-__device__ int rw_pick(const Row &r, int n, int ntiles, double u, double *tile_tot, int lane, bool force_exact,
-                       bool *exact) {
-  // pass A: tile totals
-  for (int t = 0; t < ntiles; ++t) {
-    double x[8];
-    r.template load8<VEC>(t * kRwTile + lane * 8, x);
-    double s = __dadd_rn(__dadd_rn(__dadd_rn(x[0], x[1]), __dadd_rn(x[2], x[3])),
-                         __dadd_rn(__dadd_rn(x[4], x[5]), __dadd_rn(x[6], x[7])));
-    s = warp_sum_sym(s);
-    if (lane == 0) tile_tot[t] = s;
+__device__ int rw_pick(const Row &r, int n, int ntiles, double u, double *tile_tot, double *part, int lane,
+                       bool force_exact, bool *exact) {
+  // pass A: tile totals.  Each lane sums its four column pairs of a tile
+  // (coalesced 16-B loads, 512 B per warp instruction) into part[t][lane];
+  // no cross-lane work inside the loop, so the loads of consecutive tiles
+  // overlap.  Tiles go in chunks of 32; lane l then folds tile c0 + l.
+  for (int c0 = 0; c0 < ntiles; c0 += kRwChunk) {
+    const int nt = min(kRwChunk, ntiles - c0);
+#pragma unroll 2
+    for (int t = 0; t < nt; ++t) {
+      const int base = (c0 + t) * kRwTile;
+      const double s = base + kRwTile <= n ? r.template quad_pair_sum<VEC, true>(base + 2 * lane)
+                                           : r.template quad_pair_sum<VEC, false>(base + 2 * lane);
+      part[t * 33 + lane] = s;
+    }
+    __syncwarp();
+    if (lane < nt) {  // four independent accumulators: a short dependent chain
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+      for (int i = 0; i < 32; ++i) acc[i & 3] = __dadd_rn(acc[i & 3], part[lane * 33 + i]);
+      tile_tot[c0 + lane] = __dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3]));
+    }
+    __syncwarp();
   }
-  __syncwarp();
   double total = 0.0;
   for (int t = lane; t < ntiles; t += 32) total = __dadd_rn(total, tile_tot[t]);
   total = warp_sum_sym(total);
@@ -227,13 +290,15 @@ struct RwArgs {
 };
 
 __host__ __device__ __forceinline__ size_t rw_warp_bytes(int n_leaves, int nwords, int ntiles) {
-  return ant_scratch_bytes(n_leaves, nwords) + (((size_t)8 * ntiles + 15) & ~(size_t)15);
+  return ant_scratch_bytes(n_leaves, nwords) + (((size_t)8 * ntiles + 15) & ~(size_t)15) + rw_part_bytes(ntiles);
 }
 
 // Shared memory: int2 leaves[n_leaves]; per warp (ant): leaf buffer, leaf
 // sums, visited bitmask, tile totals.
+// __launch_bounds__(128, 7): <= 72 registers, so 28 ants per SM stay resident
+// (the headline colony, 4096 ants on 148 SMs, runs in one wave)
 template <int WARPS, bool VEC>
-__global__ void __launch_bounds__(WARPS * 32) k_construct_rw(const __grid_constant__ RwArgs a) {
+__global__ void __launch_bounds__(WARPS * 32, 7) k_construct_rw(const __grid_constant__ RwArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
   int2 *leaves = reinterpret_cast<int2 *>(smem);
@@ -245,6 +310,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_rw(const __grid_consta
   double *leaf_sum = leaf_buf + kPwBlock;
   uint32_t *vis = reinterpret_cast<uint32_t *>(leaf_sum + a.n_leaves);
   double *tile_tot = reinterpret_cast<double *>(mine + ant_scratch_bytes(a.n_leaves, a.nwords));
+  double *part = tile_tot + ((a.ntiles + 1) & ~1);
   if (threadIdx.x == 0) pw_leaves(n, leaves);
   __syncthreads();
   const int ant = blockIdx.x * WARPS + warp;
@@ -267,7 +333,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_rw(const __grid_consta
     const double u = rw_uniform((uint32_t)step, gant, it, a.ks);
     const BitmaskRow row{a.p + (size_t)cur * n, vis, n};
     bool exact = false;
-    const int j = rw_pick<VEC>(row, n, a.ntiles, u, tile_tot, lane, a.force_exact != 0, &exact);
+    const int j = rw_pick<VEC>(row, n, a.ntiles, u, tile_tot, part, lane, a.force_exact != 0, &exact);
     exact_steps += exact ? 1u : 0u;
     if (j < 0 || is_visited(vis, (uint32_t)j)) {
       if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
@@ -305,11 +371,12 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int lane = threadIdx.x & 31;
   const int a = blockIdx.x * WARPS + warp;
   if (a >= m) return;
-  double *tile_tot = reinterpret_cast<double *>(smem) + (size_t)warp * ntiles;
+  double *tile_tot = reinterpret_cast<double *>(smem + (size_t)warp * (8 * (size_t)ntiles + rw_part_bytes(ntiles)));
+  double *part = tile_tot + ntiles;
   const int64_t cur = current[a];
   const ByteMaskRow row{p + (size_t)cur * n, visited + (size_t)a * n, n};
   bool exact = false;
-  const int j = rw_pick<false>(row, n, ntiles, u[a], tile_tot, lane, force_exact != 0, &exact);
+  const int j = rw_pick<false>(row, n, ntiles, u[a], tile_tot, part, lane, force_exact != 0, &exact);
   if (lane == 0) {
     if (exact && exact_count != nullptr) atomicAdd(exact_count, 1ull);
     if (j < 0) {
@@ -369,7 +436,7 @@ extern "C" int taco_rw_parity(int n, int m, int step, const double *p, const dou
   if (m == 0) return TACO_OK;
   constexpr int WARPS = 8;
   const int ntiles = (n + kRwTile - 1) / kRwTile;
-  const size_t smem = (size_t)8 * ntiles * WARPS;
+  const size_t smem = ((size_t)8 * ntiles + rw_part_bytes(ntiles)) * WARPS;
   if (set_smem((const void *)k_rw_parity<WARPS>, smem) != TACO_OK) return TACO_ERR_CUDA;
   k_rw_parity<WARPS><<<(m + WARPS - 1) / WARPS, WARPS * 32, smem, reinterpret_cast<cudaStream_t>(stream)>>>(
       n, m, step, ntiles, p, u, current, visited, tours, status, exact_count, force_exact);

@@ -13,4 +13,8 @@ ncu --set full --clock-control none --import-source on -k regex:k_row_update -s 
     -o gpurun_out/prof_row_update_$TAG $CMD > gpurun_out/ncu_row_$TAG.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_construct_dense -c 1 \
     -o gpurun_out/prof_construct_dense_$TAG $CMD > gpurun_out/ncu_dense_$TAG.log 2>&1
+RWCMD="python bench.py --config c3rw --steps 1 --warmup 3 --no-cpu-baseline"
+$RWCMD > gpurun_out/plain_rw_$TAG.log 2>&1 || { echo "plain RW run failed"; tail -20 gpurun_out/plain_rw_$TAG.log; exit 1; }
+ncu --set full --clock-control none --import-source on -k regex:k_construct_rw -s 3 -c 1 \
+    -o gpurun_out/prof_construct_rw_$TAG $RWCMD > gpurun_out/ncu_rw_$TAG.log 2>&1
 ls -la gpurun_out/

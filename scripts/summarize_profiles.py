@@ -8,6 +8,7 @@ profiles/<tag>_hotlines.txt
 import collections
 import csv
 import io
+import json
 import os
 import subprocess
 import sys
@@ -70,6 +71,30 @@ with open(os.path.join(out_dir, f"{tag}_kernels.csv"), "w", newline="") as f:
     w.writeheader()
     for rec in kern_rows:
         w.writerow(rec)
+# per-launch DRAM traffic of each captured kernel, read by bench.py for
+# roofline.traffic (dram__bytes_read.sum + dram__bytes_write.sum)
+UNITS = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "KB": 1e3, "MB": 1e6, "GB": 1e9}
+
+
+def _bytes(v):
+    if not v:
+        return None
+    num, _, unit = v.partition(" ")
+    return float(num.replace(",", "")) * UNITS.get(unit.strip(), 1)
+
+
+traffic_path = os.path.join(out_dir, "traffic.json")
+traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+for rec in kern_rows:
+    base = rec["kernel"].replace("void ", "").split("<")[0].split("::")[-1].strip()
+    rd, wr = _bytes(rec.get("dram__bytes_read.sum")), _bytes(rec.get("dram__bytes_write.sum"))
+    if rd is None or wr is None:
+        continue
+    traffic[base] = {"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+                     "duration": rec.get("gpu__time_duration.sum"), "l2_hit_rate": rec.get("lts__t_sector_hit_rate.pct"),
+                     "capture": f"profiles/{tag}_kernels.csv ({rec['report']}, ncu --set full)"}
+with open(traffic_path, "w") as f:
+    json.dump(traffic, f, indent=1, sort_keys=True)
 with open(os.path.join(out_dir, f"{tag}_hotlines.txt"), "w") as f:
     f.write("\n".join(hot))
 print(open(os.path.join(out_dir, f"{tag}_launches.csv")).read())
