@@ -221,25 +221,35 @@ def run_ours(args) -> dict | None:
     dev = _device.device()
 
     # ---- e2e: solve from host buffers through the public API ---------------
-    # timed: host instance -> Solver (H2D of dist + eta), then K x step()
-    # each returning the best tour + length to the host (D2H)
-    e2e_inst = inst
-    warm = taco.Solver(e2e_inst, params, construct=args.construct)
-    for _ in range(args.warmup):
-        warm.step()
-    del warm
+    # headline e2e: host coordinates (pinned) -> device_euclidean_instance
+    # (16n B H2D, dist/eta built on the device) -> Solver -> K x step(), each
+    # step reading status + best length + best tour back in one D2H copy.
+    # e2e_host_instance: the same from a host TspInstance (dist + eta H2D).
+    coords_pinned = torch.from_numpy(coords).pin_memory()
+
+    def e2e_run(make_instance, steps):
+        solver_ = taco.Solver(make_instance(), params, construct=args.construct)
+        out = None
+        for _ in range(steps):
+            out = solver_.step()
+        return out
+
+    def dev_inst():
+        return taco.device_euclidean_instance(coords_pinned.numpy())
+
+    e2e_run(dev_inst, args.warmup)
+    e2e_run(lambda: inst, args.warmup)
     _device._INSTANCES.clear()
     torch.cuda.synchronize()
-    _barrier(world)
-    with sampler.window() if sampler else _null():
-        t0 = time.perf_counter()
-        e2e_solver = taco.Solver(e2e_inst, params, construct=args.construct)
-        for _ in range(args.steps):
-            best_tour, best_len = e2e_solver.step()
-        torch.cuda.synchronize()
-        e2e_s = time.perf_counter() - t0
-    e2e_s = _max_over_ranks(e2e_s, world)
-    del e2e_solver
+    e2e_times = {}
+    for name, make in (("device_instance", dev_inst), ("host_instance", lambda: inst)):
+        _barrier(world)
+        with sampler.window() if (sampler and os.environ.get("TACO_BENCH_E2E_CLOCKS", "1") == "1") else _null():
+            t0 = time.perf_counter()
+            best_tour, best_len = e2e_run(make, args.steps)
+            torch.cuda.synchronize()
+            e2e_times[name] = _max_over_ranks(time.perf_counter() - t0, world)
+        _device._INSTANCES.clear()
 
     # ---- device-timed value ------------------------------------------------
     solver = taco.Solver(inst, params, construct=args.construct)
@@ -247,15 +257,15 @@ def run_ours(args) -> dict | None:
         solver.step_async()
     solver.check()
     torch.cuda.synchronize()
-    timers = {"construct": [], "update": []}
-    scan = torch.zeros(1, dtype=torch.int64, device=dev)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     _barrier(world)
     torch.cuda.synchronize()
+    # timed: K iterations through the Solver's own path (one CUDA-graph replay
+    # per iteration on a single GPU; eager launches when sharded)
     with sampler.window() if sampler else _null():
         start.record()
         for _ in range(args.steps):
-            solver.step_async(timers=timers, scan_count=scan if args.construct == "sorted" else None)
+            solver.step_async()
         end.record()
         torch.cuda.synchronize()
     if sampler:
@@ -264,9 +274,19 @@ def run_ours(args) -> dict | None:
     _barrier(world)
     elapsed_ms = _max_over_ranks(start.elapsed_time(end), world)
     ms_per_step = elapsed_ms / args.steps
+
+    # ---- per-kernel breakdown: eager iterations with events around the
+    # construction and the row update, plus the sorted kernel's window probe
+    timers = {"construct": [], "update": []}
+    scan = torch.zeros(1, dtype=torch.int64, device=dev)
+    bd_steps = min(args.steps, 10)
+    for _ in range(bd_steps):
+        solver.step_async(timers=timers, scan_count=scan if args.construct == "sorted" else None)
+    torch.cuda.synchronize()
+    solver.check()
     t_construct = float(np.mean([a.elapsed_time(b) for a, b in timers["construct"]]))
     t_update = float(np.mean([a.elapsed_time(b) for a, b in timers["update"]]))
-    windows = int(scan.item()) / args.steps
+    windows = int(scan.item()) / bd_steps
 
     # ---- L2-flushed variant: 256 MB scrub before every iteration ----------
     scrub = torch.empty(256 * 2**20, dtype=torch.uint8, device=dev)
@@ -308,6 +328,7 @@ def run_ours(args) -> dict | None:
 
     it_per_s = 1000.0 / ms_per_step
     peak, peak_kind = _peaks()
+    launches_per_iter = 5 + (0 if rw else 1) + (1 if solver.graph else 0)
     m_local = solver.shard.count
     # roofline.achieved = ALGORITHMIC bytes per launch / launch time, with the
     # per-unit figure of SURVEY §8(d): each ant streams its current row of the
@@ -348,14 +369,22 @@ def run_ours(args) -> dict | None:
         "kernel_ms": {"construct": t_construct, "update_p": t_update,
                       "construct_dense_full_row": dense_ms},
         "roofline": roof,
-        "e2e": {"value": args.steps / e2e_s, "unit": "iterations/s",
-                "h2d_bytes_per_step": (2 * n * n * 8) / args.steps,
-                "d2h_bytes_per_step": n * 4 + 8 + 16,
-                "what": "Solver(host instance: dist+eta H2D) + K x step() returning best tour/length (D2H)"},
-        "gpu_launches": args.steps * 6,
-        "gpu_launches_note": ("6 libtaco kernels per iteration: k_construct_sorted (or the lane-group "
-                              "variant), k_elite_rank, k_track_best, k_elite_neighbors, k_row_update, "
-                              "k_row_sort (CUB radix sort only for m > 16384)"),
+        "e2e": {"value": args.steps / e2e_times["device_instance"], "unit": "iterations/s",
+                "h2d_bytes_per_step": (n * 2 * 8) / args.steps,
+                "d2h_bytes_per_step": 32 + n * 4,
+                "what": ("pinned host coords -> device_euclidean_instance -> Solver -> K x step(), each returning "
+                         "status + best length + best tour in one D2H copy")},
+        "e2e_host_instance": {"value": args.steps / e2e_times["host_instance"], "unit": "iterations/s",
+                              "h2d_bytes_per_step": (2 * n * n * 8) / args.steps,
+                              "d2h_bytes_per_step": 32 + n * 4,
+                              "what": "host TspInstance (dist + eta H2D) -> Solver -> K x step()"},
+        "gpu_launches": args.steps * launches_per_iter,
+        "gpu_launches_note": (f"{launches_per_iter} libtaco kernels per iteration: k_construct_"
+                              f"{'rw' if rw else args.construct} (or the lane-group variant), k_elite_rank, "
+                              "k_track_best, k_elite_neighbors, k_row_update"
+                              f"{'' if rw else ', k_row_sort'}{', k_iter_advance' if solver.graph else ''}"
+                              f"{' (+ CUB radix-sort kernels: m > 16384)' if m > 16384 else ''}; "
+                              f"{'replayed as one CUDA graph per iteration' if solver.graph else 'eager launches'}"),
         "best_length": best_len,
     }
     if dense_ms is not None:

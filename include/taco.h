@@ -32,7 +32,7 @@
 extern "C" {
 #endif
 
-#define TACO_ABI_VERSION 1
+#define TACO_ABI_VERSION 2
 
 /* status codes (return values and status[0]) */
 #define TACO_OK 0
@@ -46,6 +46,21 @@ extern "C" {
 /* construction variants for taco_construct */
 #define TACO_CONSTRUCT_SORTED 0 /* pruned scan of the per-row descending table   */
 #define TACO_CONSTRUCT_DENSE 1  /* full-row streaming scan of dense W            */
+
+/*
+ * Device-resident iteration scalars (CUDA-graph replay of Solver steps).
+ * Entry points taking a `const taco_iter_state *state` read the iteration
+ * number / 1/gamma from device memory when state != NULL (ignoring the
+ * by-value argument), so one captured iteration replays unchanged;
+ * taco_iter_advance moves the state to the next iteration on the stream.
+ * inv_gamma is 1/gamma of the selection table built at the END of the
+ * iteration, i.e. for iteration + 1 (the W the next construction reads).
+ */
+typedef struct taco_iter_state {
+  uint32_t iteration;
+  uint32_t reserved;
+  double inv_gamma;
+} taco_iter_state;
 
 int taco_abi_version(void);
 const char *taco_status_string(int code);
@@ -74,6 +89,7 @@ int taco_max_sorted_n(void);
  * (n x n fp32 values / uint16 column indices, each row sorted descending by
  * the W bits above bit 16, stable in the column index).
  * eta_b / p outputs are skipped when want_p == 0 (delta/tau-only modes).
+ * state (nullable): inv_gamma is read from state->inv_gamma.
  */
 int taco_row_update(int n,
                     const double *tau_in, double *tau_out,
@@ -85,7 +101,8 @@ int taco_row_update(int n,
                     double *p_out, double *rowsum_out,
                     float *w_out, int ldw,
                     float *sw_out, uint16_t *si_out,
-                    int32_t *status, void *stream);
+                    int32_t *status, const taco_iter_state *state,
+                    void *stream);
 
 /*
  * Selection table from a given P (construct_tours drop-in, colony.py:116):
@@ -115,7 +132,7 @@ int taco_eta_power(int64_t count, const double *eta, double beta, double *out,
  * pairwise order (model.batch_costs model.py:292-295, bit-exact).
  * scan_count (nullable, device u64) is incremented by the number of 32-entry
  * global table windows the SORTED variant read (traffic probe for the
- * roofline report).
+ * roofline report).  state (nullable): iteration from state->iteration.
  */
 int taco_construct(int n, int m_local, int ant_offset, int variant,
                    const float *w, int ldw,
@@ -123,7 +140,7 @@ int taco_construct(int n, int m_local, int ant_offset, int variant,
                    uint64_t seed, uint32_t iteration,
                    const double *dist, int32_t *tours_out, double *costs_out,
                    int32_t *status, unsigned long long *scan_count,
-                   void *stream);
+                   const taco_iter_state *state, void *stream);
 
 /*
  * Roulette-wheel (RW) construction, device stream.
@@ -137,13 +154,14 @@ int taco_construct(int n, int m_local, int ant_offset, int variant,
  * 0xffffffff) in place of rng.step_uniforms (rng.py:52-62).  Start cities and
  * the fused tour length are as in taco_construct.  exact_count (nullable,
  * device u64) accumulates the steps that took the sequential recount;
- * force_exact != 0 makes every step take it (test hook).
+ * force_exact != 0 makes every step take it (test hook).  state as in
+ * taco_construct.
  */
 int taco_construct_rw(int n, int m_local, int ant_offset, const double *p,
                       uint64_t seed, uint32_t iteration, const double *dist,
                       int32_t *tours_out, double *costs_out, int32_t *status,
                       unsigned long long *exact_count, int force_exact,
-                      void *stream);
+                      const taco_iter_state *state, void *stream);
 
 /*
  * One lockstep round of rw_spin_block (selection.py:102-127) with the
@@ -260,7 +278,16 @@ int taco_elite_neighbors(int n, int k, const void *tours, int tours_is_i64,
 int taco_track_best(int n, const int32_t *tours, const double *costs,
                     const int32_t *order, double *best_cost,
                     int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
-                    void *stream);
+                    const taco_iter_state *state, void *stream);
+
+/*
+ * End of a graph-replayed iteration: state->iteration += 1 and
+ * state->inv_gamma = inv_gamma_table[(state->iteration + 1) % period] (the
+ * table holds 1/gamma_at(t) for t = 0..period-1, computed by the host with
+ * the reference's arithmetic, selection.py:48-59).
+ */
+int taco_iter_advance(taco_iter_state *state, const double *inv_gamma_table,
+                      int period, void *stream);
 
 #ifdef __cplusplus
 }

@@ -169,12 +169,12 @@ def device_instance(inst) -> DeviceInstance:
 def row_update(n, *, tau_in=None, tau_out=None, eta_b=None, nbr=None, inc=None, k=0,
                delta_in=None, delta_out=None, do_evap=False, keep=1.0, want_p=False,
                alpha=1.0, inv_gamma=1.0, p_out=None, rowsum_out=None, w_out=None, ldw=0,
-               sw_out=None, si_out=None, status=None) -> None:
+               sw_out=None, si_out=None, status=None, state=None) -> None:
     code = _lib.load().taco_row_update(
         n, ptr(tau_in), ptr(tau_out), ptr(eta_b), ptr(nbr), ptr(inc), int(k), ptr(delta_in),
         ptr(delta_out), int(bool(do_evap)), float(keep), int(bool(want_p)), float(alpha),
         float(inv_gamma), ptr(p_out), ptr(rowsum_out), ptr(w_out), int(ldw), ptr(sw_out),
-        ptr(si_out), ptr(status), stream_handle())
+        ptr(si_out), ptr(status), ptr(state), stream_handle())
     check(code, "taco_row_update")
 
 
@@ -202,23 +202,23 @@ def selection_table_from_p(p: torch.Tensor, inv_gamma: float, tables: SelectionT
 def construct(n: int, m_local: int, ant_offset: int, variant: int, tables: SelectionTables,
               seed: int, iteration: int, tours_out: torch.Tensor, status: torch.Tensor,
               scan_count: torch.Tensor | None = None, dist: torch.Tensor | None = None,
-              costs_out: torch.Tensor | None = None) -> None:
+              costs_out: torch.Tensor | None = None, state: torch.Tensor | None = None) -> None:
     """Build tours (and, with dist + costs_out, their lengths) on the device."""
     code = _lib.load().taco_construct(
         n, m_local, ant_offset, variant, ptr(tables.w), tables.ldw, ptr(tables.sw), ptr(tables.si),
         int(seed), int(iteration) & 0xFFFFFFFF, ptr(dist), ptr(tours_out), ptr(costs_out), ptr(status),
-        ptr(scan_count), stream_handle())
+        ptr(scan_count), ptr(state), stream_handle())
     check(code, "taco_construct")
 
 
 def construct_rw(n: int, m_local: int, ant_offset: int, p: torch.Tensor, seed: int, iteration: int,
                  tours_out: torch.Tensor, status: torch.Tensor, dist: torch.Tensor | None = None,
                  costs_out: torch.Tensor | None = None, exact_count: torch.Tensor | None = None,
-                 force_exact: bool = False) -> None:
+                 force_exact: bool = False, state: torch.Tensor | None = None) -> None:
     """Roulette-wheel tours from the f64 probability matrix (device stream)."""
     code = _lib.load().taco_construct_rw(
         n, m_local, ant_offset, ptr(p), int(seed), int(iteration) & 0xFFFFFFFF, ptr(dist), ptr(tours_out),
-        ptr(costs_out), ptr(status), ptr(exact_count), int(bool(force_exact)), stream_handle())
+        ptr(costs_out), ptr(status), ptr(exact_count), int(bool(force_exact)), ptr(state), stream_handle())
     check(code, "taco_construct_rw")
 
 

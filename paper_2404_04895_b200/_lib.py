@@ -42,11 +42,11 @@ SIGNATURES = {
     "taco_max_sorted_n": (_c_int, []),
     "taco_row_update": (_c_int, [
         _c_int, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _c_f64, _c_int, _c_f64, _c_f64,
-        _p, _p, _p, _c_int, _p, _p, _p, _p]),
+        _p, _p, _p, _c_int, _p, _p, _p, _p, _p]),
     "taco_selection_table": (_c_int, [_c_int, _p, _c_f64, _p, _c_int, _p, _p, _p]),
     "taco_eta_power": (_c_int, [_c_i64, _p, _c_f64, _p, _p]),
     "taco_construct": (_c_int, [
-        _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _p]),
+        _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _p, _p]),
     "taco_starts": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u32, _p, _p]),
     "taco_uniforms": (_c_int, [_c_int, _p, _p, _p, _c_u64, _c_u32, _p, _p]),
     "taco_philox4x32_10": (_c_int, [_c_int, _p, _p, _p, _p]),
@@ -54,7 +54,8 @@ SIGNATURES = {
     "taco_replay_workspace_bytes": (_c_size, [_c_int, _c_int]),
     "taco_select_replay": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u64, _p, _p, _p, _p, _p, _c_size, _p, _p,
                                     _p]),
-    "taco_construct_rw": (_c_int, [_c_int, _c_int, _c_int, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _c_int, _p]),
+    "taco_construct_rw": (_c_int, [_c_int, _c_int, _c_int, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _c_int, _p,
+                                   _p]),
     "taco_rw_parity": (_c_int, [_c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p, _c_int, _p]),
     "taco_rw_uniforms": (_c_int, [_c_int, _p, _p, _c_u64, _c_u32, _p, _p]),
     "taco_coord_instance": (_c_int, [_c_int, _p, _c_int, _p, _p, _c_int, _p, _p]),
@@ -63,10 +64,11 @@ SIGNATURES = {
     "taco_elite_workspace_bytes": (_c_size, [_c_int]),
     "taco_elite_order": (_c_int, [_c_int, _p, _p, _p, _c_size, _p]),
     "taco_elite_neighbors": (_c_int, [_c_int, _c_int, _p, _c_int, _p, _p, _p, _p, _p]),
-    "taco_track_best": (_c_int, [_c_int, _p, _p, _p, _p, _p, _p, _c_u32, _p]),
+    "taco_track_best": (_c_int, [_c_int, _p, _p, _p, _p, _p, _p, _c_u32, _p, _p]),
+    "taco_iter_advance": (_c_int, [_p, _p, _c_int, _p]),
 }
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 
 class TacoLibraryMissing(ImportError):

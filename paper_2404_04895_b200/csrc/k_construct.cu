@@ -54,6 +54,7 @@ struct SortedArgs {
   const uint16_t *si;
   const double *dist;
   uint32_t iteration;
+  const taco_iter_state *state;  // nullable: iteration from device memory
   int32_t *tours;
   double *costs;
   int32_t *status;
@@ -127,7 +128,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   const int ant = blockIdx.x * warps + warp;
   if (ant >= a.m_local) return;
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
-  const uint32_t it = a.iteration;
+  const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   const uint32_t un = (uint32_t)n;  // n <= 65535, so every row offset fits in 32 bits
   const float *__restrict__ sw = a.sw;
   const uint16_t *__restrict__ si = a.si;
@@ -272,6 +273,7 @@ struct GroupArgs {
   const uint16_t *si;
   const double *dist;
   uint32_t iteration;
+  const taco_iter_state *state;  // nullable: iteration from device memory
   int32_t *tours;
   double *costs;
   int32_t *status;
@@ -340,7 +342,8 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
   const int ant = (blockIdx.x * kGroupWarps + warp) * A + g;
   bool alive = ant < a.m_local;
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
-  const uint32_t it = a.iteration, un = (uint32_t)n, ld = (uint32_t)a.ld;
+  const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
+  const uint32_t un = (uint32_t)n, ld = (uint32_t)a.ld;
   const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, un);
   int32_t *trow = a.tours + (size_t)ant * n;
   GroupCost gc;
@@ -459,6 +462,7 @@ struct DenseArgs {
   const float *w;
   const double *dist;
   uint32_t iteration;
+  const taco_iter_state *state;  // nullable: iteration from device memory
   int32_t *tours;
   double *costs;
   int32_t *status;
@@ -484,7 +488,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   const int ant = blockIdx.x * WARPS + warp;
   if (ant >= a.m_local) return;
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
-  const uint32_t it = a.iteration;
+  const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
   const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, (uint32_t)n);
   __syncwarp();
@@ -632,7 +636,7 @@ static int launch_sorted(const SortedArgs &a, int grid, int threads, size_t smem
 extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, const float *w, int ldw,
                               const float *sw, const uint16_t *si, uint64_t seed, uint32_t iteration,
                               const double *dist, int32_t *tours_out, double *costs_out, int32_t *status,
-                              unsigned long long *scan_count, void *stream) {
+                              unsigned long long *scan_count, const taco_iter_state *state, void *stream) {
   if (n < 3 || n > 65535 || m_local < 0 || ant_offset < 0 || tours_out == nullptr) return TACO_ERR_ARG;
   if (costs_out != nullptr && dist == nullptr) return TACO_ERR_ARG;
   if (m_local == 0) return TACO_OK;
@@ -667,7 +671,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
       const size_t per_warp = (((size_t)4 * nwords * A + 15) & ~(size_t)15) + (size_t)8 * A * (8 + kCostStack);
       const size_t smem = ((8 * (size_t)n_leaves + (size_t)n_leaves + 15) & ~(size_t)15) + per_warp * kGroupWarps;
       if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
-      GroupArgs ga{n, m_local, ant_offset, nwords, n_leaves, ldw, sw, si, dist, iteration,
+      GroupArgs ga{n, m_local, ant_offset, nwords, n_leaves, ldw, sw, si, dist, iteration, state,
                    tours_out, costs_out, status, scan_count, ks};
       const int ants_per_cta = (int)A * kGroupWarps;
       const int grid = (m_local + ants_per_cta - 1) / ants_per_cta;
@@ -713,7 +717,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     if (T < 0 || T > 32 || T >= n) return TACO_ERR_ARG;
     const size_t smem = (((size_t)6 * n * T + 15) & ~(size_t)15) + fixed;
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
-    SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, ldw, sw, si, dist, iteration,
+    SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, ldw, sw, si, dist, iteration, state,
                  tours_out, costs_out, status, scan_count, ks};
     const int grid = (m_local + warps - 1) / warps;
     // (An L1 prefetch of the top candidates' next windows was measured slower
@@ -740,7 +744,8 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     const size_t smem = leaves_bytes + per_ant * WARPS;
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
     if (set_smem((const void *)k_construct_dense<WARPS>, smem) != TACO_OK) return TACO_ERR_CUDA;
-    DenseArgs a{n, m_local, ant_offset, ldw, nwords, n_leaves, w, dist, iteration, tours_out, costs_out, status, ks};
+    DenseArgs a{n, m_local, ant_offset, ldw, nwords, n_leaves, w, dist, iteration, state, tours_out, costs_out,
+                status, ks};
     k_construct_dense<WARPS><<<(m_local + WARPS - 1) / WARPS, WARPS * 32, smem, s>>>(a);
   } else {
     return TACO_ERR_ARG;

@@ -95,7 +95,8 @@ __global__ void k_elite_neighbors(int n, int k, const TourT *__restrict__ tours,
 }
 
 __global__ void k_track_best(int n, const int32_t *tours, const double *costs, const int32_t *order,
-                             double *best_cost, int32_t *best_tour, int32_t *best_iter, uint32_t iteration) {
+                             double *best_cost, int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
+                             const taco_iter_state *state) {
   __shared__ int s_take;
   __shared__ int s_ant;
   if (threadIdx.x == 0) {
@@ -111,7 +112,7 @@ __global__ void k_track_best(int n, const int32_t *tours, const double *costs, c
   __syncthreads();
   if (threadIdx.x == 0) {
     *best_cost = costs[s_ant];
-    *best_iter = (int32_t)iteration;
+    *best_iter = (int32_t)(state != nullptr ? state->iteration : iteration);
   }
 }
 
@@ -273,10 +274,10 @@ extern "C" int taco_elite_neighbors(int n, int k, const void *tours, int tours_i
 
 extern "C" int taco_track_best(int n, const int32_t *tours, const double *costs, const int32_t *order,
                                double *best_cost, int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
-                               void *stream) {
+                               const taco_iter_state *state, void *stream) {
   if (n < 1) return TACO_ERR_ARG;
   k_track_best<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(n, tours, costs, order, best_cost,
-                                                                      best_tour, best_iter, iteration);
+                                                                      best_tour, best_iter, iteration, state);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }
@@ -287,6 +288,21 @@ extern "C" int taco_log_weights(int64_t count, const double *p, double gamma, do
   const int64_t blocks64 = (count + 255) / 256;
   const int grid = (int)(blocks64 < 148 * 16 ? blocks64 : 148 * 16);
   k_log_weights<<<grid, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(count, p, gamma, logw_out);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+namespace taco {
+__global__ void k_iter_advance(taco_iter_state *state, const double *inv_gamma_table, int period) {
+  const uint32_t next = state->iteration + 1u;
+  state->iteration = next;
+  state->inv_gamma = inv_gamma_table[(next + 1u) % (uint32_t)period];
+}
+}  // namespace taco
+
+extern "C" int taco_iter_advance(taco_iter_state *state, const double *inv_gamma_table, int period, void *stream) {
+  if (state == nullptr || inv_gamma_table == nullptr || period < 1) return TACO_ERR_ARG;
+  taco::k_iter_advance<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(state, inv_gamma_table, period);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }

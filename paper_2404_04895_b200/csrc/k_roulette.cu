@@ -281,6 +281,7 @@ struct RwArgs {
   const double *p;
   const double *dist;
   uint32_t iteration;
+  const taco_iter_state *state;  // nullable: iteration from device memory
   int32_t *tours;
   double *costs;
   int32_t *status;
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(WARPS * 32, 7) k_construct_rw(const __grid_con
   const int ant = blockIdx.x * WARPS + warp;
   if (ant >= a.m_local) return;
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
-  const uint32_t it = a.iteration;
+  const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
   const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, (uint32_t)n);
   __syncwarp();
@@ -402,7 +403,8 @@ using namespace taco;
 
 extern "C" int taco_construct_rw(int n, int m_local, int ant_offset, const double *p, uint64_t seed,
                                  uint32_t iteration, const double *dist, int32_t *tours_out, double *costs_out,
-                                 int32_t *status, unsigned long long *exact_count, int force_exact, void *stream) {
+                                 int32_t *status, unsigned long long *exact_count, int force_exact,
+                                 const taco_iter_state *state, void *stream) {
   if (n < 3 || n > 65535 || m_local < 0 || ant_offset < 0 || p == nullptr || tours_out == nullptr)
     return TACO_ERR_ARG;
   if (costs_out != nullptr && dist == nullptr) return TACO_ERR_ARG;
@@ -413,7 +415,7 @@ extern "C" int taco_construct_rw(int n, int m_local, int ant_offset, const doubl
   const int ntiles = (n + kRwTile - 1) / kRwTile;
   const size_t smem = (((size_t)8 * n_leaves + 15) & ~(size_t)15) + rw_warp_bytes(n_leaves, nwords, ntiles) * WARPS;
   if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
-  RwArgs a{n, m_local, ant_offset, nwords, n_leaves, ntiles, p, dist, iteration, tours_out, costs_out,
+  RwArgs a{n, m_local, ant_offset, nwords, n_leaves, ntiles, p, dist, iteration, state, tours_out, costs_out,
            status, exact_count, force_exact, philox_keys(seed)};
   const bool vec = (n % 2 == 0) && ((reinterpret_cast<uintptr_t>(p) & 15u) == 0);
   const int grid = (m_local + WARPS - 1) / WARPS;

@@ -32,8 +32,8 @@ struct RowParams {
   int want_p;
   int p_given;  // tau_in holds P itself: no normalization (selection-table mode)
   double alpha;
-  int gamma_one;
   double inv_gamma;
+  const taco_iter_state *state;  // nullable: inv_gamma from device memory
   double *p_out;
   double *rowsum_out;
   float *w_out;
@@ -59,9 +59,9 @@ __device__ __forceinline__ double numpy_scalar_power(double x, double e) {
   return pow(x, e);
 }
 
-__device__ __forceinline__ float selection_weight(double p, const RowParams &a) {
+__device__ __forceinline__ float selection_weight(double p, double inv_gamma) {
   // W = P^(1/gamma) rounded once to fp32; gamma == 1 is the exact conversion
-  return a.gamma_one ? __double2float_rn(p) : __double2float_rn(pow(p, a.inv_gamma));
+  return inv_gamma == 1.0 ? __double2float_rn(p) : __double2float_rn(pow(p, inv_gamma));
 }
 
 // Shared-memory layout (bytes, all regions 16-B aligned):
@@ -117,6 +117,7 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const bool need_sum = a.want_p && !a.p_given;
+  const double inv_gamma = a.state != nullptr ? a.state->inv_gamma : a.inv_gamma;
   const bool have_delta = (a.nbr != nullptr) || (a.delta_in != nullptr);
 
   // the pairwise tree depends only on n: build it once per CTA
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
       for (int j = tid; j < n; j += BLOCK) {
         const double p = __ddiv_rn(row[j], s);
         if (a.p_out != nullptr) a.p_out[rowoff + j] = p;
-        if (a.w_out != nullptr) a.w_out[(size_t)i * a.ldw + j] = selection_weight(p, a);
+        if (a.w_out != nullptr) a.w_out[(size_t)i * a.ldw + j] = selection_weight(p, inv_gamma);
       }
       if (a.w_out != nullptr)
         for (int j = n + tid; j < a.ldw; j += BLOCK) a.w_out[(size_t)i * a.ldw + j] = 0.0f;
@@ -398,7 +399,7 @@ extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, con
                                double *delta_out, int do_evap, double keep, int want_p, double alpha,
                                double inv_gamma, double *p_out, double *rowsum_out, float *w_out,
                                int ldw, float *sw_out, uint16_t *si_out, int32_t *status,
-                               void *stream) {
+                               const taco_iter_state *state, void *stream) {
   if (n < 3 || n > 65535) return TACO_ERR_ARG;
   if (tau_in == nullptr && (do_evap || want_p || tau_out != nullptr)) return TACO_ERR_ARG;
   if (nbr != nullptr && (inc == nullptr || k < 1)) return TACO_ERR_ARG;
@@ -423,8 +424,8 @@ extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, con
   a.want_p = want_p;
   a.p_given = 0;
   a.alpha = alpha;
-  a.gamma_one = (inv_gamma == 1.0);
   a.inv_gamma = inv_gamma;
+  a.state = state;
   a.p_out = p_out;
   a.rowsum_out = rowsum_out;
   a.w_out = w_out;
@@ -448,7 +449,6 @@ extern "C" int taco_selection_table(int n, const double *p, double inv_gamma, fl
   a.want_p = 1;
   a.p_given = 1;
   a.alpha = 1.0;
-  a.gamma_one = (inv_gamma == 1.0);
   a.inv_gamma = inv_gamma;
   a.w_out = w_out;
   a.ldw = ldw;

@@ -55,9 +55,13 @@ def test_bad_arguments_are_rejected_without_a_gpu(built_lib):
 
     lib = _lib.load(built_lib)
     assert lib.taco_construct(2, 1, 0, 0, None, 0, None, None, 0, 0, None, None, None, None, None,
-                              None) == _lib.TACO_ERR_ARG
+                              None, None) == _lib.TACO_ERR_ARG
     assert lib.taco_row_update(2, None, None, None, None, None, 0, None, None, 0, 1.0, 0, 1.0, 1.0,
-                               None, None, None, 0, None, None, None, None) == _lib.TACO_ERR_ARG
+                               None, None, None, 0, None, None, None, None, None) == _lib.TACO_ERR_ARG
+    assert lib.taco_construct_rw(3, 1, 0, None, 0, 0, None, None, None, None, None, 0, None,
+                                 None) == _lib.TACO_ERR_ARG
+    assert lib.taco_iter_advance(None, None, 1, None) == _lib.TACO_ERR_ARG
+    assert lib.taco_coord_instance(2, None, 0, None, None, 0, None, None) == _lib.TACO_ERR_ARG
     assert lib.taco_log_weights(10, None, 0.0, None, None) == _lib.TACO_ERR_ARG
     with pytest.raises(ValueError):
         _lib.check(_lib.TACO_ERR_ARG, "x")

@@ -415,3 +415,23 @@ def test_device_build_instance_from_raw_tsplib_record():
     inst = taco.device_build_instance(raw, best_known=123.0)
     assert inst.name == "x37" and inst.best_known == 123.0
     assert np.array_equal(inst.dist.cpu().numpy(), z["conv/ATT/dist"])
+
+
+@pytest.mark.parametrize("selection", ["adair", "ir", "rw"])
+def test_graph_replay_equals_eager_solver(selection):
+    """CUDA-graph replay (device iteration state) == eager launches, bit for bit,
+    including run()'s multi-iteration graphs and the remainder."""
+    n, m = 45, 20
+    inst = euclid(12, n)
+    params = taco.AcoParams(m=m, k=3, selection=selection, seed=5, gamma_schedule=taco.GammaSchedule(1.5, 1.0, 6))
+    g = taco.Solver(inst, params, graph=True)
+    e = taco.Solver(inst, params, graph=False)
+    for _ in range(3):  # step(): eager warm-up, then 1-iteration graph replays
+        assert g.step()[1] == e.step()[1]
+        assert np.array_equal(g.last_batch().tours, e.last_batch().tours)
+    bg, be = g.run(19), e.run(19)  # 2 x 8-iteration graph + 3 single replays
+    assert bg[1] == be[1] and np.array_equal(bg[0], be[0])
+    assert g.iteration == e.iteration == 22
+    assert np.array_equal(g.pheromone().tau, e.pheromone().tau)
+    assert np.array_equal(g.last_batch().costs, e.last_batch().costs)
+    assert int(g.best_iter.item()) == int(e.best_iter.item())
