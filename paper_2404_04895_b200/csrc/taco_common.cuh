@@ -67,6 +67,42 @@ __device__ __forceinline__ U4 philox4x32_10(U4 c, const PhiloxKeys &ks) {
   return c;
 }
 
+// Philox4x32-10 on counter (x, step, ant, it) with the x-independent work of
+// rounds 1-2 hoisted: per (step, ant), round 1's ant product and round 2's
+// first product do not depend on x (= city >> 2), so a window of candidates
+// only runs the x-dependent half of those rounds.  Same output bits.
+struct PhiloxStep {
+  uint32_t c1x, c1y;    // round-1 words 0, 1
+  uint32_t hi0_k1, lo0;  // round-2 product of c1x: hi ^ key, lo
+};
+
+__device__ __forceinline__ PhiloxStep philox_step(uint32_t step, uint32_t ant, const PhiloxKeys &ks) {
+  PhiloxStep p;
+  p.c1x = __umulhi(kPhiloxM1, ant) ^ step ^ ks.k0[0];
+  p.c1y = kPhiloxM1 * ant;
+  p.hi0_k1 = __umulhi(kPhiloxM0, p.c1x) ^ ks.k1[1];
+  p.lo0 = kPhiloxM0 * p.c1x;
+  return p;
+}
+
+__device__ __forceinline__ U4 philox4x32_10_x(uint32_t x, uint32_t it, const PhiloxStep &p,
+                                              const PhiloxKeys &ks) {
+  // round 1: only the x product
+  const uint32_t c1z = __umulhi(kPhiloxM0, x) ^ it ^ ks.k1[0];
+  const uint32_t c1w = kPhiloxM0 * x;
+  // round 2: only the c1z product
+  U4 c{__umulhi(kPhiloxM1, c1z) ^ p.c1y ^ ks.k0[1], kPhiloxM1 * c1z, p.hi0_k1 ^ c1w, p.lo0};
+#pragma unroll
+  for (int r = 2; r < 10; ++r) {
+    const uint32_t lo0 = kPhiloxM0 * c.x;
+    const uint32_t hi0 = __umulhi(kPhiloxM0, c.x);
+    const uint32_t lo1 = kPhiloxM1 * c.z;
+    const uint32_t hi1 = __umulhi(kPhiloxM1, c.z);
+    c = U4{hi1 ^ c.y ^ ks.k0[r], lo1, hi0 ^ c.w ^ ks.k1[r], lo0};
+  }
+  return c;
+}
+
 // The device construction stream:
 //   key     = (seed & 0xffffffff, seed >> 32)
 //   counter = (city >> 2, step, ant, iteration)      selection, step >= 1
