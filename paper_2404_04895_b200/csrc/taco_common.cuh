@@ -123,6 +123,23 @@ __device__ __forceinline__ uint32_t word_of(const U4 &v, uint32_t i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }
 
+// selp: a predicated select the compiler cannot turn back into a branch
+__device__ __forceinline__ uint32_t select_u32(uint32_t pred, uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\tselp.b32 %0, %2, %3, p;\n\t}"
+      : "=r"(r)
+      : "r"(pred), "r"(a), "r"(b));
+  return r;
+}
+
+// word i of a Philox block without divergence (lanes of a window pick
+// different words): all four words are formed, then two levels of selp
+__device__ __forceinline__ uint32_t word_of_sel(const U4 &v, uint32_t i) {
+  const uint32_t lo = select_u32(i & 1u, v.y, v.x);
+  const uint32_t hi = select_u32(i & 1u, v.w, v.z);
+  return select_u32(i & 2u, hi, lo);
+}
+
 __device__ __forceinline__ uint32_t start_city(uint32_t n, uint32_t ant, uint32_t iteration,
                                                uint32_t k0, uint32_t k1) {
   U4 r = philox4x32_10(U4{0u, 0u, ant, iteration}, k0, k1);

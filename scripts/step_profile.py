@@ -50,5 +50,5 @@ lib.taco_step_profile(buf, 0)
 steps = buf[3]
 print({"m": args.m, "steps": steps, "head_cycles": buf[0] / steps, "global_cycles": buf[1] / steps,
        "bookkeeping_cycles": buf[2] / steps, "global_windows_per_step": buf[4] / steps,
-       "head_load_cycles": buf[5] / steps, "philox_cycles": buf[6] / steps,
-       "redux_max_cycles": (buf[7] & 0xffffffff) / steps, "redux_min_cycles": (buf[7] >> 32) / steps})
+       "first_window_load_wait": buf[5] / steps, "vis_philox_key_cycles": buf[6] / steps,
+       "two_redux_cycles": buf[7] / steps})
