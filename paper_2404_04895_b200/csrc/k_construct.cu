@@ -669,10 +669,11 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     // warp-per-ant kernel; TACO_SORTED_KERNEL = warp | g4e4 | g8e4 | g4e2 |
     // g8e2 | g16e2 overrides (tuning knob)
     int G = 0, E = 0;
-    // Measured on B200 at n = 2392 (profiles/README.md): the warp kernel wins
-    // while it is latency-bound (<= ~48 ants per SM); beyond that the SIMT
-    // sharing of the lane-group kernel wins (m = 16384: 6.8 vs 9.8 ms).
-    if (m_local > 48 * sm_count()) G = 8, E = 2;
+    // Measured on B200 at n = 2392 (scripts/sweep_kernel_choice.sh): the warp
+    // kernel wins up to ~64 ants per SM (m = 8192: 4.38 vs 4.79 ms); beyond
+    // that the SIMT sharing of the lane-group kernel wins (m = 12288: 6.03 vs
+    // 6.52 ms).
+    if (m_local > 64 * sm_count()) G = 8, E = 2;
     if (m_local > 200 * sm_count()) G = 4, E = 4;  // n = 5000, m = 65536: 44.9 vs 51.1 ms
     if (const char *ev = getenv("TACO_SORTED_KERNEL")) {
       G = 0;
