@@ -111,7 +111,6 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
   int2 *nb_stage = reinterpret_cast<int2 *>(smem + lay.stage_off);
   double *inc_stage = reinterpret_cast<double *>(nb_stage + kDepositChunk);
   __shared__ int s_meta[3];  // n_leaves, n_internal, height of the plan
-  __shared__ double s_stage[32];
 
   const int n = a.n;
   const int tid = threadIdx.x;
@@ -176,17 +175,20 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
               v = inc_stage[e >> 1];
             }
             const unsigned peers = __match_any_sync(0xffffffffu, col);
-            s_stage[lane] = v;
-            __syncwarp();
-            if (col >= 0 && lane == __ffs(peers) - 1) {
-              double acc = row[col];
-              unsigned p = peers;
-              while (p) {
-                const int l = __ffs(p) - 1;
-                p &= p - 1;
-                acc = __dadd_rn(acc, s_stage[l]);
+            // every lane folds its column group in lane (= rank) order; the
+            // values arrive by shuffle, so the only dependent chain is the
+            // group's additions (no shared-memory round trip per element)
+            const bool leader = col >= 0 && lane == __ffs(peers) - 1;
+            if (__any_sync(0xffffffffu, __popc(peers) > 1)) {
+              double acc = leader ? row[col] : 0.0;
+#pragma unroll
+              for (int t = 0; t < 32; ++t) {
+                const double x = __shfl_sync(0xffffffffu, v, t);
+                if ((peers >> t) & 1u) acc = __dadd_rn(acc, x);
               }
-              row[col] = acc;
+              if (leader) row[col] = acc;
+            } else if (leader) {  // no shared column in this window
+              row[col] = __dadd_rn(row[col], v);
             }
             __syncwarp();
           }
