@@ -258,13 +258,20 @@ class Solver:
     def _capture(self, iters: int) -> torch.cuda.CUDAGraph:
         # the device state already holds self.iteration (every iteration of a
         # graph-mode solver advances it on the stream); capture does not run
+        # capture_begin/end directly: torch.cuda.graph() would also synchronize,
+        # empty the device and pinned-host caches (and optionally gc.collect()),
+        # which costs milliseconds per capture; the iteration allocates nothing
         side = torch.cuda.Stream(device=self.dev)
         side.wait_stream(torch.cuda.current_stream(self.dev))
         g = torch.cuda.CUDAGraph()
         it0 = self.iteration
-        with torch.cuda.graph(g, stream=side, capture_error_mode="thread_local"):
-            for _ in range(iters):
-                self._enqueue(None, None)
+        with torch.cuda.stream(side):
+            g.capture_begin(capture_error_mode="thread_local")
+            try:
+                for _ in range(iters):
+                    self._enqueue(None, None)
+            finally:
+                g.capture_end()
         self.iteration = it0  # _enqueue counted the captured (not yet run) iterations
         torch.cuda.current_stream(self.dev).wait_stream(side)
         self._graphs[iters] = g
