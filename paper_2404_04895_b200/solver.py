@@ -393,6 +393,45 @@ class Solver:
                 self.step_async()
         return self._read_back()
 
+    # ---- checkpoint / resume ----------------------------------------------
+    def checkpoint(self) -> dict:
+        """Host copy of the whole iteration state: tau, the iteration counter
+        and the best-so-far tour.  The streams are keyed by (seed, iteration),
+        so ``restore`` continues bit-identically (the reference's
+        state is (tau, iteration), model.py:218-232)."""
+        self.check()
+        tour, length = self.best()
+        return {"tau": _device.download(self.tau).copy(), "iteration": int(self.iteration),
+                "best_tour": tour, "best_length": length, "best_iteration": int(self.best_iter.item()),
+                "n": int(self.n), "seed": int(self.params.seed)}
+
+    def restore(self, ckpt: dict) -> None:
+        """Load a ``checkpoint()`` of a Solver on the same instance and params."""
+        if int(ckpt["n"]) != self.n or int(ckpt["seed"]) != int(self.params.seed):
+            raise ValueError("checkpoint is for a different instance size or seed")
+        tau = np.asarray(ckpt["tau"], dtype=np.float64)
+        if tau.shape != (self.n, self.n):
+            raise ValueError(f"tau must have shape ({self.n}, {self.n})")
+        it = int(ckpt["iteration"])
+        self.tau.copy_(torch.from_numpy(np.ascontiguousarray(tau)))
+        self.best_tour.copy_(torch.from_numpy(np.asarray(ckpt["best_tour"], dtype=np.int32)))
+        self.best_cost.fill_(float(ckpt["best_length"]))
+        self.best_iter.fill_(int(ckpt["best_iteration"]))
+        self.iteration = it
+        self._write_state(it)
+        # P / W of iteration `it` from the restored tau (what the end of
+        # iteration it-1 built)
+        self._rebuild_tables(evaporate=False, gamma_next=construction_gamma(self.params, it))
+
+    def save(self, path: str) -> None:
+        """``checkpoint()`` to an .npz file."""
+        np.savez(path, **{k: np.asarray(v) for k, v in self.checkpoint().items()})
+
+    def load(self, path: str) -> None:
+        """``restore()`` from a ``save()`` file."""
+        with np.load(path) as z:
+            self.restore({k: z[k] for k in z.files})
+
     # ---- state inspection (host copies) ---------------------------------
     def pheromone(self) -> PheromoneState:
         return PheromoneState(tau=_device.download(self.tau), iteration=self.iteration)

@@ -435,3 +435,24 @@ def test_graph_replay_equals_eager_solver(selection):
     assert np.array_equal(g.pheromone().tau, e.pheromone().tau)
     assert np.array_equal(g.last_batch().costs, e.last_batch().costs)
     assert int(g.best_iter.item()) == int(e.best_iter.item())
+
+
+@pytest.mark.parametrize("selection", ["adair", "rw"])
+def test_checkpoint_resume_is_bit_identical(tmp_path, selection):
+    inst = euclid(40, 64)
+    params = taco.AcoParams(m=24, k=3, selection=selection, seed=8, gamma_schedule=taco.GammaSchedule(1.5, 1.0, 7))
+    full = taco.Solver(inst, params)
+    full.run(9)
+    first = taco.Solver(inst, params)
+    first.run(4)
+    first.save(str(tmp_path / "ck.npz"))
+    second = taco.Solver(inst, params)
+    second.load(str(tmp_path / "ck.npz"))
+    assert second.iteration == 4
+    tour, length = second.run(5)
+    assert second.iteration == full.iteration == 9
+    assert np.array_equal(second.pheromone().tau, full.pheromone().tau)
+    assert length == full.best()[1] and np.array_equal(tour, full.best()[0])
+    assert np.array_equal(second.last_batch().tours, full.last_batch().tours)
+    with pytest.raises(ValueError):
+        taco.Solver(euclid(40, 65), params).restore(first.checkpoint())
