@@ -272,6 +272,20 @@ int taco_elite_neighbors(int n, int k, const void *tours, int tours_is_i64,
                          int32_t *nbr_out, double *inc_out, void *stream);
 
 /*
+ * Multi-GPU costs-first exchange, local half.  After the m
+ * lengths are all-gathered and ranked (order), elite row r (r < k) receives
+ * this rank's tour of global ant order[r] when the rank owns it (ants
+ * [ant_offset, ant_offset + count), tours_local count x n), zeros otherwise;
+ * a SUM all-reduce of elite_tours (k x n int32) over the ranks then holds every
+ * elite tour exactly — k·n instead of m·n exchanged.  elite_costs[r] =
+ * costs_all[order[r]].
+ */
+int taco_shard_elites(int n, int k, const int32_t *order, int ant_offset,
+                      int count, const int32_t *tours_local,
+                      const double *costs_all, int32_t *elite_tours,
+                      double *elite_costs, void *stream);
+
+/*
  * Best-so-far tracking for Solver.step(): if costs[order[0]] < *best_cost,
  * copy that tour to best_tour and update best_cost / best_iter.
  */

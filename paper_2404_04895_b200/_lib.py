@@ -66,6 +66,7 @@ SIGNATURES = {
     "taco_elite_neighbors": (_c_int, [_c_int, _c_int, _p, _c_int, _p, _p, _p, _p, _p]),
     "taco_track_best": (_c_int, [_c_int, _p, _p, _p, _p, _p, _p, _c_u32, _p, _p]),
     "taco_iter_advance": (_c_int, [_p, _p, _c_int, _p]),
+    "taco_shard_elites": (_c_int, [_c_int, _c_int, _p, _c_int, _c_int, _p, _p, _p, _p, _p]),
 }
 
 ABI_VERSION = 2

@@ -94,6 +94,22 @@ __global__ void k_elite_neighbors(int n, int k, const TourT *__restrict__ tours,
   if (s == 0) inc[r] = __ddiv_rn(1.0, costs[a]);  // pheromone.py:66 inc = 1.0 / cost
 }
 
+// Costs-first exchange, local half: elite row r = this rank's tour of global
+// ant order[r] when it owns it, zeros otherwise (a SUM all-reduce over the
+// ranks then assembles every elite tour exactly); elite_costs[r] =
+// costs_all[order[r]] on every rank.
+__global__ void k_shard_elites(int n, int k, const int32_t *__restrict__ order, int ant_offset, int count,
+                               const int32_t *__restrict__ tours_local, const double *__restrict__ costs_all,
+                               int32_t *elite_tours, double *elite_costs) {
+  const int r = blockIdx.x;
+  const int a = order[r];
+  const bool mine = a >= ant_offset && a < ant_offset + count;
+  const int32_t *src = tours_local + (size_t)(mine ? a - ant_offset : 0) * n;
+  int32_t *dst = elite_tours + (size_t)r * n;
+  for (int s = threadIdx.x; s < n; s += blockDim.x) dst[s] = mine ? src[s] : 0;
+  if (threadIdx.x == 0) elite_costs[r] = costs_all[a];
+}
+
 __global__ void k_track_best(int n, const int32_t *tours, const double *costs, const int32_t *order,
                              double *best_cost, int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
                              const taco_iter_state *state) {
@@ -268,6 +284,18 @@ extern "C" int taco_elite_neighbors(int n, int k, const void *tours, int tours_i
   else
     k_elite_neighbors<int32_t><<<grid, 256, 0, s>>>(n, k, (const int32_t *)tours, order, costs,
                                                     reinterpret_cast<int2 *>(nbr_out), inc_out);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+extern "C" int taco_shard_elites(int n, int k, const int32_t *order, int ant_offset, int count,
+                                 const int32_t *tours_local, const double *costs_all, int32_t *elite_tours,
+                                 double *elite_costs, void *stream) {
+  if (n < 1 || k < 1 || ant_offset < 0 || count < 0 || order == nullptr || tours_local == nullptr ||
+      costs_all == nullptr || elite_tours == nullptr || elite_costs == nullptr)
+    return TACO_ERR_ARG;
+  k_shard_elites<<<k, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(n, k, order, ant_offset, count, tours_local,
+                                                                        costs_all, elite_tours, elite_costs);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }

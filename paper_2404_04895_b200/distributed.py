@@ -8,6 +8,12 @@ exchange per iteration: the tours and lengths are all-gathered, then every
 rank runs the identical elite sort, deposit and P rebuild on replicated
 state — no n x n all-reduce.  The helpers work on any torch.distributed
 backend (NCCL on the B200 box, gloo for the CPU tests).
+
+The Solver uses the costs-first form: all-gather the m lengths,
+rank them identically on every rank, then assemble only the k elite tours
+with one SUM all-reduce of a k x n buffer in which each rank filled the rows
+it owns (taco_shard_elites) — k·n·4 bytes instead of m·n·4 (10x less at
+k = m/10).  ``gather_colony`` (all tours) remains for ``last_batch()``.
 """
 
 from __future__ import annotations
@@ -87,3 +93,25 @@ def gather_colony(local_tours: torch.Tensor, local_costs: torch.Tensor, shard: A
     torch.index_select(pad_tours, 0, idx, out=tours_all)
     torch.index_select(pad_costs, 0, idx, out=costs_all)
     return tours_all, costs_all
+
+
+def gather_costs(local_costs: torch.Tensor, shard: AntShard, costs_all: torch.Tensor, group=None,
+                 pad_costs: torch.Tensor | None = None) -> torch.Tensor:
+    """All-gather every rank's tour lengths into the global (m,) buffer in
+    global ant order (first half of the costs-first exchange)."""
+    if shard.m % shard.world == 0:
+        _all_gather_into(costs_all, local_costs, group)
+        return costs_all
+    if pad_costs is None:
+        raise ValueError("uneven shards need a padded gather buffer")
+    _all_gather_into(pad_costs, local_costs, group)
+    idx = gather_index(shard.m, shard.world).to(pad_costs.device)
+    torch.index_select(pad_costs, 0, idx, out=costs_all)
+    return costs_all
+
+
+def share_elites(elite_tours: torch.Tensor, group=None) -> torch.Tensor:
+    """Second half: every rank filled the elite rows it owns (zeros elsewhere);
+    an integer SUM all-reduce leaves every elite tour on every rank, exactly."""
+    dist.all_reduce(elite_tours, op=dist.ReduceOp.SUM, group=group)
+    return elite_tours

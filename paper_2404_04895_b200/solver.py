@@ -38,7 +38,7 @@ import torch.distributed as tdist
 
 from . import _device, _lib
 from .colony import NumericalUnderflow, construction_gamma
-from .distributed import AntShard, gather_colony, shard_ants
+from .distributed import AntShard, gather_colony, gather_costs, shard_ants, share_elites
 from .model import AcoParams, PheromoneState, ProbabilityMatrix, Selection, TourBatch, instance_from_distances
 
 
@@ -158,11 +158,15 @@ class Solver:
         self.tours_local = torch.zeros((sh.per_rank, n), dtype=torch.int32, device=dev)
         self.costs_local = torch.zeros(sh.per_rank, dtype=torch.float64, device=dev)
         if world > 1:
-            self.tours_all = torch.zeros((m, n), dtype=torch.int32, device=dev)
+            # costs-first exchange: all m lengths, then only the k elite tours
             self.costs_all = torch.zeros(m, dtype=torch.float64, device=dev)
             uneven = m % world != 0
-            self._pad_tours = torch.zeros((world * sh.per_rank, n), dtype=torch.int32, device=dev) if uneven else None
             self._pad_costs = torch.zeros(world * sh.per_rank, dtype=torch.float64, device=dev) if uneven else None
+            self.elite_tours = torch.zeros((k, n), dtype=torch.int32, device=dev)
+            self.elite_costs = torch.zeros(k, dtype=torch.float64, device=dev)
+            self._ident_k = torch.arange(k, dtype=torch.int32, device=dev)
+            self._all_tours_iteration = -1  # last_batch() gathers all tours on demand
+            self.tours_all = None
         else:
             self.tours_all, self.costs_all = self.tours_local, self.costs_local
         self.order = torch.zeros(m, dtype=torch.int32, device=dev)
@@ -296,14 +300,22 @@ class Solver:
                               costs_out=self.costs_local, state=st)
         ev.stop("construct")
         if sh.world > 1:
-            gather_colony(self.tours_local, self.costs_local, sh, self.tours_all, self.costs_all,
-                          self.group, self._pad_tours, self._pad_costs)
+            gather_costs(self.costs_local, sh, self.costs_all, self.group, self._pad_costs)
         _device.elite_order(self.costs_all, self.elite_ws, self.order)
-        _lib.check(lib.taco_track_best(self.n, self.tours_all.data_ptr(), self.costs_all.data_ptr(),
-                                       self.order.data_ptr(), self.best_cost.data_ptr(),
-                                       self.best_tour.data_ptr(), self.best_iter.data_ptr(), it & 0xFFFFFFFF,
-                                       _lib.ptr(st), _device.stream_handle()), "taco_track_best")
-        _device.elite_neighbors(self.tours_all, self.order, self.costs_all, p.k, self.nbr, self.inc)
+        if sh.world > 1:
+            _lib.check(lib.taco_shard_elites(self.n, p.k, self.order.data_ptr(), sh.offset, sh.count,
+                                             self.tours_local.data_ptr(), self.costs_all.data_ptr(),
+                                             self.elite_tours.data_ptr(), self.elite_costs.data_ptr(),
+                                             _device.stream_handle()), "taco_shard_elites")
+            share_elites(self.elite_tours, self.group)
+            tours, costs, order = self.elite_tours, self.elite_costs, self._ident_k
+        else:
+            tours, costs, order = self.tours_all, self.costs_all, self.order
+        _lib.check(lib.taco_track_best(self.n, tours.data_ptr(), costs.data_ptr(), order.data_ptr(),
+                                       self.best_cost.data_ptr(), self.best_tour.data_ptr(),
+                                       self.best_iter.data_ptr(), it & 0xFFFFFFFF, _lib.ptr(st),
+                                       _device.stream_handle()), "taco_track_best")
+        _device.elite_neighbors(tours, order, costs, p.k, self.nbr, self.inc)
         ev.start("update")
         self._rebuild_tables(evaporate=True, gamma_next=construction_gamma(p, it + 1), state=st)
         ev.stop("update")
@@ -443,7 +455,19 @@ class Solver:
         return ProbabilityMatrix(p=_device.download(p))
 
     def last_batch(self) -> TourBatch:
-        """Tours and lengths of the most recent iteration (all ranks' ants)."""
+        """Tours and lengths of the most recent iteration (all ranks' ants;
+        sharded runs all-gather the tours here, on demand — a collective every
+        rank must call)."""
+        if self.shard.world > 1 and self._all_tours_iteration != self.iteration:
+            sh, m, n = self.shard, self.params.m, self.n
+            if self.tours_all is None:
+                self.tours_all = torch.zeros((m, n), dtype=torch.int32, device=self.dev)
+            pad_t = torch.zeros((sh.world * sh.per_rank, n), dtype=torch.int32, device=self.dev) \
+                if m % sh.world else None
+            scratch = torch.zeros_like(self.costs_all)
+            pad_c = torch.zeros_like(self._pad_costs) if self._pad_costs is not None else None
+            gather_colony(self.tours_local, self.costs_local, sh, self.tours_all, scratch, self.group, pad_t, pad_c)
+            self._all_tours_iteration = self.iteration
         return TourBatch(tours=_device.download(self.tours_all).astype(np.int64),
                          costs=_device.download(self.costs_all))
 

@@ -56,8 +56,22 @@ def _worker(rank: int, world: int, port: int, m: int, n: int, out_dir: str) -> N
                                   None, pad_t, pad_c)
         order = ref.elite_ranks(costs_all.numpy(), max(1, m // 10))
         delta = ref.deposit(tours_all.numpy()[order].astype(np.int64), costs_all.numpy()[order], n)
+        # costs-first exchange (the Solver's path): lengths, identical ranking,
+        # then only the k elite tours, each rank filling the rows it owns
+        k = max(1, m // 10)
+        costs2 = torch.zeros(m, dtype=torch.float64)
+        distributed.gather_costs(torch.from_numpy(costs), sh, costs2, None,
+                                 torch.zeros(world * sh.per_rank, dtype=torch.float64) if m % world else None)
+        order2 = ref.elite_ranks(costs2.numpy(), k)
+        elite = np.zeros((k, n), dtype=np.int32)
+        for r, a in enumerate(order2):  # what taco_shard_elites does on the device
+            if sh.offset <= a < sh.offset + sh.count:
+                elite[r] = local[a - sh.offset]
+        elite_t = distributed.share_elites(torch.from_numpy(elite))
+        delta2 = ref.deposit(elite_t.numpy().astype(np.int64), costs2.numpy()[order2], n)
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), tours=tours_all.numpy(), costs=costs_all.numpy(),
-                 order=order, delta=delta)
+                 order=order, delta=delta, costs2=costs2.numpy(), order2=order2, elite=elite_t.numpy(),
+                 delta2=delta2)
     finally:
         dist.destroy_process_group()
 
@@ -77,3 +91,10 @@ def test_sharded_colony_equals_single_process(tmp_path, m):
     # every rank applies the identical elite deposit: replicated pheromone
     assert np.array_equal(ranks[0]["order"], ranks[1]["order"])
     assert np.array_equal(ranks[0]["delta"], ranks[1]["delta"])
+    # the costs-first exchange reaches the same elites and deposit with k x n traffic
+    order = ref.elite_ranks(want_costs, max(1, m // 10))
+    for r in ranks:
+        assert np.array_equal(r["costs2"], want_costs)
+        assert np.array_equal(r["order2"], order)
+        assert np.array_equal(r["elite"], want[order])
+        assert np.array_equal(r["delta2"], ranks[0]["delta"])
