@@ -421,7 +421,8 @@ def run_reference(args) -> dict | None:
 
     n, m, selection = CONFIGS[args.config]
     k = max(1, m // 10)
-    cores = max(1, min(os.cpu_count() or 1, args.ref_procs))
+    host = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    cores = max(1, min(host, args.ref_procs) if args.ref_procs > 0 else host)
     # warm-up samples (untimed), then K sampled iterations, `cores` colonies at a time
     if args.warmup:
         cpu_baseline.parallel_samples(n, m, k, selection, min(args.warmup, cores), cores, steps=2)
@@ -459,7 +460,7 @@ def main() -> None:
     ap.add_argument("--construct", choices=("sorted", "dense"), default="sorted")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=6)
-    ap.add_argument("--ref-procs", type=int, default=16)
+    ap.add_argument("--ref-procs", type=int, default=0, help="reference arm processes (0: all host cores)")
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         ap.error("need --steps >= 1 and --warmup >= 0")
