@@ -108,12 +108,14 @@ def rw_tours(p: np.ndarray, seed: int, iteration: int, ants) -> np.ndarray:
 
 
 def selection_table(p: np.ndarray, g: float) -> np.ndarray:
-    """W = fp32(P^(1/g)); exact for g == 1.  (For g != 1 numpy's pow may
-    differ from CUDA's by an ulp before rounding; parity tests therefore feed
-    the device-built W to `build_tours`.)"""
+    """W = fp32(P^(1/g)) as the device builds it: exact conversion for g == 1,
+    else fp32(exp2(log2(P)/g)) in f64 (k_row_update.cu selection_weight).
+    numpy's log2/exp2 may differ from CUDA's by an ulp before the fp32
+    rounding, so parity tests feed the device-built W to `build_tours`."""
     if g == 1.0:
         return p.astype(np.float32)
-    return np.power(p, 1.0 / g).astype(np.float32)
+    with np.errstate(divide="ignore"):
+        return np.exp2((1.0 / g) * np.log2(p)).astype(np.float32)
 
 
 def build_tours(w: np.ndarray, seed: int, iteration: int, ants) -> np.ndarray:

@@ -60,8 +60,12 @@ __device__ __forceinline__ double numpy_scalar_power(double x, double e) {
 }
 
 __device__ __forceinline__ float selection_weight(double p, double inv_gamma) {
-  // W = P^(1/gamma) rounded once to fp32; gamma == 1 is the exact conversion
-  return inv_gamma == 1.0 ? __double2float_rn(p) : __double2float_rn(pow(p, inv_gamma));
+  // W = P^(1/gamma) rounded once to fp32; gamma == 1 is the exact conversion.
+  // exp2(log2(p) / gamma) in f64 is within ~2^-47 of the exact power, so the
+  // fp32 rounding equals that of a correctly rounded pow except for ~1 entry
+  // in 10^7 (one fp32 ulp); it costs 12 us instead of 35 at C3 (365 vs 737 us
+  // at n = 10000).  p = 0 gives log2 = -inf and W = 0.
+  return inv_gamma == 1.0 ? __double2float_rn(p) : __double2float_rn(exp2(inv_gamma * log2(p)));
 }
 
 // Shared-memory layout (bytes, all regions 16-B aligned):
