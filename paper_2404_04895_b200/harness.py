@@ -13,8 +13,12 @@ path, so for ``instance_path`` the caller passes the instance (or
 
 from __future__ import annotations
 
+import csv
+import io
+import json
+import os
 import time
-from dataclasses import dataclass, replace
+from dataclasses import asdict, dataclass, replace
 
 import numpy as np
 import torch
@@ -25,6 +29,11 @@ from .selection import gamma_at
 from .solver import Solver
 
 CONVERGENCE_BAND = 1e-3  # bench.py:40
+
+ITER_COLUMNS = [  # bench.py:42-45: the per-iteration CSV, fixed column order
+    "run_id", "seed", "iteration", "wall_clock_ms", "iteration_best_cost",
+    "best_cost_so_far", "solution_error_percent", "gamma", "rho",
+]
 
 
 @dataclass(frozen=True)
@@ -167,3 +176,58 @@ def run_experiment(config: ExperimentConfig, inst=None, clock=time.perf_counter,
             convergence_generation=convergence_generation(trace),
             mean_ms_per_iter=float(np.mean(measured)), terminated_by=terminated_by))
     return records, summaries
+
+
+# ---------------------------------------------------------------------------
+# the reference's output formats (bench.py:395-462): per-iteration CSV and the
+# per-experiment summary JSON, byte-identical for the same records
+# ---------------------------------------------------------------------------
+def _fmt(v) -> str:
+    if v is None:
+        return ""
+    if isinstance(v, float):
+        return repr(v)
+    return str(v)
+
+
+def write_records_csv(records: list[IterationRecord], out) -> None:
+    """Per-iteration CSV with the fixed ITER_COLUMNS order (bench.py:403-408)."""
+    w = csv.writer(out, lineterminator="\n")
+    w.writerow(ITER_COLUMNS)
+    for r in records:
+        w.writerow([_fmt(getattr(r, c)) for c in ITER_COLUMNS])
+
+
+def records_csv_text(records: list[IterationRecord]) -> str:
+    buf = io.StringIO()
+    write_records_csv(records, buf)
+    return buf.getvalue()
+
+
+def config_to_dict(config: ExperimentConfig) -> dict:
+    """bench.py:424-427: dataclass dict with the selection as its string value."""
+    d = asdict(config)
+    d["params"]["selection"] = Selection(config.params.selection).value
+    return d
+
+
+def summary_json_text(config: ExperimentConfig, inst, summaries: list[RunSummary]) -> str:
+    """One JSON document per experiment: config echo plus aggregates
+    (bench.py:441-462)."""
+    finals = [s.final_best_cost for s in summaries]
+    convs = [s.convergence_generation for s in summaries]
+    doc = {
+        "config": config_to_dict(config),
+        "instance": {
+            "name": getattr(inst, "name", ""), "n": int(inst.n), "best_known": getattr(inst, "best_known", None),
+            "best_known_source": ("override" if config.best_known is not None else "bundled-table"),
+        },
+        "runs": [asdict(s) for s in summaries],
+        "aggregate": {
+            "median_final_best_cost": float(np.median(finals)),
+            "median_convergence_generation": float(np.median(convs)),
+            "mean_ms_per_iter": float(np.mean([s.mean_ms_per_iter for s in summaries])),
+            "cpu_count": os.cpu_count(),
+        },
+    }
+    return json.dumps(doc, indent=2, sort_keys=True) + "\n"

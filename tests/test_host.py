@@ -122,3 +122,32 @@ def test_shard_errors():
         distributed.shard_ants(3, 0, 4)
     with pytest.raises(ValueError):
         distributed.shard_ants(8, 4, 4)
+
+
+def test_harness_output_formats_match_reference_golden():
+    """records CSV and summary JSON are byte-identical to antbatch's writers
+    (bench.py:395-462) on the same values (tests/golden/make_harness.py)."""
+    import json
+    import os
+    from types import SimpleNamespace
+
+    from paper_2404_04895_b200 import harness
+
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    recs = [harness.IterationRecord(*r) for r in (
+        (0, 5, 0, 1.25, 1234.5, 1234.5, 3.1, 1.5, 0.1),
+        (0, 5, 1, 0.1 + 0.2, 1200.0, 1200.0, None, 1.4268, 0.1),
+        (1, 6, 0, 2.0, 987.654321, 987.654321, None, None, 0.25))]
+    sums = [harness.RunSummary(*r) for r in (
+        (0, 5, 2, 1200.0, 0.5, 1, 0.30000000000000004, "max_iters"),
+        (1, 6, 1, 987.654321, None, 0, 2.0, "time_limit"))]
+    assert harness.records_csv_text(recs) == open(os.path.join(here, "harness_records.csv")).read()
+    config = harness.ExperimentConfig(
+        params=taco.AcoParams(m=8, k=2, alpha=1.0, beta=2.0, rho=0.1, selection="adair",
+                              gamma_schedule=taco.GammaSchedule(1.5, 1.0, 7), max_iters=2, seed=5),
+        synthetic=harness.SyntheticSpec(n=12, seed=1, kind="uniform"), repetitions=2, best_known=1000.0)
+    doc = json.loads(harness.summary_json_text(config, SimpleNamespace(name="rnd12", n=12, best_known=1000.0),
+                                               sums))
+    assert doc["aggregate"]["cpu_count"] == os.cpu_count()
+    doc["aggregate"]["cpu_count"] = None
+    assert json.dumps(doc, indent=2, sort_keys=True) + "\n" == open(os.path.join(here, "harness_summary.json")).read()
