@@ -281,17 +281,14 @@ static int sm_count_row() {
   return cached;
 }
 
-constexpr int kRowBlock = 256;
-
-static int launch_row(const RowParams &a, cudaStream_t stream) {
-  const RowLayout lay = row_layout(a.n, a.n_leaves > 0 ? a.n_leaves : 1, 0);
-  if (lay.total > 227 * 1024) return TACO_ERR_UNSUPPORTED;
+template <int BLOCK>
+static int launch_row_t(const RowParams &a, const RowLayout &lay, cudaStream_t stream) {
   static size_t configured = 0;
   static int blocks_per_sm = 0;
   static size_t blocks_for = 0;
   if (lay.total > 48 * 1024 && lay.total > configured) {
-    const cudaError_t e = cudaFuncSetAttribute(k_row_update<kRowBlock>,
-                                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
+    const cudaError_t e =
+        cudaFuncSetAttribute(k_row_update<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
     if (e != cudaSuccess) {
       note_cuda_error(e);
       return TACO_ERR_CUDA;
@@ -299,17 +296,27 @@ static int launch_row(const RowParams &a, cudaStream_t stream) {
     configured = lay.total;
   }
   if (blocks_for != lay.total) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_row_update<kRowBlock>, kRowBlock,
-                                                      lay.total) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_row_update<BLOCK>, BLOCK, lay.total) !=
+            cudaSuccess ||
         blocks_per_sm < 1)
       blocks_per_sm = 1;
     blocks_for = lay.total;
   }
   const int sms = sm_count_row();
   const int grid = a.n < sms * blocks_per_sm ? a.n : sms * blocks_per_sm;
-  k_row_update<kRowBlock><<<grid, kRowBlock, lay.total, stream>>>(a, lay);
+  k_row_update<BLOCK><<<grid, BLOCK, lay.total, stream>>>(a, lay);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
+}
+
+static int launch_row(const RowParams &a, cudaStream_t stream) {
+  const RowLayout lay = row_layout(a.n, a.n_leaves > 0 ? a.n_leaves : 1, 0);
+  if (lay.total > 227 * 1024) return TACO_ERR_UNSUPPORTED;
+  // CTA width by row length (scripts/row_update_probe.py): 256 threads are
+  // best up to n ~ 5000 (n = 2392: 153 us vs 154 / 211 for 128 / 512 with the
+  // k = 409 deposit); long rows want 512 (n = 10000: 1565 vs 1832 us)
+  if (a.n > 7000) return launch_row_t<512>(a, lay, stream);
+  return launch_row_t<256>(a, lay, stream);
 }
 
 // ---------------------------------------------------------------------------
