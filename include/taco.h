@@ -1,7 +1,7 @@
 /*
  * taco.h — C ABI of libtaco.so, the B200 (sm_100a) engine behind the
  * TensorACO hot path: one ACO iteration with Independent-Roulette (IR) or
- * Adaptive-IR (AdaIR) selection.
+ * Adaptive-IR (AdaIR) selection (and the roulette-wheel ablation, RW).
  *
  * The reference (`antbatch`, /root/reference/pkg/src/antbatch) is a pure
  * Python/numpy package and has no FFI of its own; its "plugin boundary" is the
@@ -15,10 +15,11 @@
  *     separate ld argument is given.
  *   - `stream` is a cudaStream_t passed as void*; every call is asynchronous on
  *     that stream and never allocates memory (callers pass workspaces).
- *   - `status` points to 4 device int32 words, zeroed by the caller.  Kernels
- *     record the first data-dependent failure there: status[0] = code
- *     (TACO_UNDERFLOW / TACO_NO_CANDIDATE), status[1] = smallest offending
- *     row (underflow) or ant (no candidate).
+ *   - `status` points to 4 device int32 words the caller initializes to
+ *     {0, INT32_MAX, 0, 0}.  Kernels record the first data-dependent failure
+ *     there: status[0] = code (TACO_UNDERFLOW / TACO_NO_CANDIDATE /
+ *     TACO_DEGENERATE), status[1] = smallest offending row (underflow,
+ *     degenerate) or ant (no candidate), kept with atomicMin.
  *   - The return value reports argument / launch errors synchronously:
  *     0 = launched, negative = error (see taco_status_string).
  */
