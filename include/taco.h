@@ -91,6 +91,7 @@ int taco_max_sorted_n(void);
  * the W bits above bit 16, stable in the column index).
  * eta_b / p outputs are skipped when want_p == 0 (delta/tau-only modes).
  * state (nullable): inv_gamma is read from state->inv_gamma.
+ * The row is staged in shared memory: n <= ~27900 (TACO_ERR_UNSUPPORTED above).
  */
 int taco_row_update(int n,
                     const double *tau_in, double *tau_out,
