@@ -19,7 +19,10 @@
  *     {0, INT32_MAX, 0, 0}.  Kernels record the first data-dependent failure
  *     there: status[0] = code (TACO_UNDERFLOW / TACO_NO_CANDIDATE /
  *     TACO_DEGENERATE), status[1] = smallest offending row (underflow,
- *     degenerate) or ant (no candidate), kept with atomicMin.
+ *     degenerate) or ant (no candidate), kept with atomicMin.  Fail-stop:
+ *     a construction call that starts with status[0] != 0 sets status[3] and
+ *     builds nothing; a row update that sees status[3] != 0 changes nothing —
+ *     iterations queued after a failure leave the failing state in place.
  *   - The return value reports argument / launch errors synchronously:
  *     0 = launched, negative = error (see taco_status_string).
  */

@@ -134,6 +134,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
 
   const int ant = blockIdx.x * warps + warp;
   if (ant >= a.m_local) return;
+  if (__shfl_sync(kFull, lane == 0 ? (int)chain_stopped_construct(a.status) : 0, 0)) return;  // fail-stop
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   const uint32_t un = (uint32_t)n;  // n <= 65535, so every row offset fits in 32 bits
@@ -353,6 +354,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
 
   const int g = lane / G, gl = lane % G, gbase = g * G;
   const int ant = (blockIdx.x * kGroupWarps + warp) * A + g;
+  if (__shfl_sync(kFull, lane == 0 ? (int)chain_stopped_construct(a.status) : 0, 0)) return;  // fail-stop
   bool alive = ant < a.m_local;
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
@@ -501,6 +503,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   __syncthreads();
   const int ant = blockIdx.x * WARPS + warp;
   if (ant >= a.m_local) return;
+  if (__shfl_sync(kFull, lane == 0 ? (int)chain_stopped_construct(a.status) : 0, 0)) return;  // fail-stop
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;

@@ -316,6 +316,7 @@ __global__ void __launch_bounds__(WARPS * 32, 7) k_construct_rw(const __grid_con
   __syncthreads();
   const int ant = blockIdx.x * WARPS + warp;
   if (ant >= a.m_local) return;
+  if (__shfl_sync(kFull, lane == 0 ? (int)chain_stopped_construct(a.status) : 0, 0)) return;  // fail-stop
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;

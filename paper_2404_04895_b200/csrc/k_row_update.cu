@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
   uint8_t *hgt = pp;
   int2 *nb_stage = reinterpret_cast<int2 *>(smem + lay.stage_off);
   double *inc_stage = reinterpret_cast<double *>(nb_stage + kDepositChunk);
-  __shared__ int s_meta[3];  // n_leaves, n_internal, height of the plan
+  __shared__ int s_meta[4];  // n_leaves, n_internal, height of the plan; fail-stop flag
 
   const int n = a.n;
   const int tid = threadIdx.x;
@@ -130,7 +130,11 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
     s_meta[1] = plan.n_internal;
     s_meta[2] = plan.height;
   }
+  // fail-stop (taco_common.cuh): tau / P / W untouched after a failed
+  // iteration, one decision per CTA
+  if (tid == 0) s_meta[3] = chain_stopped_update(a.status);
   __syncthreads();
+  if (s_meta[3]) return;
   plan.n_leaves = s_meta[0];
   plan.n_internal = s_meta[1];
   plan.height = s_meta[2];

@@ -161,6 +161,22 @@ __device__ __forceinline__ float bucket_ceiling(float w) {
 // ---------------------------------------------------------------------------
 // status word: [0] = first failure code, [1] = smallest offending index
 // ---------------------------------------------------------------------------
+// Fail-stop across Solver iterations: a construction kernel that starts after
+// a recorded failure (status[0] != 0) sets status[3] and does nothing; a row
+// update that sees status[3] leaves tau / P / W / row sums as they were, so
+// a host that checks only after several iterations still reads the state of
+// the failing iteration (where the reference raised).  One decision per warp
+// (construction) or CTA (row update) keeps barriers uniform.
+__device__ __forceinline__ bool chain_stopped_construct(int32_t *status) {
+  if (status == nullptr || *reinterpret_cast<volatile int32_t *>(status) == 0) return false;
+  reinterpret_cast<volatile int32_t *>(status)[3] = 1;
+  return true;
+}
+
+__device__ __forceinline__ bool chain_stopped_update(const int32_t *status) {
+  return status != nullptr && reinterpret_cast<const volatile int32_t *>(status)[3] != 0;
+}
+
 __device__ __forceinline__ void record_status(int32_t *status, int code, int index) {
   if (status == nullptr) return;
   atomicCAS(status, 0, code);

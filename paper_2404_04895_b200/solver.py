@@ -205,8 +205,10 @@ class Solver:
             raise ValueError("CUDA-graph replay covers the single-GPU device-stream solver")
         self.graph = use_graph
         self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
-        # P / W for iteration 0 from the initial pheromone (bench.py:191-192)
+        # P / W for iteration 0 from the initial pheromone (bench.py:191-192);
+        # the reference raises NumericalUnderflow right there
         self._rebuild_tables(evaporate=False, gamma_next=construction_gamma(p, 0))
+        self.check()
 
     # ------------------------------------------------------------------
     def _rebuild_tables(self, evaporate: bool, gamma_next: float, state=None) -> None:
@@ -425,6 +427,7 @@ class Solver:
         if tau.shape != (self.n, self.n):
             raise ValueError(f"tau must have shape ({self.n}, {self.n})")
         it = int(ckpt["iteration"])
+        self.status.copy_(_device.new_status(self.dev))  # a restored solver starts healthy
         self.tau.copy_(torch.from_numpy(np.ascontiguousarray(tau)))
         self.best_tour.copy_(torch.from_numpy(np.asarray(ckpt["best_tour"], dtype=np.int32)))
         self.best_cost.fill_(float(ckpt["best_length"]))

@@ -12,7 +12,8 @@ concern the hot path:
   beta = 0 gives uniform 1/(n-1) rows (test_colony.py:41-48);
   chunking is bit-invisible (test_colony.py:120-129);
   the device uniforms are in (0, 1) and uniform (KS), the reference's
-  stream-contract analog (test_rng.py, test_selection.py:207-237).
+  stream-contract analog (test_rng.py, test_selection.py:207-237);
+  the Solver raises the reference's exceptions (colony.py:63-68, :149).
 """
 
 import itertools
@@ -154,3 +155,36 @@ def test_starts_cover_every_city():
     starts = trng.device_starts(3, 0, 37, 20_000)
     counts = np.bincount(starts, minlength=37)
     assert counts.min() > 0 and counts.max() < 2 * counts.mean()
+
+
+BETA = 4.0  # eta^4 underflows to 0 across 1e90, not within 1e75
+
+
+def _two_far_clusters():
+    # cities 0-3 and 4-7 in two clusters 1e90 apart: eta^BETA is exactly 0
+    # across the clusters, so P has exact zeros between them
+    pts = np.array([[0, 0], [1, 0], [0, 1], [1, 1]], dtype=np.float64)
+    coords = np.concatenate([pts, 1e90 + 1e75 * pts])
+    return taco.euclidean_instance(coords)
+
+
+def test_solver_raises_the_reference_exceptions():
+    inst = _two_far_clusters()
+    # every ant gets stuck in its start cluster: the reference's argmax over an
+    # all -inf row picks a visited city and fails its assert (colony.py:149)
+    for construct in ("sorted", "dense"):
+        with pytest.raises(AssertionError, match="selector chose a visited city"):
+            taco.Solver(inst, taco.AcoParams(m=4, k=1, beta=BETA, selection="ir", seed=0),
+                        construct=construct).step()
+    with pytest.raises(AssertionError, match="selector chose a visited city"):
+        taco.Solver(inst, taco.AcoParams(m=4, k=1, beta=BETA, selection="rw", seed=0)).step()
+    # the reference's drop-in raises the same
+    params = taco.AcoParams(m=4, k=1, beta=BETA, selection="ir")
+    prob = taco.compute_probability_matrix(taco.PheromoneState.initial(8, 1.0), inst, params)
+    with pytest.raises(AssertionError):
+        taco.construct_tours(prob, inst, params, 0)
+    # a row whose normalizer underflows: NumericalUnderflow from the Solver's
+    # own row update, with the reference's message
+    far = taco.euclidean_instance(np.array([[0.0, 0.0], [1e90, 0.0], [0.0, 1e90], [1e90, 1e90]]))
+    with pytest.raises(taco.NumericalUnderflow, match="row 0 normalizer"):
+        taco.Solver(far, taco.AcoParams(m=4, k=1, beta=BETA)).step()
