@@ -110,6 +110,24 @@ int taco_row_update(int n,
                     void *stream);
 
 /*
+ * The same update as taco_row_update in Solver mode (edge-map deposit,
+ * evaporation, P, W / sorted table), as three streaming kernels that need no
+ * row in shared memory (any n <= 65535): a warp-per-row deposit into
+ * delta_ws (n x n f64), an elementwise evaporation + tau^alpha eta^beta into
+ * unnorm_ws (n x n f64), and a warp-per-row pairwise normalization writing P
+ * (p_out, nullable), the row sums and W.  Bit-identical results.  nbr / inc
+ * (nullable: no deposit) need do_evap; do_evap == 0 leaves tau untouched.
+ */
+int taco_update_split(int n, const double *tau_in, double *tau_out,
+                      const double *eta_b, const int32_t *nbr,
+                      const double *inc, int k, int do_evap, double keep,
+                      double alpha, double inv_gamma, double *delta_ws,
+                      double *unnorm_ws, double *p_out, double *rowsum_out,
+                      float *w_out, int ldw, float *sw_out, uint16_t *si_out,
+                      int32_t *status, const taco_iter_state *state,
+                      void *stream);
+
+/*
  * Selection table from a given P (construct_tours drop-in, colony.py:116):
  * W = fp32(P^(1/gamma)) dense (n x ldw) and/or row-sorted (sw_out/si_out).
  */

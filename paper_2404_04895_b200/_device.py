@@ -178,6 +178,17 @@ def row_update(n, *, tau_in=None, tau_out=None, eta_b=None, nbr=None, inc=None, 
     check(code, "taco_row_update")
 
 
+def update_split(n, *, tau_in, tau_out, eta_b, nbr, inc, k, do_evap, keep, alpha, inv_gamma, delta_ws,
+                 unnorm_ws, p_out=None, rowsum_out=None, w_out=None, ldw=0, sw_out=None, si_out=None,
+                 status=None, state=None) -> None:
+    """Solver-mode update as three streaming kernels (taco_update_split)."""
+    code = _lib.load().taco_update_split(
+        n, ptr(tau_in), ptr(tau_out), ptr(eta_b), ptr(nbr), ptr(inc), int(k), int(bool(do_evap)), float(keep),
+        float(alpha), float(inv_gamma), ptr(delta_ws), ptr(unnorm_ws), ptr(p_out), ptr(rowsum_out), ptr(w_out),
+        int(ldw), ptr(sw_out), ptr(si_out), ptr(status), ptr(state), stream_handle())
+    check(code, "taco_update_split")
+
+
 class SelectionTables:
     """fp32 selection table W = P^(1/gamma): dense and/or row-sorted (values
     sw + column indices si), all with row pitch ldw (multiple of 32).  The

@@ -399,6 +399,10 @@ static int launch_sort(int n, int ldw, const float *w, float *sw, uint16_t *si, 
   return TACO_ERR_UNSUPPORTED;
 }
 
+int launch_sort_table(int n, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t s) {
+  return launch_sort(n, ldw, w, sw, si, s);
+}
+
 }  // namespace taco
 
 using namespace taco;

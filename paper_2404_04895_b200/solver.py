@@ -98,6 +98,7 @@ class Solver:
 
     GRAPH_BATCH = 8  # iterations per graph replay in run()
     GRAPH_MAX_WORK = 1 << 16  # default graph mode below this many (city x ant) selections per iteration
+    FUSED_MAX_N = 27000  # the fused row kernel stages a row of n doubles in shared memory
 
     def __init__(self, instance, params=None, *, construct: str = "sorted", stream: str = "device",
                  group=None, graph: bool | None = None, **overrides):
@@ -183,6 +184,11 @@ class Solver:
         self.best_iter.fill_(-1)
         self.best_tour = self._io[32:].view(torch.int32)
         self.rowsum = torch.zeros(n, dtype=torch.float64, device=dev)
+        # rows longer than the fused kernel's shared-memory row use the split
+        # update, with its delta / tau^alpha eta^beta workspaces
+        self._split_update = n > self.FUSED_MAX_N
+        self._delta_ws = torch.empty((n, n), dtype=torch.float64, device=dev) if self._split_update else None
+        self._unnorm_ws = torch.empty((n, n), dtype=torch.float64, device=dev) if self._split_update else None
         self.status = self._io[0:16].view(torch.int32)
         self.status[1] = 2**31 - 1  # _device.new_status layout: smallest offending index
         self.iteration = 0
@@ -212,20 +218,23 @@ class Solver:
 
     # ------------------------------------------------------------------
     def _rebuild_tables(self, evaporate: bool, gamma_next: float, state=None) -> None:
+        """End-of-iteration update: deposit + evaporation + P / W.  The fused
+        row kernel (taco_row_update) is faster while a row fits in shared
+        memory; longer rows use the split streaming kernels (taco_update_split,
+        bit-identical, any n)."""
         t = self.tables
-        if self.stream == "replay" or self.rw:  # P itself is the next iteration's input
-            _device.row_update(
-                self.n, tau_in=self.tau, tau_out=self.tau if evaporate else None, eta_b=self.eta_b,
-                nbr=self.nbr if evaporate else None, inc=self.inc if evaporate else None,
-                k=self.params.k if evaporate else 0, do_evap=evaporate, keep=self.keep, want_p=True,
-                alpha=float(self.params.alpha), p_out=self.p, rowsum_out=self.rowsum, status=self.status)
-            return
-        _device.row_update(
-            self.n, tau_in=self.tau, tau_out=self.tau if evaporate else None, eta_b=self.eta_b,
+        p_mode = self.stream == "replay" or self.rw  # P itself is the next iteration's input
+        common = dict(
+            tau_in=self.tau, tau_out=self.tau if evaporate else None, eta_b=self.eta_b,
             nbr=self.nbr if evaporate else None, inc=self.inc if evaporate else None,
-            k=self.params.k if evaporate else 0, do_evap=evaporate, keep=self.keep, want_p=True,
-            alpha=float(self.params.alpha), inv_gamma=1.0 / gamma_next, rowsum_out=self.rowsum,
-            w_out=t.w, ldw=t.ldw, sw_out=t.sw, si_out=t.si, status=self.status, state=state)
+            k=self.params.k if evaporate else 0, do_evap=evaporate, keep=self.keep,
+            alpha=float(self.params.alpha), inv_gamma=1.0 / gamma_next, p_out=self.p if p_mode else None,
+            rowsum_out=self.rowsum, w_out=None if p_mode else t.w, ldw=t.ldw,
+            sw_out=None if p_mode else t.sw, si_out=None if p_mode else t.si, status=self.status, state=state)
+        if self._split_update:
+            _device.update_split(self.n, delta_ws=self._delta_ws, unnorm_ws=self._unnorm_ws, **common)
+        else:
+            _device.row_update(self.n, want_p=True, **common)
 
     def _write_state(self, it: int) -> None:
         """Device state for iteration `it`: (it, 1/gamma(it + 1))."""

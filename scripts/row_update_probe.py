@@ -75,3 +75,14 @@ for label, k, same in (("k=409 random", 409, False), ("k=409 identical", 409, Tr
     inc = torch.full((k,), 1e-5, dtype=torch.float64, device=dev)
     print(f"deposit only (delta_out) {label}:", round(timeit(lambda: _device.row_update(
         n, nbr=nb, inc=inc, k=k, delta_out=dout)), 1), "us")
+
+# split path (taco_update_split): deposit / evaporation+unnorm / normalize kernels
+dws, uws = torch.empty_like(tau), torch.empty_like(tau)
+for label, k, same in (("no deposit", 0, False), ("k=409 random", 409, False), ("k=409 identical", 409, True)):
+    nb = nbr_for(k, same) if k else None
+    inc = torch.full((max(k, 1),), 1e-5, dtype=torch.float64, device=dev)
+    tout = tau.clone()
+    print(f"split {label:16s} (no sort)", round(timeit(lambda: _device.update_split(
+        n, tau_in=tout, tau_out=tout, eta_b=eta, nbr=nb, inc=inc if k else None, k=k, do_evap=True, keep=0.9,
+        alpha=1.0, inv_gamma=1 / 1.3, delta_ws=dws, unnorm_ws=uws, rowsum_out=rowsum, w_out=tables.w,
+        ldw=tables.ldw, status=st)), 1), "us")

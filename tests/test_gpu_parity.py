@@ -456,3 +456,57 @@ def test_checkpoint_resume_is_bit_identical(tmp_path, selection):
     assert np.array_equal(second.last_batch().tours, full.last_batch().tours)
     with pytest.raises(ValueError):
         taco.Solver(euclid(40, 65), params).restore(first.checkpoint())
+
+
+@pytest.mark.parametrize("n,k,gamma,same", [(37, 5, 1.3, False), (300, 40, 1.0, True), (2392, 409, 1.17, False),
+                                            (1001, 102, 1.4, True)])
+def test_split_update_equals_fused_row_kernel(n, k, gamma, same):
+    """taco_update_split (Solver path) == taco_row_update (fused) bit for bit:
+    tau', row sums, P, W and the sorted table, with duplicate-heavy deposits."""
+    dev = _device.device()
+    g = np.random.default_rng(n)
+    tau0 = torch.from_numpy(g.uniform(1e-13, 2.0, (n, n))).to(dev)
+    eta = torch.from_numpy(g.uniform(0.01, 1.0, (n, n))).to(dev)
+    tours = np.stack([g.permutation(n) for _ in range(1 if same else k)])
+    tours = np.repeat(tours, k, axis=0) if same else tours
+    nbr = np.zeros((n, k, 2), dtype=np.int32)
+    for r, t in enumerate(tours):
+        nbr[t, r, 0], nbr[t, r, 1] = np.roll(t, 1), np.roll(t, -1)
+    nbr_t = torch.from_numpy(nbr).to(dev)
+    inc = torch.from_numpy(1.0 / g.uniform(1e3, 1e4, k)).to(dev)
+    outs = []
+    for split in (False, True):
+        tau = tau0.clone()
+        t = _device.SelectionTables(n, dev, dense=True, sorted_=True)
+        p = torch.zeros((n, n), dtype=torch.float64, device=dev)
+        rs = torch.zeros(n, dtype=torch.float64, device=dev)
+        st = _device.new_status(dev)
+        common = dict(tau_in=tau, tau_out=tau, eta_b=eta, nbr=nbr_t, inc=inc, k=k, do_evap=True, keep=0.9,
+                      alpha=1.0, inv_gamma=1.0 / gamma, p_out=p, rowsum_out=rs, w_out=t.w, ldw=t.ldw,
+                      sw_out=t.sw, si_out=t.si, status=st)
+        if split:
+            _device.update_split(n, delta_ws=torch.empty_like(tau), unnorm_ws=torch.empty_like(tau), **common)
+        else:
+            _device.row_update(n, want_p=True, **common)
+        torch.cuda.synchronize()
+        assert _device.read_status(st)[0] == 0
+        outs.append([x.cpu().numpy() for x in (tau, rs, p, t.w, t.sw, t.si)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("selection", ["adair", "rw"])
+def test_solver_split_update_path_is_bit_identical(monkeypatch, selection):
+    """Rows too long for the fused kernel's shared memory take the split
+    update; forced here at small n, the runs are identical."""
+    inst = euclid(77, 90)
+    params = taco.AcoParams(m=30, k=4, selection=selection, seed=3, gamma_schedule=taco.GammaSchedule(1.5, 1.0, 5))
+    fused = taco.Solver(inst, params)
+    fused.run(6)
+    monkeypatch.setattr(taco.Solver, "FUSED_MAX_N", 10)
+    split = taco.Solver(inst, params)
+    assert split._split_update
+    split.run(6)
+    assert np.array_equal(split.pheromone().tau, fused.pheromone().tau)
+    assert split.best()[1] == fused.best()[1]
+    assert np.array_equal(split.last_batch().tours, fused.last_batch().tours)
