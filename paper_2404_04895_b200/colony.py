@@ -59,8 +59,14 @@ def compute_probability_matrix(tau, inst, params) -> ProbabilityMatrix:
     p_t = torch.empty_like(tau_t)
     sums = torch.empty(n, dtype=torch.float64, device=dev)
     status = _device.new_status(dev)
-    _device.row_update(n, tau_in=tau_t, eta_b=di.eta_beta(params.beta), want_p=True,
-                       alpha=float(params.alpha), p_out=p_t, rowsum_out=sums, status=status)
+    if n > 27000:  # beyond the fused row kernel's shared-memory row: the split kernels
+        _device.update_split(n, tau_in=tau_t, tau_out=None, eta_b=di.eta_beta(params.beta), nbr=None, inc=None,
+                             k=0, do_evap=False, keep=1.0, alpha=float(params.alpha), inv_gamma=1.0,
+                             delta_ws=None, unnorm_ws=torch.empty_like(tau_t), p_out=p_t, rowsum_out=sums,
+                             status=status)
+    else:
+        _device.row_update(n, tau_in=tau_t, eta_b=di.eta_beta(params.beta), want_p=True,
+                           alpha=float(params.alpha), p_out=p_t, rowsum_out=sums, status=status)
     code, _ = _device.read_status(status)
     if code == _lib.TACO_UNDERFLOW:
         raise _underflow_from_sums(_device.download(sums))
