@@ -20,6 +20,7 @@ per core (the reference is single-threaded numpy).
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import math
 import os
@@ -58,12 +59,15 @@ def _peaks() -> tuple[float, str]:
         return HBM_FALLBACK, "fallback"
 
 
-def _traffic(kernel: str):
+def _traffic(kernel: str, config: str):
     """Per-launch DRAM bytes of `kernel` from the committed ncu capture
-    (profiles/traffic.json, written by scripts/summarize_profiles.py)."""
+    (profiles/traffic.json, written by scripts/summarize_profiles.py), when
+    that capture was taken on this config; else (None, None)."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             rec = json.load(f)[kernel]
+        if rec.get("config") != config:
+            return None, None
         return rec["dram_bytes_per_launch"], rec["capture"]
     except (OSError, KeyError, ValueError):
         return None, None
@@ -241,15 +245,20 @@ def run_ours(args) -> dict | None:
     e2e_run(lambda: inst, args.warmup)
     _device._INSTANCES.clear()
     torch.cuda.synchronize()
-    e2e_times = {}
-    for name, make in (("device_instance", dev_inst), ("host_instance", lambda: inst)):
-        _barrier(world)
-        with sampler.window() if (sampler and os.environ.get("TACO_BENCH_E2E_CLOCKS", "1") == "1") else _null():
-            t0 = time.perf_counter()
-            best_tour, best_len = e2e_run(make, args.steps)
-            torch.cuda.synchronize()
-            e2e_times[name] = _max_over_ranks(time.perf_counter() - t0, world)
-        _device._INSTANCES.clear()
+    # each e2e figure is the median of three complete runs (instance, Solver,
+    # K steps): millisecond-scale host timings pick up scheduler / GC noise
+    e2e_times = {"device_instance": [], "host_instance": []}
+    for _rep in range(3):
+        for name, make in (("device_instance", dev_inst), ("host_instance", lambda: inst)):
+            gc.collect()
+            _barrier(world)
+            with sampler.window() if sampler else _null():
+                t0 = time.perf_counter()
+                best_tour, best_len = e2e_run(make, args.steps)
+                torch.cuda.synchronize()
+                e2e_times[name].append(_max_over_ranks(time.perf_counter() - t0, world))
+            _device._INSTANCES.clear()
+    e2e_times = {k: float(np.median(v)) for k, v in e2e_times.items()}
 
     # ---- device-timed value ------------------------------------------------
     solver = taco.Solver(inst, params, construct=args.construct)
@@ -341,7 +350,7 @@ def run_ours(args) -> dict | None:
     dom_ms = t_construct
     kernel = "k_construct_rw" if rw else f"k_construct_{args.construct}"
     alg = m_local * (n - 1) * (n * 8 + 2048) if rw else alg_full
-    traffic, traffic_src = _traffic(kernel)
+    traffic, traffic_src = _traffic(kernel, args.config)
     roof = {"kernel": kernel, "bound": "hbm", "achieved": alg / (dom_ms * 1e-3) / 1e9, "peak": peak,
             "unit": "GB/s", "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
             "ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step, "alg_bytes_per_launch": alg,
@@ -373,7 +382,7 @@ def run_ours(args) -> dict | None:
                 "h2d_bytes_per_step": (n * 2 * 8) / args.steps,
                 "d2h_bytes_per_step": 32 + n * 4,
                 "what": ("pinned host coords -> device_euclidean_instance -> Solver -> K x step(), each returning "
-                         "status + best length + best tour in one D2H copy")},
+                         "status + best length + best tour in one D2H copy; median of 3 complete runs")},
         "e2e_host_instance": {"value": args.steps / e2e_times["host_instance"], "unit": "iterations/s",
                               "h2d_bytes_per_step": (2 * n * n * 8) / args.steps,
                               "d2h_bytes_per_step": 32 + n * 4,
@@ -391,7 +400,7 @@ def run_ours(args) -> dict | None:
         line["roofline_dense"] = {"kernel": "k_construct_dense", "bound": "hbm",
                                   "achieved": alg_full / (dense_ms * 1e-3) / 1e9, "peak": peak,
                                   "unit": "GB/s", "frac": alg_full / (dense_ms * 1e-3) / 1e9 / peak,
-                                  "ms_per_launch": dense_ms, "traffic": _traffic("k_construct_dense")[0],
+                                  "ms_per_launch": dense_ms, "traffic": _traffic("k_construct_dense", args.config)[0],
                                   "alg_bytes_def": "full-row stream m*(n-1)*n*4 B (SURVEY 8d)"}
     if sampler:
         line["clocks"] = sampler.summary()

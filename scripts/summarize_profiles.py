@@ -90,7 +90,8 @@ for rec in kern_rows:
     rd, wr = _bytes(rec.get("dram__bytes_read.sum")), _bytes(rec.get("dram__bytes_write.sum"))
     if rd is None or wr is None:
         continue
-    traffic[base] = {"dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+    traffic[base] = {"config": "c3rw" if base == "k_construct_rw" else "c3",  # scripts/profile_round.sh
+                     "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
                      "duration": rec.get("gpu__time_duration.sum"), "l2_hit_rate": rec.get("lts__t_sector_hit_rate.pct"),
                      "capture": f"profiles/{tag}_kernels.csv ({rec['report']}, ncu --set full)"}
 with open(traffic_path, "w") as f:
