@@ -57,7 +57,8 @@ struct LeafCost {
   }
   // lane 0 starts loading the length of edge (a, b); it is parked one step later
   __device__ __forceinline__ void load(uint32_t a, uint32_t b) {
-    if (active && lane == 0) pending = __ldg(dist + (size_t)a * n + b);
+    // 32-bit index: n <= 65535, so a * n + b < 2^32 (one IMAD instead of 64-bit math)
+    if (active && lane == 0) pending = __ldg(dist + (a * (uint32_t)n + b));
   }
   __device__ __forceinline__ void push() {
     if (!active) return;
