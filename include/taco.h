@@ -253,6 +253,16 @@ int taco_select_replay(int n, int m, int step, uint64_t key0, uint64_t key1,
 #define TACO_EDGE_ATT 3     /* TSPLIB ATT pseudo-Euclidean    tsplib.py:211-214 */
 
 /*
+ * Column 0 of the step's reference block, E[a, 0] for every ant (e0_out, m
+ * f64), decoded on the device like taco_select_replay: the roulette wheel's
+ * thresholds are u = exp(-E[:, 0]) (rng.step_uniforms rng.py:52-62), taken by
+ * the host with numpy's own exp for bit parity.  flags_out as above.
+ */
+int taco_replay_first_column(int n, int m, uint64_t key0, uint64_t key1,
+                             void *workspace, size_t ws_bytes, double *e0_out,
+                             unsigned *flags_out, void *stream);
+
+/*
  * Instance on the device from (n, 2) f64 coordinates:
  * dist under `edge_weight` and eta = 1/dist off the diagonal, bit-exact with
  * euclidean_instance (model.py:124-134) / build_instance (model.py:98-119)

@@ -56,6 +56,7 @@ SIGNATURES = {
     "taco_replay_workspace_bytes": (_c_size, [_c_int, _c_int]),
     "taco_select_replay": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u64, _p, _p, _p, _p, _p, _c_size, _p, _p,
                                     _p]),
+    "taco_replay_first_column": (_c_int, [_c_int, _c_int, _c_u64, _c_u64, _p, _c_size, _p, _p, _p]),
     "taco_construct_rw": (_c_int, [_c_int, _c_int, _c_int, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _c_int, _p,
                                    _p]),
     "taco_rw_parity": (_c_int, [_c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p, _c_int, _p]),

@@ -103,9 +103,10 @@ def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = No
     variant: "sorted" (pruned scan of the row-sorted table) or "dense" (full
     row streaming); both return identical tours.
     Roulette wheel (selection="rw", colony.py:127-141) spins on P itself:
-    stream="device" draws one threshold per (step, ant) on chip; "numpy"
-    uses the reference's thresholds exp(-E[:, 0]) (rng.py:52-62) and returns
-    its tours bit for bit; "replay" is not available for RW.
+    stream="device" draws one threshold per (step, ant) on chip; "numpy" and
+    "replay" use the reference's thresholds exp(-E[:, 0]) (rng.py:52-62) —
+    generated by numpy, or decoded on the device with numpy taking the exp —
+    and return its tours bit for bit.
     """
     if probe is not None:
         raise NotImplementedError("construction probes are not supported by the device engine")
@@ -157,10 +158,7 @@ def _construct_roulette(p_host, n, m, seed, iteration, dev, dist, stream):
         _device.construct_rw(n, m, 0, p_t, seed, iteration, tours, status, dist=dist, costs_out=costs)
         _raise_construct_status(status)
         return tours, costs
-    if stream == "replay":
-        raise NotImplementedError("roulette-wheel thresholds are exp(-E) under numpy's own exp; "
-                                  "use stream='numpy' for RW reference parity")
-    if stream != "numpy":
+    if stream not in ("numpy", "replay"):
         raise ValueError(f"stream must be 'device', 'replay' or 'numpy', got {stream!r}")
     starts = _rng.start_cities(seed, iteration, m, n)
     current = _device.upload(starts, dev)
@@ -169,13 +167,46 @@ def _construct_roulette(p_host, n, m, seed, iteration, dev, dist, stream):
     tours = torch.zeros((m, n), dtype=torch.int64, device=dev)
     tours[:, 0] = current
     lib, hs = _lib.load(), _device.stream_handle()
+    replay = rw_replay_thresholds(seed, iteration, m, n, dev) if stream == "replay" else None
     for step in range(1, n):
-        u_t = _device.upload(_rng.step_uniforms(seed, iteration, step, m, n), dev)
+        u = replay(step) if replay else _rng.step_uniforms(seed, iteration, step, m, n)
+        u_t = _device.upload(u, dev)
         _lib.check(lib.taco_rw_parity(n, m, step, p_t.data_ptr(), u_t.data_ptr(), current.data_ptr(),
                                       visited.data_ptr(), tours.data_ptr(), status.data_ptr(), None, 0, hs),
                    "taco_rw_parity")
+    if replay:
+        replay.check()
     _raise_construct_status(status)
     return tours, _device.tour_cost(tours, dist)
+
+
+class rw_replay_thresholds:
+    """The reference's roulette thresholds u = exp(-E[:, 0]) of each step
+    (rng.step_uniforms rng.py:52-62): column 0 of the step's Exp(1) block is
+    decoded on the device from numpy's Philox key (taco_replay_first_column),
+    and the exponential is taken by numpy itself, so u is the reference's bit
+    for bit (one m-element round trip per step instead of the (m, n) block)."""
+
+    def __init__(self, seed: int, iteration: int, m: int, n: int, dev):
+        self.m, self.n, self.dev = m, n, dev
+        self.keys = _rng.step_keys(seed, iteration, n)
+        lib = _lib.load()
+        self.ws_bytes = int(lib.taco_replay_workspace_bytes(m, n))
+        self.ws = torch.empty(self.ws_bytes, dtype=torch.uint8, device=dev)
+        self.flags = torch.zeros(2, dtype=torch.int32, device=dev)
+        self.e0 = torch.empty(m, dtype=torch.float64, device=dev)
+
+    def __call__(self, step: int) -> np.ndarray:
+        k0, k1 = (int(v) for v in self.keys[step - 1])
+        _lib.check(_lib.load().taco_replay_first_column(self.n, self.m, k0, k1, self.ws.data_ptr(), self.ws_bytes,
+                                                        self.e0.data_ptr(), self.flags.data_ptr(),
+                                                        _device.stream_handle()), "taco_replay_first_column")
+        return np.exp(-_device.download(self.e0))  # numpy's exp, as rng.py:62
+
+    def check(self) -> None:
+        ambiguous, overflow = (int(v) for v in self.flags.cpu().tolist())
+        if ambiguous or overflow:
+            raise ReplayUnreliable(f"replay flags: {ambiguous} close wedge tests, overflow={overflow}")
 
 
 def _raise_construct_status(status: torch.Tensor) -> None:

@@ -204,6 +204,38 @@ __global__ void k_np_count(uint64_t words, const uint32_t *cov, uint32_t *cnt) {
 }
 
 // One warp per ant: the reference's lockstep round on the replayed block.
+// Stream position of sample k (the k-th uncovered position): binary search
+// over the per-word start counts, then the k-th free bit.
+__device__ __forceinline__ uint64_t sample_position(const ReplayWs &ws, uint64_t k) {
+  const uint64_t words = ws.P / 32;
+  uint64_t lo = 0, hi = words;  // invariant: starts_before(lo) <= k
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) / 2;
+    const uint64_t sb = 32 * mid - ws.before[mid];
+    if (sb <= k) lo = mid; else hi = mid;
+  }
+  uint32_t freebits = ~ws.cov[lo];
+  uint64_t rank = k - (32 * lo - ws.before[lo]);
+  while (rank >= (uint64_t)__popc(freebits)) {  // (only past the last word on overflow)
+    rank -= __popc(freebits);
+    ++lo;
+    freebits = lo < words ? ~ws.cov[lo] : 0xffffffffu;
+  }
+  return lo * 32 + (__fns(freebits, 0, (int)rank + 1));
+}
+
+// E[a, 0] of the step's (m, n) block for every ant: the roulette wheel's
+// threshold source, u = exp(-E[:, 0]) (rng.step_uniforms rng.py:52-62)
+__global__ void k_np_first(int n, int m, uint64_t k0, uint64_t k1, ReplayWs ws, double *e0) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= m) return;
+  const uint64_t pos = sample_position(ws, (uint64_t)a * n);
+  if (pos + 1 > ws.P) atomicOr(ws.flags + 1, 1u);
+  int len;
+  const NpWords word{ws.words, ws.P, k0, k1};
+  e0[a] = np_sample(pos, word(pos), word, len, nullptr);
+}
+
 template <int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     k_np_select(int n, int m, int step, uint64_t k0, uint64_t k1, const double *__restrict__ logw,
@@ -211,23 +243,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int lane = threadIdx.x & 31;
   const int a = blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (a >= m) return;
-  const uint64_t words = ws.P / 32;
-  // position of sample k0 = a * n: last word w with starts_before(w) <= k0
-  const uint64_t k_first = (uint64_t)a * n;
-  uint64_t lo = 0, hi = words;  // invariant: starts_before(lo) <= k_first
-  while (hi - lo > 1) {
-    const uint64_t mid = (lo + hi) / 2;
-    const uint64_t sb = 32 * mid - ws.before[mid];
-    if (sb <= k_first) lo = mid; else hi = mid;
-  }
-  uint32_t freebits = ~ws.cov[lo];
-  uint64_t rank = k_first - (32 * lo - ws.before[lo]);
-  while (rank >= (uint64_t)__popc(freebits)) {  // (only past the last word on overflow)
-    rank -= __popc(freebits);
-    ++lo;
-    freebits = lo < words ? ~ws.cov[lo] : 0xffffffffu;
-  }
-  uint64_t pos = lo * 32 + (__fns(freebits, 0, (int)rank + 1));
+  uint64_t pos = sample_position(ws, (uint64_t)a * n);
 
   const int64_t cur = current[a];
   const double *lr = logw + (size_t)cur * n;
@@ -318,14 +334,8 @@ extern "C" size_t taco_replay_workspace_bytes(int m, int n) {
   return al256(P * 8) + 3 * al256(words * 4) + al256(P) + al256(scan_bytes(words));
 }
 
-extern "C" int taco_select_replay(int n, int m, int step, uint64_t key0, uint64_t key1, const double *logw,
-                                  int64_t *current, uint8_t *visited, int64_t *tours, void *workspace,
-                                  size_t ws_bytes, unsigned *flags_out, int32_t *status, void *stream) {
-  if (n < 2 || m < 1 || step < 1 || step >= n || logw == nullptr || workspace == nullptr) return TACO_ERR_ARG;
-  if (flags_out == nullptr || ws_bytes < taco_replay_workspace_bytes(m, n)) return TACO_ERR_ARG;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  ReplayWs r = carve(workspace, m, n);
-  r.flags = flags_out;
+// the step's decode pipeline: words, slow-path cover, sample-start counts
+static int replay_decode(ReplayWs &r, uint64_t key0, uint64_t key1, unsigned *flags_out, cudaStream_t s) {
   const uint64_t words = r.P / 32;
   if (cudaMemsetAsync(r.slow, 0, words * 4, s) != cudaSuccess ||
       cudaMemsetAsync(r.cov, 0, words * 4, s) != cudaSuccess)
@@ -340,9 +350,36 @@ extern "C" int taco_select_replay(int n, int m, int step, uint64_t key0, uint64_
   size_t tb = r.scan_bytes;
   if (cub::DeviceScan::ExclusiveSum(r.scan_tmp, tb, r.before, r.before, (int)words, s) != cudaSuccess)
     return TACO_ERR_CUDA;
+  return TACO_OK;
+}
+
+extern "C" int taco_select_replay(int n, int m, int step, uint64_t key0, uint64_t key1, const double *logw,
+                                  int64_t *current, uint8_t *visited, int64_t *tours, void *workspace,
+                                  size_t ws_bytes, unsigned *flags_out, int32_t *status, void *stream) {
+  if (n < 2 || m < 1 || step < 1 || step >= n || logw == nullptr || workspace == nullptr) return TACO_ERR_ARG;
+  if (flags_out == nullptr || ws_bytes < taco_replay_workspace_bytes(m, n)) return TACO_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  ReplayWs r = carve(workspace, m, n);
+  r.flags = flags_out;
+  const int rc = replay_decode(r, key0, key1, flags_out, s);
+  if (rc != TACO_OK) return rc;
   constexpr int WARPS = 8;
   k_np_select<WARPS><<<(m + WARPS - 1) / WARPS, WARPS * 32, 0, s>>>(n, m, step, key0, key1, logw, current,
                                                                    visited, tours, r, status);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
+
+extern "C" int taco_replay_first_column(int n, int m, uint64_t key0, uint64_t key1, void *workspace,
+                                        size_t ws_bytes, double *e0_out, unsigned *flags_out, void *stream) {
+  if (n < 2 || m < 1 || workspace == nullptr || e0_out == nullptr || flags_out == nullptr) return TACO_ERR_ARG;
+  if (ws_bytes < taco_replay_workspace_bytes(m, n)) return TACO_ERR_ARG;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  ReplayWs r = carve(workspace, m, n);
+  r.flags = flags_out;
+  const int rc = replay_decode(r, key0, key1, flags_out, s);
+  if (rc != TACO_OK) return rc;
+  k_np_first<<<(m + 255) / 256, 256, 0, s>>>(n, m, key0, key1, r, e0_out);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }

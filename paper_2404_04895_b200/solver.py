@@ -128,9 +128,6 @@ class Solver:
         self.shard: AntShard = shard_ants(p.m, rank, world)
         if stream == "replay" and world > 1:
             raise ValueError("the reference-stream replay runs on one GPU")
-        if stream == "replay" and self.rw:
-            raise ValueError("the reference-stream replay covers IR / AdaIR; RW parity runs through "
-                             "construct_tours(stream='numpy')")
 
         self.di = device_inst if device_inst is not None else _device.device_instance(self.inst)
         dev = self.dev = self.di.dev
@@ -343,19 +340,33 @@ class Solver:
         from .colony import ReplayUnreliable
 
         n, p, lib = self.n, self.params, _lib.load()
+        starts = torch.from_numpy(_rng.start_cities(p.seed, it, p.m, n)).to(self.dev)
+        self.current.copy_(starts)
+        self.visited.zero_()
+        self.visited[torch.arange(p.m, device=self.dev), starts] = 1
+        self.tours64[:, 0] = starts
+        stream = _device.stream_handle()
+        if self.rw:  # roulette wheel on the reference's thresholds (colony.py:127-134)
+            from .colony import rw_replay_thresholds
+
+            thresholds = rw_replay_thresholds(p.seed, it, p.m, n, self.dev)
+            for step in range(1, n):
+                u_t = _device.upload(thresholds(step), self.dev)
+                _lib.check(lib.taco_rw_parity(n, p.m, step, self.p.data_ptr(), u_t.data_ptr(),
+                                              self.current.data_ptr(), self.visited.data_ptr(),
+                                              self.tours64.data_ptr(), self.status.data_ptr(), None, 0, stream),
+                           "taco_rw_parity")
+            self.tours_local.copy_(self.tours64)
+            _device.tour_cost(self.tours64, self.di.dist, self.costs_local)
+            thresholds.check()
+            return
         gamma = construction_gamma(p, it)
         ph = _device.download(self.p)
         logw = np.full(ph.shape, -np.inf)
         np.log(ph, out=logw, where=ph > 0)  # selection.py:72-74, numpy's own log
         np.divide(logw, gamma, out=logw)
         self.logw.copy_(torch.from_numpy(logw))
-        starts = torch.from_numpy(_rng.start_cities(p.seed, it, p.m, n)).to(self.dev)
-        self.current.copy_(starts)
-        self.visited.zero_()
-        self.visited[torch.arange(p.m, device=self.dev), starts] = 1
-        self.tours64[:, 0] = starts
         keys = _rng.step_keys(p.seed, it, n)
-        stream = _device.stream_handle()
         for step in range(1, n):
             k0, k1 = (int(v) for v in keys[step - 1])
             _lib.check(lib.taco_select_replay(n, p.m, step, k0, k1, self.logw.data_ptr(), self.current.data_ptr(),

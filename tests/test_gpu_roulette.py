@@ -5,7 +5,8 @@
   adversarial rows and thresholds placed exactly on CDF values, where only the
   exact sequential recount can decide;
 * the device stream: taco_construct_rw == oracle fastpath.rw_tours;
-* the golden pipeline of the reference's RW runs (stream="numpy");
+* the golden pipeline of the reference's RW runs (stream="numpy" and the
+  device replay of its stream, drop-ins and full Solver runs);
 * the Solver with selection="rw" against the chained drop-ins.
 """
 
@@ -148,12 +149,21 @@ def test_rw_dropin_pipeline_matches_reference_golden(golden, name):
             batch = taco.construct_tours(prob, inst, params, it, stream="numpy")
             assert np.array_equal(batch.tours, golden[f"{key}/tours"])
             assert np.array_equal(batch.costs, golden[f"{key}/costs"])
+            replayed = taco.construct_tours(prob, inst, params, it, stream="replay")
+            assert np.array_equal(replayed.tours, golden[f"{key}/tours"])
             tau = taco.apply_update(tau, taco.accumulate_increments(taco.select_elite(batch, params.k), inst.n),
                                     params.rho)
             assert np.array_equal(tau.tau, golden[f"{key}/tau"])
             prob = taco.compute_probability_matrix(tau, inst, params)
-    with pytest.raises(NotImplementedError):
-        taco.construct_tours(prob, inst, params, 0, stream="replay")
+    # full Solver runs on the reference's streams reproduce the golden runs
+    for seed in golden[f"{name}/seeds"].tolist():
+        params = taco.AcoParams(m=int(m), k=int(k), alpha=alpha, beta=beta, rho=rho, selection="rw", seed=seed)
+        s = taco.Solver(inst, params, stream="replay")
+        for it in range(int(iters)):
+            s.step()
+            key = f"{name}/s{seed}/it{it}"
+            assert np.array_equal(s.last_batch().tours, golden[f"{key}/tours"])
+            assert np.array_equal(s.pheromone().tau, golden[f"{key}/tau"])
 
 
 def test_rw_solver_matches_chained_dropins():
@@ -175,8 +185,6 @@ def test_rw_solver_matches_chained_dropins():
         assert np.array_equal(s.pheromone().tau, tau.tau)
         best = min(best, batch.costs.min())
         assert length == best
-    with pytest.raises(ValueError):
-        taco.Solver(inst, params, stream="replay")
 
 
 def test_rw_quality_below_ir_like_the_reference():
