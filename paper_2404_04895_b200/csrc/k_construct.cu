@@ -644,7 +644,6 @@ __global__ void __launch_bounds__(WARPS * 32)
 
 using namespace taco;
 
-constexpr size_t kSmemBudget = 200 * 1024;
 
 template <bool HEAD, bool PROBE>
 static int launch_sorted(const SortedArgs &a, int grid, int threads, size_t smem, cudaStream_t s) {
@@ -723,17 +722,12 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     if (const char *ev = getenv("TACO_SORTED_WARPS")) warps = atoi(ev);
     if (warps < 1 || warps > kSortedMaxWarps) return TACO_ERR_ARG;
     const size_t fixed = leaves_bytes + per_ant * warps;
+    // Shared-memory row-head cache: off by default.  Since the next row's first
+    // global window is issued a step ahead, scoring it directly beats a
+    // separate pass over a cached head at every ant count (n = 2392: m = 512
+    // 1.39 vs 1.62 ms with T = 12; m = 2048 1.68 vs 1.90; m = 4096 2.19 vs
+    // 2.45).  TACO_SORTED_T=<T> re-enables it (tuning knob).
     int T = 0;
-    for (int cand : {16, 8, 4, 2}) {
-      if (cand < n && fixed + (((size_t)6 * n * cand + 15) & ~(size_t)15) <= kSmemBudget) {
-        T = cand;
-        break;
-      }
-    }
-    // With > ~20 ants per SM the kernel is issue-bound and the extra shared
-    // window costs more than the L2 latency it hides (measured crossover at
-    // m ~ 3000 on 148 SMs, n = 2392; profiles/README.md).
-    if (m_local > 20 * sm_count()) T = 0;
     if (const char *ev = getenv("TACO_SORTED_T")) T = atoi(ev);
     if (T < 0 || T > 32 || T >= n) return TACO_ERR_ARG;
     const size_t smem = (((size_t)6 * n * T + 15) & ~(size_t)15) + fixed;
