@@ -340,6 +340,7 @@ class Solver:
         from .colony import ReplayUnreliable
 
         n, p, lib = self.n, self.params, _lib.load()
+        self.check()  # the host drives this mode step by step: raise where the reference would
         starts = torch.from_numpy(_rng.start_cities(p.seed, it, p.m, n)).to(self.dev)
         self.current.copy_(starts)
         self.visited.zero_()
