@@ -110,6 +110,23 @@ int taco_row_update(int n,
                     void *stream);
 
 /*
+ * taco_row_update restricted to rows [row_begin, row_end) (the row-partitioned
+ * multi-GPU update: each rank updates its rows of tau / P / W / the sorted
+ * table, then the tables are all-gathered).  Rows outside the range are not
+ * touched; all pointers still address the full n-row matrices.
+ */
+int taco_row_update_rows(int row_begin, int row_end, int n,
+                         const double *tau_in, double *tau_out,
+                         const double *eta_b, const int32_t *nbr,
+                         const double *inc, int k, const double *delta_in,
+                         double *delta_out, int do_evap, double keep,
+                         int want_p, double alpha, double inv_gamma,
+                         double *p_out, double *rowsum_out, float *w_out,
+                         int ldw, float *sw_out, uint16_t *si_out,
+                         int32_t *status, const taco_iter_state *state,
+                         void *stream);
+
+/*
  * The same update as taco_row_update in Solver mode (edge-map deposit,
  * evaporation, P, W / sorted table), as three streaming kernels that need no
  * row in shared memory (any n <= 65535): a warp-per-row deposit into

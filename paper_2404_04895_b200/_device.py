@@ -178,6 +178,19 @@ def row_update(n, *, tau_in=None, tau_out=None, eta_b=None, nbr=None, inc=None, 
     check(code, "taco_row_update")
 
 
+def row_update_rows(row_begin, row_end, n, *, tau_in=None, tau_out=None, eta_b=None, nbr=None, inc=None, k=0,
+                    delta_in=None, delta_out=None, do_evap=False, keep=1.0, want_p=False, alpha=1.0,
+                    inv_gamma=1.0, p_out=None, rowsum_out=None, w_out=None, ldw=0, sw_out=None, si_out=None,
+                    status=None, state=None) -> None:
+    """row_update on rows [row_begin, row_end) only (taco_row_update_rows)."""
+    code = _lib.load().taco_row_update_rows(
+        int(row_begin), int(row_end), n, ptr(tau_in), ptr(tau_out), ptr(eta_b), ptr(nbr), ptr(inc), int(k),
+        ptr(delta_in), ptr(delta_out), int(bool(do_evap)), float(keep), int(bool(want_p)), float(alpha),
+        float(inv_gamma), ptr(p_out), ptr(rowsum_out), ptr(w_out), int(ldw), ptr(sw_out), ptr(si_out), ptr(status),
+        ptr(state), stream_handle())
+    check(code, "taco_row_update_rows")
+
+
 def update_split(n, *, tau_in, tau_out, eta_b, nbr, inc, k, do_evap, keep, alpha, inv_gamma, delta_ws,
                  unnorm_ws, p_out=None, rowsum_out=None, w_out=None, ldw=0, sw_out=None, si_out=None,
                  status=None, state=None) -> None:
@@ -194,13 +207,14 @@ class SelectionTables:
     sw + column indices si), all with row pitch ldw (multiple of 32).  The
     sorted rows' pad columns stay W = 0 (zero-initialized, never selectable)."""
 
-    def __init__(self, n: int, dev, dense: bool, sorted_: bool):
+    def __init__(self, n: int, dev, dense: bool, sorted_: bool, rows: int | None = None):
         self.n = n
         self.ldw = pad_ld(n)
+        rows = n if rows is None else rows  # > n: padding rows for equal all-gather chunks
         # the sorted table is built from the dense one, so sorted implies dense
-        self.w = torch.empty((n, self.ldw), dtype=torch.float32, device=dev) if dense or sorted_ else None
-        self.sw = torch.zeros((n, self.ldw), dtype=torch.float32, device=dev) if sorted_ else None
-        self.si = torch.zeros((n, self.ldw), dtype=torch.uint16, device=dev) if sorted_ else None
+        self.w = torch.empty((rows, self.ldw), dtype=torch.float32, device=dev) if dense or sorted_ else None
+        self.sw = torch.zeros((rows, self.ldw), dtype=torch.float32, device=dev) if sorted_ else None
+        self.si = torch.zeros((rows, self.ldw), dtype=torch.uint16, device=dev) if sorted_ else None
 
 
 def selection_table_from_p(p: torch.Tensor, inv_gamma: float, tables: SelectionTables) -> None:

@@ -43,6 +43,9 @@ SIGNATURES = {
     "taco_row_update": (_c_int, [
         _c_int, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _c_f64, _c_int, _c_f64, _c_f64,
         _p, _p, _p, _c_int, _p, _p, _p, _p, _p]),
+    "taco_row_update_rows": (_c_int, [
+        _c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _c_int, _p, _p, _c_int, _c_f64, _c_int, _c_f64, _c_f64,
+        _p, _p, _p, _c_int, _p, _p, _p, _p, _p]),
     "taco_update_split": (_c_int, [_c_int, _p, _p, _p, _p, _p, _c_int, _c_int, _c_f64, _c_f64, _c_f64, _p, _p,
                                    _p, _p, _p, _c_int, _p, _p, _p, _p, _p]),
     "taco_selection_table": (_c_int, [_c_int, _p, _c_f64, _p, _c_int, _p, _p, _p]),

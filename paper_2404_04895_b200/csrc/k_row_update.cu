@@ -42,6 +42,7 @@ struct RowParams {
   uint16_t *si_out;
   int32_t *status;
   int n_leaves;
+  int row_begin, row_end;  // rows [row_begin, row_end) of the n x n matrices (row-partitioned update)
 };
 
 constexpr int kDepositChunk = 512;  // elites staged in shared memory per pass
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
   plan.n_internal = s_meta[1];
   plan.height = s_meta[2];
 
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+  for (int i = a.row_begin + blockIdx.x; i < a.row_end; i += gridDim.x) {
     const size_t rowoff = (size_t)i * n;
     // tau / eta^b of this row are loaded kBatch elements per thread at a time;
     // the first batch is issued before the deposit so it lands meanwhile
@@ -307,7 +308,9 @@ static int launch_row_t(const RowParams &a, const RowLayout &lay, cudaStream_t s
     blocks_for = lay.total;
   }
   const int sms = sm_count_row();
-  const int grid = a.n < sms * blocks_per_sm ? a.n : sms * blocks_per_sm;
+  const int rows = a.row_end - a.row_begin;
+  if (rows <= 0) return TACO_OK;
+  const int grid = rows < sms * blocks_per_sm ? rows : sms * blocks_per_sm;
   k_row_update<BLOCK><<<grid, BLOCK, lay.total, stream>>>(a, lay);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
@@ -335,13 +338,14 @@ static int launch_row(const RowParams &a, cudaStream_t stream) {
 #endif
 
 template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) k_row_sort(int n, int ldw, const float *__restrict__ w,
-                                                    float *__restrict__ sw, uint16_t *__restrict__ si) {
+__global__ void __launch_bounds__(BLOCK) k_row_sort(int n, int row_begin, int row_end, int ldw,
+                                                    const float *__restrict__ w, float *__restrict__ sw,
+                                                    uint16_t *__restrict__ si) {
   using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, cub::NullType, TACO_SORT_RADIX_BITS>;
   extern __shared__ __align__(16) unsigned char smem[];
   auto &ts = *reinterpret_cast<typename Sort::TempStorage *>(smem);
   float *wrow = reinterpret_cast<float *>(smem + ((sizeof(typename Sort::TempStorage) + 15) & ~(size_t)15));
-  for (int i = blockIdx.x; i < n; i += gridDim.x) {
+  for (int i = row_begin + blockIdx.x; i < row_end; i += gridDim.x) {
     const float *src = w + (size_t)i * ldw;
     for (int j = threadIdx.x; j < n; j += BLOCK) wrow[j] = src[j];
     __syncthreads();
@@ -366,7 +370,8 @@ __global__ void __launch_bounds__(BLOCK) k_row_sort(int n, int ldw, const float 
 }
 
 template <int BLOCK, int ITEMS>
-static int launch_sort_t(int n, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t stream) {
+static int launch_sort_t(int n, int r0, int r1, int ldw, const float *w, float *sw, uint16_t *si,
+                         cudaStream_t stream) {
   using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, cub::NullType, TACO_SORT_RADIX_BITS>;
   const size_t smem = ((sizeof(typename Sort::TempStorage) + 15) & ~(size_t)15) + (size_t)4 * n;
   if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
@@ -388,23 +393,25 @@ static int launch_sort_t(int n, int ldw, const float *w, float *sw, uint16_t *si
     configured = smem;
   }
   const int sms = sm_count_row();
-  const int grid = n < sms * blocks_per_sm ? n : sms * blocks_per_sm;
-  k_row_sort<BLOCK, ITEMS><<<grid, BLOCK, smem, stream>>>(n, ldw, w, sw, si);
+  const int rows = r1 - r0;
+  if (rows <= 0) return TACO_OK;
+  const int grid = rows < sms * blocks_per_sm ? rows : sms * blocks_per_sm;
+  k_row_sort<BLOCK, ITEMS><<<grid, BLOCK, smem, stream>>>(n, r0, r1, ldw, w, sw, si);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }
 
-static int launch_sort(int n, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t s) {
-  if (n <= 1024) return launch_sort_t<128, 8>(n, ldw, w, sw, si, s);
-  if (n <= 2560) return launch_sort_t<256, 10>(n, ldw, w, sw, si, s);
-  if (n <= 5120) return launch_sort_t<512, 10>(n, ldw, w, sw, si, s);
-  if (n <= 10240) return launch_sort_t<512, 20>(n, ldw, w, sw, si, s);
-  if (n <= 20480) return launch_sort_t<1024, 20>(n, ldw, w, sw, si, s);
+static int launch_sort(int n, int r0, int r1, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t s) {
+  if (n <= 1024) return launch_sort_t<128, 8>(n, r0, r1, ldw, w, sw, si, s);
+  if (n <= 2560) return launch_sort_t<256, 10>(n, r0, r1, ldw, w, sw, si, s);
+  if (n <= 5120) return launch_sort_t<512, 10>(n, r0, r1, ldw, w, sw, si, s);
+  if (n <= 10240) return launch_sort_t<512, 20>(n, r0, r1, ldw, w, sw, si, s);
+  if (n <= 20480) return launch_sort_t<1024, 20>(n, r0, r1, ldw, w, sw, si, s);
   return TACO_ERR_UNSUPPORTED;
 }
 
 int launch_sort_table(int n, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t s) {
-  return launch_sort(n, ldw, w, sw, si, s);
+  return launch_sort(n, 0, n, ldw, w, sw, si, s);
 }
 
 }  // namespace taco
@@ -416,15 +423,15 @@ extern "C" int taco_max_sorted_n(void) { return 20480; }
 static int launch_variant(RowParams &a, bool sorted, cudaStream_t s) {
   const int rc = launch_row(a, s);
   if (rc != TACO_OK || !sorted) return rc;
-  return launch_sort(a.n, a.ldw, a.w_out, a.sw_out, a.si_out, s);
+  return launch_sort(a.n, a.row_begin, a.row_end, a.ldw, a.w_out, a.sw_out, a.si_out, s);
 }
 
-extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, const double *eta_b,
-                               const int32_t *nbr, const double *inc, int k, const double *delta_in,
-                               double *delta_out, int do_evap, double keep, int want_p, double alpha,
-                               double inv_gamma, double *p_out, double *rowsum_out, float *w_out,
-                               int ldw, float *sw_out, uint16_t *si_out, int32_t *status,
-                               const taco_iter_state *state, void *stream) {
+static int row_update_impl(int row_begin, int row_end, int n, const double *tau_in, double *tau_out,
+                           const double *eta_b, const int32_t *nbr, const double *inc, int k,
+                           const double *delta_in, double *delta_out, int do_evap, double keep, int want_p,
+                           double alpha, double inv_gamma, double *p_out, double *rowsum_out, float *w_out,
+                           int ldw, float *sw_out, uint16_t *si_out, int32_t *status, const taco_iter_state *state,
+                           void *stream) {
   if (n < 3 || n > 65535) return TACO_ERR_ARG;
   if (tau_in == nullptr && (do_evap || want_p || tau_out != nullptr)) return TACO_ERR_ARG;
   if (nbr != nullptr && (inc == nullptr || k < 1)) return TACO_ERR_ARG;
@@ -459,7 +466,33 @@ extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, con
   a.si_out = si_out;
   a.status = status;
   a.n_leaves = want_p ? pw_num_leaves(n) : 0;
+  a.row_begin = row_begin;
+  a.row_end = row_end;
   return launch_variant(a, sw_out != nullptr, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int taco_row_update(int n, const double *tau_in, double *tau_out, const double *eta_b,
+                               const int32_t *nbr, const double *inc, int k, const double *delta_in,
+                               double *delta_out, int do_evap, double keep, int want_p, double alpha,
+                               double inv_gamma, double *p_out, double *rowsum_out, float *w_out,
+                               int ldw, float *sw_out, uint16_t *si_out, int32_t *status,
+                               const taco_iter_state *state, void *stream) {
+  return row_update_impl(0, n, n, tau_in, tau_out, eta_b, nbr, inc, k, delta_in, delta_out, do_evap, keep, want_p,
+                         alpha, inv_gamma, p_out, rowsum_out, w_out, ldw, sw_out, si_out, status, state, stream);
+}
+
+// rows [row_begin, row_end) only (row-partitioned multi-GPU update): same
+// arguments as taco_row_update; rows outside the range are not touched
+extern "C" int taco_row_update_rows(int row_begin, int row_end, int n, const double *tau_in, double *tau_out,
+                                    const double *eta_b, const int32_t *nbr, const double *inc, int k,
+                                    const double *delta_in, double *delta_out, int do_evap, double keep,
+                                    int want_p, double alpha, double inv_gamma, double *p_out, double *rowsum_out,
+                                    float *w_out, int ldw, float *sw_out, uint16_t *si_out, int32_t *status,
+                                    const taco_iter_state *state, void *stream) {
+  if (row_begin < 0 || row_end < row_begin || row_end > n) return TACO_ERR_ARG;
+  return row_update_impl(row_begin, row_end, n, tau_in, tau_out, eta_b, nbr, inc, k, delta_in, delta_out, do_evap,
+                         keep, want_p, alpha, inv_gamma, p_out, rowsum_out, w_out, ldw, sw_out, si_out, status,
+                         state, stream);
 }
 
 extern "C" int taco_selection_table(int n, const double *p, double inv_gamma, float *w_out, int ldw,
@@ -480,6 +513,8 @@ extern "C" int taco_selection_table(int n, const double *p, double inv_gamma, fl
   a.sw_out = sw_out;
   a.si_out = si_out;
   a.n_leaves = 0;
+  a.row_begin = 0;
+  a.row_end = n;
   return launch_variant(a, sw_out != nullptr, reinterpret_cast<cudaStream_t>(stream));
 }
 

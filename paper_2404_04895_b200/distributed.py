@@ -14,6 +14,14 @@ rank them identically on every rank, then assemble only the k elite tours
 with one SUM all-reduce of a k x n buffer in which each rank filled the rows
 it owns (taco_shard_elites) — k·n·4 bytes instead of m·n·4 (10x less at
 k = m/10).  ``gather_colony`` (all tours) remains for ``last_batch()``.
+
+Row-partitioned update (the default when sharded): the deposit is identical
+on every rank, and the row update is independent per row (colony.py:27-60,
+evaporation + row normalization), so rank r updates only rows
+[r·nr, (r+1)·nr) of tau, P and the selection table (``row_partition``) and
+the construction input is then all-gathered in place (``gather_rows``):
+n²·4·(R-1)/R bytes in, (R-1)/R of the update work saved.  ``share_status``
+keeps the fail-stop status words identical on every rank.
 """
 
 from __future__ import annotations
@@ -115,3 +123,54 @@ def share_elites(elite_tours: torch.Tensor, group=None) -> torch.Tensor:
     an integer SUM all-reduce leaves every elite tour on every rank, exactly."""
     dist.all_reduce(elite_tours, op=dist.ReduceOp.SUM, group=group)
     return elite_tours
+
+
+@dataclass(frozen=True)
+class RowPartition:
+    """Rows [begin, end) of an n-row table owned by one rank; every rank's
+    chunk is `chunk` rows (the buffers carry world * chunk rows, the tail
+    rows past n are padding) so one equal-size all-gather moves them."""
+
+    rank: int
+    world: int
+    n: int
+    chunk: int
+    begin: int
+    end: int
+
+    @property
+    def rows(self) -> int:
+        return self.world * self.chunk
+
+
+def row_partition(n: int, rank: int, world: int) -> RowPartition:
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of world {world}")
+    chunk = -(-n // world)
+    return RowPartition(rank, world, n, chunk, min(n, rank * chunk), min(n, (rank + 1) * chunk))
+
+
+def gather_rows(buf: torch.Tensor, part: RowPartition, group=None) -> torch.Tensor:
+    """In-place all-gather of a row-partitioned (world * chunk, ...) buffer:
+    afterwards every rank holds every rank's rows."""
+    if buf.shape[0] != part.rows or not buf.is_contiguous():
+        raise ValueError(f"need a contiguous buffer of {part.rows} rows, got {tuple(buf.shape)}")
+    c = part.chunk
+    raw = buf.view(torch.uint8)  # as bytes: gloo / NCCL have no uint16 (the sorted table's indices)
+    _all_gather_into(raw, raw[part.rank * c:(part.rank + 1) * c], group)
+    return buf
+
+
+_INT32_MAX = 2**31 - 1
+
+
+def share_status(status: torch.Tensor, group=None) -> torch.Tensor:
+    """Make the 4 fail-stop status words (include/taco.h) identical on every
+    rank without a host sync: one MAX all-reduce of
+    (code << 32 | INT32_MAX - row) — the highest code wins, then the smallest
+    row / ant.  status[3] (the local stop flag) is left alone."""
+    key = status[0:1].to(torch.int64) * (1 << 32) + (_INT32_MAX - status[1:2].to(torch.int64))
+    dist.all_reduce(key, op=dist.ReduceOp.MAX, group=group)
+    status[0:1].copy_(key >> 32)
+    status[1:2].copy_(_INT32_MAX - (key & 0xFFFFFFFF))
+    return status

@@ -11,11 +11,14 @@ HBM and five kernel launches per iteration:
     1. taco_construct        tours (m x n int32) from the fp32 selection table,
                              with their lengths accumulated on the fly in
                              numpy's pairwise order
-       [multi-GPU: all-gather of tours + lengths over NCCL]
+       [multi-GPU: all-gather of the m lengths over NCCL]
     3. taco_elite_order      stable radix argsort of the lengths
     4. taco_track_best       best-so-far tour / length on device
        taco_elite_neighbors  (prev, next) of every city in the k elite tours
+       [multi-GPU: taco_shard_elites + SUM all-reduce of the k elite tours]
     5. taco_row_update       deposit + evaporation + P + W(gamma of it+1)
+       [multi-GPU, row-partitioned: this rank's rows only, then an in-place
+        all-gather of the selection table and of the status words]
 
 The host synchronizes only when a result is read (``step()`` returns the best
 tour and length; ``run()`` reads once at the end).
@@ -38,7 +41,8 @@ import torch.distributed as tdist
 
 from . import _device, _lib
 from .colony import NumericalUnderflow, construction_gamma
-from .distributed import AntShard, gather_colony, gather_costs, shard_ants, share_elites
+from .distributed import (AntShard, gather_colony, gather_costs, gather_rows, row_partition, shard_ants,
+                          share_elites, share_status)
 from .model import AcoParams, PheromoneState, ProbabilityMatrix, Selection, TourBatch, instance_from_distances
 
 
@@ -91,6 +95,9 @@ class Solver:
     pheromone, best lengths) — the parity mode, one GPU only.
     group: torch.distributed group to shard ants over (default: the world
     group when initialized with more than one rank).
+    update: "replicated" (every rank updates all rows) or "partitioned" (each
+    rank updates its n/R rows of tau / P / the selection table and the table
+    rows are all-gathered; default when sharded).
     graph: replay a captured CUDA graph per iteration (default: on for a
     single-GPU device-stream colony with n*m < 2^16, where launch
     overhead matters; the sharded and replay modes always run eagerly).
@@ -101,7 +108,7 @@ class Solver:
     FUSED_MAX_N = 27000  # the fused row kernel stages a row of n doubles in shared memory
 
     def __init__(self, instance, params=None, *, construct: str = "sorted", stream: str = "device",
-                 group=None, graph: bool | None = None, **overrides):
+                 group=None, graph: bool | None = None, update: str | None = None, **overrides):
         if isinstance(instance, _device.DeviceInstance):  # built on the device (from_coords)
             self.inst, device_inst = None, instance
         else:
@@ -129,18 +136,31 @@ class Solver:
         if stream == "replay" and world > 1:
             raise ValueError("the reference-stream replay runs on one GPU")
 
+        if update is None:
+            update = "partitioned" if world > 1 else "replicated"
+        if update not in ("replicated", "partitioned"):
+            raise ValueError(f"update must be 'replicated' or 'partitioned', got {update!r}")
+        # (rows past the fused row kernel's shared memory take the replicated
+        # split update)
+        self.partitioned = update == "partitioned" and world > 1 and n <= self.FUSED_MAX_N
+        # row partition: this rank updates rows [begin, end); the row buffers
+        # carry world * chunk rows so the table all-gather has equal chunks
+        self._part = row_partition(n, rank, world) if self.partitioned else row_partition(n, 0, 1)
+        rows = self._part.rows if self.partitioned else n
+
         self.di = device_inst if device_inst is not None else _device.device_instance(self.inst)
         dev = self.dev = self.di.dev
         m, k = p.m, p.k
         self.eta_b = self.di.eta_beta(p.beta)
-        self.tau = torch.full((n, n), float(p.q0_tau), dtype=torch.float64, device=dev)
-        self.tau.fill_diagonal_(0.0)
+        self.tau = torch.zeros((rows, n), dtype=torch.float64, device=dev)
+        self.tau[:n].fill_(float(p.q0_tau))
+        self.tau[:n].fill_diagonal_(0.0)
         replay = stream == "replay"
         table = not (replay or self.rw)
         self.tables = _device.SelectionTables(n, dev, dense=(construct == "dense" and table),
-                                              sorted_=(construct == "sorted" and table))
+                                              sorted_=(construct == "sorted" and table), rows=rows)
         if self.rw:  # P (f64) is the spin input; steps that needed the exact recount
-            self.p = torch.empty((n, n), dtype=torch.float64, device=dev)
+            self.p = torch.empty((rows, n), dtype=torch.float64, device=dev)
             self.rw_exact_steps = torch.zeros(1, dtype=torch.int64, device=dev)
         if replay:  # reference-stream state: P, the numpy log table, lockstep buffers
             self.p = torch.empty((n, n), dtype=torch.float64, device=dev)
@@ -228,10 +248,42 @@ class Solver:
             alpha=float(self.params.alpha), inv_gamma=1.0 / gamma_next, p_out=self.p if p_mode else None,
             rowsum_out=self.rowsum, w_out=None if p_mode else t.w, ldw=t.ldw,
             sw_out=None if p_mode else t.sw, si_out=None if p_mode else t.si, status=self.status, state=state)
-        if self._split_update:
+        if self.partitioned:  # my rows, then every rank's rows of the construction input
+            _device.row_update_rows(self._part.begin, self._part.end, self.n, want_p=True, **common)
+            if p_mode:
+                self._gather_rows(self.p)
+            elif t.sw is not None:
+                self._gather_rows(t.sw)
+                self._gather_rows(t.si)
+            else:
+                self._gather_rows(t.w)
+        elif self._split_update:
             _device.update_split(self.n, delta_ws=self._delta_ws, unnorm_ws=self._unnorm_ws, **common)
         else:
             _device.row_update(self.n, want_p=True, **common)
+        if self.shard.world > 1:
+            self._share_status()
+
+    def _share_status(self) -> None:
+        """Make the status words identical on every rank (device-side, no host
+        sync): a failure seen by one rank's ants or rows stops every rank's next
+        construction, and every rank raises it at the same step.  One MAX
+        all-reduce of (code << 32 | INT32_MAX - row): the highest code wins,
+        then the smallest row / ant."""
+        st = self.status
+        key = st[0:1].to(torch.int64) * (1 << 32) + (_INT32_MAX - st[1:2].to(torch.int64))
+        tdist.all_reduce(key, op=tdist.ReduceOp.MAX, group=self.group)
+        st[0:1].copy_(key >> 32)
+        st[1:2].copy_(_INT32_MAX - (key & 0xFFFFFFFF))
+
+    def _gather_rows(self, buf: torch.Tensor) -> None:
+        gather_rows(buf, self._part, self.group)
+
+    def _share_status(self) -> None:
+        """Fail-stop across ranks: a failure seen by one rank's ants or rows
+        stops every rank's next construction, and every rank raises it at the
+        same step (device-side, no host sync)."""
+        share_status(self.status, self.group)
 
     def _write_state(self, it: int) -> None:
         """Device state for iteration `it`: (it, 1/gamma(it + 1))."""
@@ -382,14 +434,20 @@ class Solver:
             raise ReplayUnreliable(f"replay flags: {ambiguous} close wedge tests, overflow={overflow}")
 
     def check(self) -> None:
-        """Raise the reference's exception for any failure recorded so far."""
-        code, _ = _device.read_status(self.status)
+        """Raise the reference's exception for any failure recorded so far
+        (with a row-partitioned update, the underflow report is a collective;
+        every rank raises it at the same step)."""
+        code, _ = _device.read_status(self.status)  # identical on every rank (_share_status)
         self._raise_status(code)
 
     def _raise_status(self, code: int) -> None:
         if code == _lib.TACO_UNDERFLOW:
             from .colony import _underflow_from_sums
-            raise _underflow_from_sums(_device.download(self.rowsum))
+            sums = self.rowsum
+            if self.partitioned:  # each rank wrote its own rows of the sums (the rest stay 0)
+                sums = sums.clone()
+                tdist.all_reduce(sums, op=tdist.ReduceOp.SUM, group=self.group)
+            raise _underflow_from_sums(_device.download(sums))
         if code == _lib.TACO_NO_CANDIDATE:
             raise AssertionError("selector chose a visited city")
         if code != 0:
@@ -436,7 +494,9 @@ class Solver:
         state is (tau, iteration), model.py:218-232)."""
         self.check()
         tour, length = self.best()
-        return {"tau": _device.download(self.tau).copy(), "iteration": int(self.iteration),
+        if self.partitioned:
+            self._gather_rows(self.tau)
+        return {"tau": _device.download(self.tau[:self.n]).copy(), "iteration": int(self.iteration),
                 "best_tour": tour, "best_length": length, "best_iteration": int(self.best_iter.item()),
                 "n": int(self.n), "seed": int(self.params.seed)}
 
@@ -449,7 +509,7 @@ class Solver:
             raise ValueError(f"tau must have shape ({self.n}, {self.n})")
         it = int(ckpt["iteration"])
         self.status.copy_(_device.new_status(self.dev))  # a restored solver starts healthy
-        self.tau.copy_(torch.from_numpy(np.ascontiguousarray(tau)))
+        self.tau[:self.n].copy_(torch.from_numpy(np.ascontiguousarray(tau)))
         self.best_tour.copy_(torch.from_numpy(np.asarray(ckpt["best_tour"], dtype=np.int32)))
         self.best_cost.fill_(float(ckpt["best_length"]))
         self.best_iter.fill_(int(ckpt["best_iteration"]))
@@ -470,10 +530,15 @@ class Solver:
 
     # ---- state inspection (host copies) ---------------------------------
     def pheromone(self) -> PheromoneState:
-        return PheromoneState(tau=_device.download(self.tau), iteration=self.iteration)
+        """tau (a collective when row-partitioned: the rows are all-gathered)."""
+        if self.partitioned:
+            self._gather_rows(self.tau)
+        return PheromoneState(tau=_device.download(self.tau[:self.n]), iteration=self.iteration)
 
     def probability(self) -> ProbabilityMatrix:
-        p = torch.empty_like(self.tau)
+        if self.partitioned:
+            self._gather_rows(self.tau)
+        p = torch.empty_like(self.tau[:self.n])
         _device.row_update(self.n, tau_in=self.tau, eta_b=self.eta_b, want_p=True,
                            alpha=float(self.params.alpha), p_out=p)
         return ProbabilityMatrix(p=_device.download(p))

@@ -1,4 +1,4 @@
-"""CPU, world_size 2 over gloo: the multi-GPU plumbing of the Solver.
+"""CPU, world_size 2-4 over gloo: the multi-GPU plumbing of the Solver.
 
 Each rank builds its contiguous ant shard (here with the oracle's restatement
 of the device stream, keyed by GLOBAL ant id), the colony is all-gathered
@@ -98,3 +98,54 @@ def test_sharded_colony_equals_single_process(tmp_path, m):
         assert np.array_equal(r["order2"], order)
         assert np.array_equal(r["elite"], want[order])
         assert np.array_equal(r["delta2"], ranks[0]["delta"])
+
+
+def _row_worker(rank: int, world: int, port: int, n: int, out_dir: str) -> None:
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from paper_2404_04895_b200 import distributed
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        # each rank runs the row update on its rows only (here: the oracle's
+        # row normalization), the table rows are then gathered in place
+        tau = ref.initial_tau(n, 1.0) + np.random.default_rng(3).uniform(0, 1, (n, n))
+        _, eta = ref.instance_arrays(np.random.default_rng(42).uniform(0, 1000, (n, 2)))
+        part = distributed.row_partition(n, rank, world)
+        p_full = ref.transition(tau, eta, 1.0, 2.0)
+        buf = torch.full((part.rows, n), -1.0, dtype=torch.float64)
+        buf[part.begin:part.end] = torch.from_numpy(p_full[part.begin:part.end])
+        distributed.gather_rows(buf, part)
+        # status: rank 1 saw (NO_CANDIDATE, ant 5), rank 0 (NO_CANDIDATE, ant 9)
+        # and, in a second round, rank 0 an UNDERFLOW at row 40 — highest code,
+        # then smallest row, on every rank
+        st = torch.tensor([2, 9 if rank == 0 else 5, 0, rank], dtype=torch.int32)
+        distributed.share_status(st)
+        st2 = torch.tensor([1, 40, 0, 0] if rank == 0 else [0, 2**31 - 1, 0, 0], dtype=torch.int32)
+        distributed.share_status(st2)
+        st3 = torch.tensor([0, 2**31 - 1, 0, 0], dtype=torch.int32)
+        distributed.share_status(st3)
+        np.savez(os.path.join(out_dir, f"rows{rank}.npz"), p=buf.numpy()[:n], want=p_full, st=st.numpy(),
+                 st2=st2.numpy(), st3=st3.numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,n", [(2, 23), (3, 10), (4, 3)])  # uneven chunks, an empty rank
+def test_row_partitioned_update_gathers_every_row(tmp_path, world, n):
+    from paper_2404_04895_b200.distributed import row_partition
+
+    parts = [row_partition(n, r, world) for r in range(world)]
+    assert parts[0].begin == 0 and parts[-1].end == n
+    assert all(a.end == b.begin for a, b in zip(parts, parts[1:]))
+    assert all(p.end - p.begin <= p.chunk for p in parts)
+    mp.start_processes(_row_worker, args=(world, _free_port(), n, str(tmp_path)), nprocs=world,
+                       start_method="spawn", join=True)
+    for r in range(world):
+        got = np.load(tmp_path / f"rows{r}.npz")
+        assert np.array_equal(got["p"], got["want"])
+        assert got["st"][:2].tolist() == [2, 5] and got["st"][3] == r  # the local stop flag stays
+        assert got["st2"][:2].tolist() == [1, 40]
+        assert got["st3"][:2].tolist() == [0, 2**31 - 1]

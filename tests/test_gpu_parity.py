@@ -495,6 +495,51 @@ def test_split_update_equals_fused_row_kernel(n, k, gamma, same):
         assert np.array_equal(a, b)
 
 
+@pytest.mark.parametrize("n,cuts", [(300, (0, 1, 150, 299, 300)), (1000, (0, 333, 666, 1000))])
+def test_row_range_update_pieces_equal_whole(n, cuts):
+    """taco_row_update_rows over a row partition (the multi-GPU row-partitioned
+    update) == taco_row_update over all rows, and rows outside the range are
+    untouched."""
+    dev = _device.device()
+    g = np.random.default_rng(n + 1)
+    tau0 = torch.from_numpy(g.uniform(1e-3, 2.0, (n, n))).to(dev)
+    eta = torch.from_numpy(g.uniform(0.01, 1.0, (n, n))).to(dev)
+    k = 7
+    tours = np.stack([g.permutation(n) for _ in range(k)])
+    nbr = np.zeros((n, k, 2), dtype=np.int32)
+    for r, t in enumerate(tours):
+        nbr[t, r, 0], nbr[t, r, 1] = np.roll(t, 1), np.roll(t, -1)
+    nbr_t = torch.from_numpy(nbr).to(dev)
+    inc = torch.from_numpy(1.0 / g.uniform(1e3, 1e4, k)).to(dev)
+    outs = []
+    for pieces in (False, True):
+        tau = tau0.clone()
+        t = _device.SelectionTables(n, dev, dense=True, sorted_=True)
+        p = torch.zeros((n, n), dtype=torch.float64, device=dev)
+        rs = torch.zeros(n, dtype=torch.float64, device=dev)
+        st = _device.new_status(dev)
+        common = dict(tau_in=tau, tau_out=tau, eta_b=eta, nbr=nbr_t, inc=inc, k=k, do_evap=True, keep=0.9,
+                      alpha=1.0, inv_gamma=1.0 / 1.5, p_out=p, rowsum_out=rs, w_out=t.w, ldw=t.ldw,
+                      sw_out=t.sw, si_out=t.si, status=st)
+        if pieces:
+            _device.row_update_rows(cuts[1], cuts[2], n, want_p=True, **common)
+            torch.cuda.synchronize()
+            assert torch.equal(tau[:cuts[1]], tau0[:cuts[1]]) and torch.equal(tau[cuts[2]:], tau0[cuts[2]:])
+            assert not p[:cuts[1]].any() and not p[cuts[2]:].any()
+            for a, b in zip(cuts[2:-1], cuts[3:]):
+                _device.row_update_rows(a, b, n, want_p=True, **common)
+            _device.row_update_rows(cuts[0], cuts[1], n, want_p=True, **common)
+        else:
+            _device.row_update(n, want_p=True, **common)
+        torch.cuda.synchronize()
+        assert _device.read_status(st)[0] == 0
+        outs.append([x.cpu().numpy() for x in (tau, rs, p, t.w, t.sw, t.si)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
+    with pytest.raises(ValueError):
+        _device.row_update_rows(5, 4, n, want_p=True, **common)
+
+
 @pytest.mark.parametrize("selection", ["adair", "rw"])
 def test_solver_split_update_path_is_bit_identical(monkeypatch, selection):
     """Rows too long for the fused kernel's shared memory take the split
