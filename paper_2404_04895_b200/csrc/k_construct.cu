@@ -48,6 +48,7 @@ __device__ __forceinline__ uint32_t entry_key(float w, uint32_t j, float best, c
 //   uint16 cache_i[n * T]
 //   int2   leaves[n_leaves]
 //   per ant: double leaf_buf[kPwBlock], double leaf_sum[n_leaves], uint32 vis[nwords]
+//            (VIS8: nwords = ceil(n / 4), one byte per city)
 struct SortedArgs {
   int n, m_local, ant_offset, T, nwords, n_leaves, ld;  // ld: sorted-table row pitch
   const float *sw;
@@ -76,18 +77,32 @@ __device__ __forceinline__ uint32_t consume(float x) {
 }
 #endif
 
+// Visited set of the warp kernel: one byte per city when it fits in shared
+// memory (VIS8: the test is one LDS.U8, the update one STS.U8), else a bit map.
+template <bool VIS8>
+__device__ __forceinline__ bool visited_at(const uint32_t *vis, uint32_t j) {
+  if (VIS8) return reinterpret_cast<const uint8_t *>(vis)[j] != 0;
+  return (vis[j >> 5] >> (j & 31)) & 1u;
+}
+
+template <bool VIS8>
+__device__ __forceinline__ void mark_visited(uint32_t *vis, uint32_t j) {
+  if (VIS8)
+    reinterpret_cast<uint8_t *>(vis)[j] = 1;
+  else
+    vis[j >> 5] |= 1u << (j & 31);
+}
+
 // Score the 32-entry window (w, j) of the sorted row against the running
 // (best, bestj).  Warp-uniform control flow: the Philox chain runs once per
 // window for all lanes iff any lane holds a candidate (unvisited, W > 0,
 // W >= best); a window without candidates costs one shared load per lane.
-__device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t *vis, uint32_t step,
-                                             uint32_t gant, uint32_t it, const PhiloxKeys &ks, float &best,
-                                             uint32_t &bestj) {
-  const uint32_t vw = vis[j >> 5];
-  const bool cand = (w > 0.0f) && (w >= best) && !((vw >> (j & 31)) & 1u);
+template <bool VIS8, class Uniform>
+__device__ __forceinline__ void score_window_u(float w, uint32_t j, const uint32_t *vis, float &best,
+                                               uint32_t &bestj, Uniform uniform) {
+  const bool cand = (w > 0.0f) && (w >= best) && !visited_at<VIS8>(vis, j);
   if (__any_sync(kFull, cand)) {
-    const U4 r = philox4x32_10(U4{j >> 2, step, gant, it}, ks);
-    const uint32_t x = word_of_sel(r, j & 3);
+    const uint32_t x = uniform();
     const uint32_t key = cand ? __float_as_uint(__fmul_rn(w, bits_to_uniform(x))) + 1u : 0u;
     const uint32_t mkey = __reduce_max_sync(kFull, key);
     if (mkey != 0u) {
@@ -101,10 +116,18 @@ __device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t
   }
 }
 
+template <bool VIS8>
+__device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t *vis, uint32_t step,
+                                             uint32_t gant, uint32_t it, const PhiloxKeys &ks, float &best,
+                                             uint32_t &bestj) {
+  score_window_u<VIS8>(w, j, vis, best, bestj,
+                       [&] { return word_of_sel(philox4x32_10(U4{j >> 2, step, gant, it}, ks), j & 3); });
+}
+
 // The first global window of the next row is issued as soon as the step's
 // winner is known, ahead of the step's bookkeeping (visited bit, tour and
 // length buffers), so that L2 round trip overlaps it.
-template <bool HEAD, bool PROBE>
+template <bool HEAD, bool PROBE, bool VIS8>
 __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const __grid_constant__ SortedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
@@ -143,7 +166,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
   const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, un);
   __syncwarp();
-  if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
+  if (lane == 0) mark_visited<VIS8>(vis, start);
   __syncwarp();
 
   TourWriter tw{a.tours + (size_t)ant * n, n, lane, 0};
@@ -175,7 +198,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
         w = cache_w[cur * T + lane];
         j = cache_i[cur * T + lane];
       }
-      score_window(w, j, vis, step, gant, it, a.ks, best, bestj);
+      score_window<VIS8>(w, j, vis, step, gant, it, a.ks, best, bestj);
       const float wl = __shfl_sync(kFull, w, T - 1);
       done = (bucket_ceiling(wl) < best) || (wl <= 0.0f);
     }
@@ -191,8 +214,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
         const long long pa = clock64();
         const uint32_t sink = consume(wg) ^ jg;
         const long long pb = clock64();
-        const uint32_t vw = vis[jg >> 5];
-        const bool cand = (wg > 0.0f) && !((vw >> (jg & 31)) & 1u);
+        const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
         const U4 r = philox4x32_10(U4{jg >> 2, step, gant, it}, a.ks);
         const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(word_of(r, jg & 3)))) + 1u : 0u;
         const uint32_t k2 = consume(__uint_as_float(key));
@@ -208,7 +230,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
         }
       }
 #endif
-      score_window(wg, jg, vis, step, gant, it, a.ks, best, bestj);
+      score_window<VIS8>(wg, jg, vis, step, gant, it, a.ks, best, bestj);
       if (PROBE) ++windows;
       // entries after this window have W <= bucket_ceiling(window's last W)
       const float wl = __shfl_sync(kFull, wg, 31);
@@ -241,7 +263,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
         jg = __ldg(si + (bestj * (uint32_t)a.ld + e));
       }
     }
-    if (lane == 0) vis[bestj >> 5] |= 1u << (bestj & 31);
+    if (lane == 0) mark_visited<VIS8>(vis, bestj);
     if (step > 1) lc.push();  // edge step-2, loaded one step ago
     lc.load(cur, bestj);      // edge step-1
     __syncwarp();
@@ -509,7 +531,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
   const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, (uint32_t)n);
   __syncwarp();
-  if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
+  if (lane == 0) mark_visited<false>(vis, start);
   __syncwarp();
 
   TourWriter tw{a.tours + (size_t)ant * n, n, lane, 0};
@@ -645,10 +667,10 @@ __global__ void __launch_bounds__(WARPS * 32)
 using namespace taco;
 
 
-template <bool HEAD, bool PROBE>
+template <bool HEAD, bool PROBE, bool VIS8>
 static int launch_sorted(const SortedArgs &a, int grid, int threads, size_t smem, cudaStream_t s) {
-  if (set_smem((const void *)k_construct_sorted<HEAD, PROBE>, smem) != TACO_OK) return TACO_ERR_CUDA;
-  k_construct_sorted<HEAD, PROBE><<<grid, threads, smem, s>>>(a);
+  if (set_smem((const void *)k_construct_sorted<HEAD, PROBE, VIS8>, smem) != TACO_OK) return TACO_ERR_CUDA;
+  k_construct_sorted<HEAD, PROBE, VIS8><<<grid, threads, smem, s>>>(a);
   return TACO_OK;
 }
 
@@ -721,7 +743,13 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     warps = warps < 1 ? 1 : (warps > kSortedMaxWarps ? kSortedMaxWarps : warps);
     if (const char *ev = getenv("TACO_SORTED_WARPS")) warps = atoi(ev);
     if (warps < 1 || warps > kSortedMaxWarps) return TACO_ERR_ARG;
-    const size_t fixed = leaves_bytes + per_ant * warps;
+    // visited set: a byte per city when that fits next to the rest (VIS8),
+    // else the bit map; TACO_SORTED_VIS=bits forces the bit map (tuning knob)
+    const int nwords8 = (n + 3) / 4;
+    const size_t per_ant8 = ant_scratch_bytes(n_leaves, nwords8);
+    bool vis8 = leaves_bytes + per_ant8 * warps <= 200 * 1024;
+    if (const char *ev = getenv("TACO_SORTED_VIS")) vis8 = vis8 && ev[0] != 'b';
+    const size_t fixed = leaves_bytes + (vis8 ? per_ant8 : per_ant) * warps;
     // Shared-memory row-head cache: off by default.  Since the next row's first
     // global window is issued a step ahead, scoring it directly beats a
     // separate pass over a cached head at every ant count (n = 2392: m = 512
@@ -732,18 +760,22 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     if (T < 0 || T > 32 || T >= n) return TACO_ERR_ARG;
     const size_t smem = (((size_t)6 * n * T + 15) & ~(size_t)15) + fixed;
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
-    SortedArgs a{n, m_local, ant_offset, T, nwords, n_leaves, ldw, sw, si, dist, iteration, state,
+    SortedArgs a{n, m_local, ant_offset, T, vis8 ? nwords8 : nwords, n_leaves, ldw, sw, si, dist, iteration, state,
                  tours_out, costs_out, status, scan_count, ks};
     const int grid = (m_local + warps - 1) / warps;
     // (An L1 prefetch of the top candidates' next windows was measured slower
     // on B200, 2.68 vs 2.48 ms at m = 4096, and removed.)
-    const int code = (T > 0 ? 2 : 0) | (scan_count ? 1 : 0);
+    const int code = (vis8 ? 4 : 0) | (T > 0 ? 2 : 0) | (scan_count ? 1 : 0);
     int rc = TACO_ERR_ARG;
     switch (code) {
-      case 0: rc = launch_sorted<false, false>(a, grid, warps * 32, smem, s); break;
-      case 1: rc = launch_sorted<false, true>(a, grid, warps * 32, smem, s); break;
-      case 2: rc = launch_sorted<true, false>(a, grid, warps * 32, smem, s); break;
-      case 3: rc = launch_sorted<true, true>(a, grid, warps * 32, smem, s); break;
+      case 0: rc = launch_sorted<false, false, false>(a, grid, warps * 32, smem, s); break;
+      case 1: rc = launch_sorted<false, true, false>(a, grid, warps * 32, smem, s); break;
+      case 2: rc = launch_sorted<true, false, false>(a, grid, warps * 32, smem, s); break;
+      case 3: rc = launch_sorted<true, true, false>(a, grid, warps * 32, smem, s); break;
+      case 4: rc = launch_sorted<false, false, true>(a, grid, warps * 32, smem, s); break;
+      case 5: rc = launch_sorted<false, true, true>(a, grid, warps * 32, smem, s); break;
+      case 6: rc = launch_sorted<true, false, true>(a, grid, warps * 32, smem, s); break;
+      case 7: rc = launch_sorted<true, true, true>(a, grid, warps * 32, smem, s); break;
     }
     if (rc != TACO_OK) return rc;
   } else if (variant == TACO_CONSTRUCT_DENSE) {
