@@ -19,11 +19,9 @@
 //          the full scan while touching only the head of the row.  Because the
 //          uniforms are counter-addressed by city, visiting candidates in
 //          sorted order draws exactly the values the full scan would.  The
-//          first T entries of every row are cached in shared memory (one CTA
-//          per SM), so most steps never leave the SM: the median step stops
-//          after 3 entries.
-// Both variants accumulate the tour length on the fly in numpy's pairwise
-// order (bit-exact with batch_costs), so no separate m x n gather pass runs.
+//          median step stops after 3 entries.
+// The tour length, in numpy's pairwise order (bit-exact with batch_costs), is
+// either accumulated on the fly or computed by k_tour_cost afterwards.
 #include <cstdlib>
 
 #include "construct_common.cuh"
@@ -44,13 +42,11 @@ __device__ __forceinline__ uint32_t entry_key(float w, uint32_t j, float best, c
 }
 
 // Shared-memory layout of the sorted kernel (dynamic):
-//   float  cache_w[n * T]    first T entries of every sorted row
-//   uint16 cache_i[n * T]
 //   int2   leaves[n_leaves]
 //   per ant: double leaf_buf[kPwBlock], double leaf_sum[n_leaves], uint32 vis[nwords]
 //            (VIS8: nwords = ceil(n / 4), one byte per city)
 struct SortedArgs {
-  int n, m_local, ant_offset, T, nwords, n_leaves, ld;  // ld: sorted-table row pitch
+  int n, m_local, ant_offset, nwords, n_leaves, ld;  // ld: sorted-table row pitch
   const float *sw;
   const uint16_t *si;
   const double *dist;
@@ -63,10 +59,11 @@ struct SortedArgs {
   PhiloxKeys ks;
 };
 
-constexpr int kSortedMaxWarps = 28;
+constexpr int kSortedMaxWarps = 28;      // fused tour length: 72 registers per thread
+constexpr int kSortedMaxWarpsLean = 32;  // separate tour length: <= 32 registers, 2 CTAs per SM
 
 #ifdef TACO_STEP_PROFILE
-// per-step latency phases of ant 0 (head window, global windows, bookkeeping;
+// per-step latency phases of ant 0 (-, windows, bookkeeping;
 // [5..7]: first-window load wait, vis+Philox+key, the two reductions)
 __device__ unsigned long long g_step_prof[8];
 
@@ -124,35 +121,32 @@ __device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t
                        [&] { return word_of_sel(philox4x32_10(U4{j >> 2, step, gant, it}, ks), j & 3); });
 }
 
-// The first global window of the next row is issued as soon as the step's
-// winner is known, ahead of the step's bookkeeping (visited bit, tour and
-// length buffers), so that L2 round trip overlaps it.
-template <bool HEAD, bool PROBE, bool VIS8>
-__global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const __grid_constant__ SortedArgs a) {
+// The first window of the next row is issued as soon as the step's winner is
+// known, ahead of the step's bookkeeping (visited bit, tour and length
+// buffers), so that L2 round trip overlaps it.  COST: the tour length is
+// accumulated on the fly (else taco_construct runs k_tour_cost afterwards).
+template <bool PROBE, bool VIS8, bool COST>
+__global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsLean * 32, COST ? 1 : 2)
+    k_construct_sorted(const __grid_constant__ SortedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
-  const int T = HEAD ? a.T : 0;
-  float *cache_w = reinterpret_cast<float *>(smem);
-  uint16_t *cache_i = reinterpret_cast<uint16_t *>(smem + (size_t)4 * n * T);
-  size_t off = ((size_t)6 * n * T + 15) & ~(size_t)15;
-  int2 *leaves = reinterpret_cast<int2 *>(smem + off);
-  off += ((size_t)8 * a.n_leaves + 15) & ~(size_t)15;
   const int warps = blockDim.x >> 5;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  unsigned char *mine = smem + off + ant_scratch_bytes(a.n_leaves, a.nwords) * warp;
-  double *leaf_buf = reinterpret_cast<double *>(mine);
-  double *leaf_sum = leaf_buf + kPwBlock;
-  uint32_t *vis = reinterpret_cast<uint32_t *>(leaf_sum + a.n_leaves);
-
-  if (HEAD) {  // stage the head of every row (written by k_row_update this iteration)
-    for (int idx = threadIdx.x; idx < n * T; idx += blockDim.x) {
-      const int row = idx / (T > 0 ? T : 1), t = idx - row * T;
-      cache_w[idx] = __ldg(a.sw + (size_t)row * a.ld + t);
-      cache_i[idx] = __ldg(a.si + (size_t)row * a.ld + t);
-    }
+  int2 *leaves = reinterpret_cast<int2 *>(smem);
+  double *leaf_buf = nullptr, *leaf_sum = nullptr;
+  uint32_t *vis;
+  if (COST) {  // leaves, then per ant: leaf buffer, leaf sums, visited set
+    unsigned char *mine = smem + (((size_t)8 * a.n_leaves + 15) & ~(size_t)15) +
+                          ant_scratch_bytes(a.n_leaves, a.nwords) * warp;
+    leaf_buf = reinterpret_cast<double *>(mine);
+    leaf_sum = leaf_buf + kPwBlock;
+    vis = reinterpret_cast<uint32_t *>(leaf_sum + a.n_leaves);
+  } else {  // per ant: the visited set only
+    vis = reinterpret_cast<uint32_t *>(smem + (((size_t)4 * a.nwords + 15) & ~(size_t)15) * warp);
   }
-  if (threadIdx.x == 0) pw_leaves(n, leaves);
+
+  if (COST && threadIdx.x == 0) pw_leaves(n, leaves);
   __syncthreads();
 
   const int ant = blockIdx.x * warps + warp;
@@ -172,16 +166,16 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
   TourWriter tw{a.tours + (size_t)ant * n, n, lane, 0};
   tw.put(0, (int32_t)start);
   LeafCost lc;
-  lc.init(a.costs != nullptr ? a.dist : nullptr, leaves, leaf_buf, leaf_sum, n, lane);
+  lc.init(COST && a.costs != nullptr ? a.dist : nullptr, leaves, leaf_buf, leaf_sum, n, lane);
   uint32_t cur = start;
-  unsigned long long windows = 0;  // 32-entry global windows read (traffic probe)
-  // first global window (entries T..T+31) of the current row, in flight
-  // across the step boundary
+  unsigned long long windows = 0;  // 32-entry windows read (traffic probe)
+  // first window (entries 0..31) of the current row, in flight across the
+  // step boundary
   float wg = 0.0f;
   uint32_t jg = 0;
-  if ((uint32_t)T + lane < un) {
-    wg = __ldg(sw + (cur * (uint32_t)a.ld + (uint32_t)T + lane));
-    jg = __ldg(si + (cur * (uint32_t)a.ld + (uint32_t)T + lane));
+  if ((uint32_t)lane < un) {
+    wg = __ldg(sw + (cur * (uint32_t)a.ld + lane));
+    jg = __ldg(si + (cur * (uint32_t)a.ld + lane));
   }
   for (uint32_t step = 1; step < un; ++step) {
 #ifdef TACO_STEP_PROFILE
@@ -191,22 +185,11 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
     float best = -1.0f;
     uint32_t bestj = 0xffffffffu;
     bool done = false;
-    if (HEAD) {
-      float w = 0.0f;
-      uint32_t j = 0;
-      if (lane < T) {
-        w = cache_w[cur * T + lane];
-        j = cache_i[cur * T + lane];
-      }
-      score_window<VIS8>(w, j, vis, step, gant, it, a.ks, best, bestj);
-      const float wl = __shfl_sync(kFull, w, T - 1);
-      done = (bucket_ceiling(wl) < best) || (wl <= 0.0f);
-    }
 #ifdef TACO_STEP_PROFILE
     const long long t1 = clock64();
     int nwin = 0;
 #endif
-    uint32_t base = (uint32_t)T;
+    uint32_t base = 0;
     while (!done) {
 #ifdef TACO_STEP_PROFILE
       ++nwin;
@@ -255,7 +238,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
     }
     // next row's first window: issued before this step's bookkeeping
     {
-      const uint32_t e = (uint32_t)T + lane;
+      const uint32_t e = (uint32_t)lane;
       wg = 0.0f;
       jg = 0;
       if (step + 1 < un && e < un) {
@@ -264,8 +247,10 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
       }
     }
     if (lane == 0) mark_visited<VIS8>(vis, bestj);
-    if (step > 1) lc.push();  // edge step-2, loaded one step ago
-    lc.load(cur, bestj);      // edge step-1
+    if (COST) {
+      if (step > 1) lc.push();  // edge step-2, loaded one step ago
+      lc.load(cur, bestj);      // edge step-1
+    }
     __syncwarp();
     tw.put((int)step, (int32_t)bestj);
     cur = bestj;
@@ -281,7 +266,7 @@ __global__ void __launch_bounds__(kSortedMaxWarps * 32) k_construct_sorted(const
 #endif
   }
   tw.flush();
-  if (lc.active) {
+  if (COST && lc.active) {
     lc.push();  // edge n-2
     lc.load(cur, start);
     lc.push();  // closing edge n-1
@@ -667,10 +652,10 @@ __global__ void __launch_bounds__(WARPS * 32)
 using namespace taco;
 
 
-template <bool HEAD, bool PROBE, bool VIS8>
+template <bool PROBE, bool VIS8, bool COST>
 static int launch_sorted(const SortedArgs &a, int grid, int threads, size_t smem, cudaStream_t s) {
-  if (set_smem((const void *)k_construct_sorted<HEAD, PROBE, VIS8>, smem) != TACO_OK) return TACO_ERR_CUDA;
-  k_construct_sorted<HEAD, PROBE, VIS8><<<grid, threads, smem, s>>>(a);
+  if (set_smem((const void *)k_construct_sorted<PROBE, VIS8, COST>, smem) != TACO_OK) return TACO_ERR_CUDA;
+  k_construct_sorted<PROBE, VIS8, COST><<<grid, threads, smem, s>>>(a);
   return TACO_OK;
 }
 
@@ -737,46 +722,56 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
 #undef TACO_GROUP_CASE
       return TACO_ERR_ARG;
     }
-    // one CTA per SM when the colony allows it: the row-head cache is staged
-    // once per CTA.  Knobs (tuning only): TACO_SORTED_WARPS, TACO_SORTED_T.
-    int warps = (m_local + sm_count() - 1) / sm_count();
-    warps = warps < 1 ? 1 : (warps > kSortedMaxWarps ? kSortedMaxWarps : warps);
+    // tour length: a separate k_tour_cost pass after the construction (the
+    // kernel then needs <= 32 registers instead of 72), or fused (COST) when
+    // dist is too large to stay in L2 and the separate pass would pay for
+    // random DRAM sectors: n = 2392, m = 4096 2.05 vs 2.08 ms; n = 5000,
+    // m = 4096 4.36 vs 4.44; n = 10000, m = 8192 20.8 vs 19.9 (fused).
+    // TACO_SORTED_COST=fused|separate overrides (tuning knob).
+    bool fused_cost = costs_out != nullptr && n > 7000;
+    if (const char *ev = getenv("TACO_SORTED_COST")) fused_cost = costs_out != nullptr && ev[0] == 'f';
+    const int max_warps = fused_cost ? kSortedMaxWarps : kSortedMaxWarpsLean;
+    // warps per CTA: all ants of an SM in one CTA when they fit (one wave);
+    // larger colonies run 32-warp CTAs, two per SM.  TACO_SORTED_WARPS
+    // overrides (tuning knob).
+    const int ants_per_sm = (m_local + sm_count() - 1) / sm_count();
+    int warps = ants_per_sm < 1 ? 1 : (ants_per_sm > max_warps ? max_warps : ants_per_sm);
     if (const char *ev = getenv("TACO_SORTED_WARPS")) warps = atoi(ev);
-    if (warps < 1 || warps > kSortedMaxWarps) return TACO_ERR_ARG;
-    // visited set: a byte per city when that fits next to the rest (VIS8),
+    if (warps < 1 || warps > max_warps) return TACO_ERR_ARG;
+    auto scratch = [&](int nw) {
+      return fused_cost ? ant_scratch_bytes(n_leaves, nw) : (((size_t)4 * nw + 15) & ~(size_t)15);
+    };
+    const size_t lb = fused_cost ? leaves_bytes : 0;
+    // visited set: a byte per city when the SM's ants fit with it (VIS8),
     // else the bit map; TACO_SORTED_VIS=bits forces the bit map (tuning knob)
     const int nwords8 = (n + 3) / 4;
-    const size_t per_ant8 = ant_scratch_bytes(n_leaves, nwords8);
-    bool vis8 = leaves_bytes + per_ant8 * warps <= 200 * 1024;
+    const int resident = ants_per_sm < 2 * max_warps ? ants_per_sm : 2 * max_warps;
+    bool vis8 = lb + scratch(nwords8) * (resident > warps ? resident : warps) <= 200 * 1024;
     if (const char *ev = getenv("TACO_SORTED_VIS")) vis8 = vis8 && ev[0] != 'b';
-    const size_t fixed = leaves_bytes + (vis8 ? per_ant8 : per_ant) * warps;
-    // Shared-memory row-head cache: off by default.  Since the next row's first
-    // global window is issued a step ahead, scoring it directly beats a
-    // separate pass over a cached head at every ant count (n = 2392: m = 512
-    // 1.39 vs 1.62 ms with T = 12; m = 2048 1.68 vs 1.90; m = 4096 2.19 vs
-    // 2.45).  TACO_SORTED_T=<T> re-enables it (tuning knob).
-    int T = 0;
-    if (const char *ev = getenv("TACO_SORTED_T")) T = atoi(ev);
-    if (T < 0 || T > 32 || T >= n) return TACO_ERR_ARG;
-    const size_t smem = (((size_t)6 * n * T + 15) & ~(size_t)15) + fixed;
+    // (Measured and removed: a shared-memory cache of the first T entries of
+    // every row.  Once the next row's first window is issued a step ahead,
+    // the separate pass over the cached head only adds work: n = 2392, m = 512
+    // 1.39 vs 1.62 ms with T = 12; m = 4096 2.19 vs 2.45.  An L1 prefetch of
+    // the top candidates' next windows was slower too, 2.68 vs 2.48 ms.)
+    const size_t smem = lb + scratch(vis8 ? nwords8 : nwords) * warps;
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
-    SortedArgs a{n, m_local, ant_offset, T, vis8 ? nwords8 : nwords, n_leaves, ldw, sw, si, dist, iteration, state,
-                 tours_out, costs_out, status, scan_count, ks};
+    SortedArgs a{n, m_local, ant_offset, vis8 ? nwords8 : nwords, n_leaves, ldw, sw, si, dist, iteration, state,
+                 tours_out, fused_cost ? costs_out : nullptr, status, scan_count, ks};
     const int grid = (m_local + warps - 1) / warps;
-    // (An L1 prefetch of the top candidates' next windows was measured slower
-    // on B200, 2.68 vs 2.48 ms at m = 4096, and removed.)
-    const int code = (vis8 ? 4 : 0) | (T > 0 ? 2 : 0) | (scan_count ? 1 : 0);
+    const int code = (vis8 ? 4 : 0) | (fused_cost ? 2 : 0) | (scan_count ? 1 : 0);
     int rc = TACO_ERR_ARG;
     switch (code) {
       case 0: rc = launch_sorted<false, false, false>(a, grid, warps * 32, smem, s); break;
-      case 1: rc = launch_sorted<false, true, false>(a, grid, warps * 32, smem, s); break;
-      case 2: rc = launch_sorted<true, false, false>(a, grid, warps * 32, smem, s); break;
-      case 3: rc = launch_sorted<true, true, false>(a, grid, warps * 32, smem, s); break;
-      case 4: rc = launch_sorted<false, false, true>(a, grid, warps * 32, smem, s); break;
-      case 5: rc = launch_sorted<false, true, true>(a, grid, warps * 32, smem, s); break;
-      case 6: rc = launch_sorted<true, false, true>(a, grid, warps * 32, smem, s); break;
+      case 1: rc = launch_sorted<true, false, false>(a, grid, warps * 32, smem, s); break;
+      case 2: rc = launch_sorted<false, false, true>(a, grid, warps * 32, smem, s); break;
+      case 3: rc = launch_sorted<true, false, true>(a, grid, warps * 32, smem, s); break;
+      case 4: rc = launch_sorted<false, true, false>(a, grid, warps * 32, smem, s); break;
+      case 5: rc = launch_sorted<true, true, false>(a, grid, warps * 32, smem, s); break;
+      case 6: rc = launch_sorted<false, true, true>(a, grid, warps * 32, smem, s); break;
       case 7: rc = launch_sorted<true, true, true>(a, grid, warps * 32, smem, s); break;
     }
+    if (rc == TACO_OK && costs_out != nullptr && !fused_cost)
+      rc = taco_tour_cost(n, m_local, tours_out, 0, dist, costs_out, stream);
     if (rc != TACO_OK) return rc;
   } else if (variant == TACO_CONSTRUCT_DENSE) {
     if (w == nullptr || ldw < n || (ldw % 4) != 0) return TACO_ERR_ARG;

@@ -2,7 +2,7 @@
 
 Runs a Solver at the given size for a few iterations (so the pheromone and
 the sorted tables look like a real run), then times taco_construct with CUDA
-events.  Knobs are read by libtaco from the environment (TACO_SORTED_T,
+events.  Knobs are read by libtaco from the environment (TACO_SORTED_COST, TACO_SORTED_VIS,
 TACO_SORTED_WARPS), so variants are compared in separate processes:
 
     python scripts/bench_construct.py --n 2392 --m 4096 --iters 5
@@ -57,7 +57,7 @@ for r in range(args.reps + 1):
         times.append(a.elapsed_time(b))
 assert _device.read_status(st)[0] == 0
 print(json.dumps({"n": args.n, "m": args.m, "variant": args.variant,
-                  "T": os.environ.get("TACO_SORTED_T"), "warps": os.environ.get("TACO_SORTED_WARPS"),
+                  "cost": os.environ.get("TACO_SORTED_COST"), "vis": os.environ.get("TACO_SORTED_VIS"), "warps": os.environ.get("TACO_SORTED_WARPS"),
                   "ms": float(np.median(times)), ("exact_recount_steps" if rw else "windows_per_ant_step"):
                       int(scan.item()) if rw else int(scan.item()) / (args.m * (args.n - 1)),
                   "tour_checksum": int(tours.sum().item())}))

@@ -48,7 +48,7 @@ s.step_async()
 torch.cuda.synchronize()
 lib.taco_step_profile(buf, 0)
 steps = buf[3]
-print({"m": args.m, "steps": steps, "head_cycles": buf[0] / steps, "global_cycles": buf[1] / steps,
+print({"m": args.m, "steps": steps, "global_cycles": buf[1] / steps,
        "bookkeeping_cycles": buf[2] / steps, "global_windows_per_step": buf[4] / steps,
        "first_window_load_wait": buf[5] / steps, "vis_philox_key_cycles": buf[6] / steps,
        "two_redux_cycles": buf[7] / steps})
