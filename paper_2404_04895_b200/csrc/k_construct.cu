@@ -125,8 +125,11 @@ __device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t
 // known, ahead of the step's bookkeeping (visited bit, tour and length
 // buffers), so that L2 round trip overlaps it.  COST: the tour length is
 // accumulated on the fly (else taco_construct runs k_tour_cost afterwards).
-template <bool PROBE, bool VIS8, bool COST>
-__global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsLean * 32, COST ? 1 : 2)
+// MODE 0: fused tour length (COST); 1: separate length, one CTA per SM (up
+// to 64 registers); 2: separate length, two 32-warp CTAs per SM (<= 32
+// registers: the compiler rematerializes more, so only for > 32 ants/SM).
+template <bool PROBE, bool VIS8, int MODE, bool COST = (MODE == 0)>
+__global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsLean * 32, MODE == 2 ? 2 : 1)
     k_construct_sorted(const __grid_constant__ SortedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
@@ -652,10 +655,10 @@ __global__ void __launch_bounds__(WARPS * 32)
 using namespace taco;
 
 
-template <bool PROBE, bool VIS8, bool COST>
+template <bool PROBE, bool VIS8, int MODE>
 static int launch_sorted(const SortedArgs &a, int grid, int threads, size_t smem, cudaStream_t s) {
-  if (set_smem((const void *)k_construct_sorted<PROBE, VIS8, COST>, smem) != TACO_OK) return TACO_ERR_CUDA;
-  k_construct_sorted<PROBE, VIS8, COST><<<grid, threads, smem, s>>>(a);
+  if (set_smem((const void *)k_construct_sorted<PROBE, VIS8, MODE>, smem) != TACO_OK) return TACO_ERR_CUDA;
+  k_construct_sorted<PROBE, VIS8, MODE><<<grid, threads, smem, s>>>(a);
   return TACO_OK;
 }
 
@@ -758,17 +761,16 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     SortedArgs a{n, m_local, ant_offset, vis8 ? nwords8 : nwords, n_leaves, ldw, sw, si, dist, iteration, state,
                  tours_out, fused_cost ? costs_out : nullptr, status, scan_count, ks};
     const int grid = (m_local + warps - 1) / warps;
-    const int code = (vis8 ? 4 : 0) | (fused_cost ? 2 : 0) | (scan_count ? 1 : 0);
+    const int mode = fused_cost ? 0 : (ants_per_sm > max_warps ? 2 : 1);
+    const int code = mode * 4 + (vis8 ? 2 : 0) + (scan_count ? 1 : 0);
     int rc = TACO_ERR_ARG;
     switch (code) {
-      case 0: rc = launch_sorted<false, false, false>(a, grid, warps * 32, smem, s); break;
-      case 1: rc = launch_sorted<true, false, false>(a, grid, warps * 32, smem, s); break;
-      case 2: rc = launch_sorted<false, false, true>(a, grid, warps * 32, smem, s); break;
-      case 3: rc = launch_sorted<true, false, true>(a, grid, warps * 32, smem, s); break;
-      case 4: rc = launch_sorted<false, true, false>(a, grid, warps * 32, smem, s); break;
-      case 5: rc = launch_sorted<true, true, false>(a, grid, warps * 32, smem, s); break;
-      case 6: rc = launch_sorted<false, true, true>(a, grid, warps * 32, smem, s); break;
-      case 7: rc = launch_sorted<true, true, true>(a, grid, warps * 32, smem, s); break;
+#define TACO_SORTED_CASE(MODE, V, P) \
+  case MODE * 4 + (V) * 2 + (P): rc = launch_sorted<P, V, MODE>(a, grid, warps * 32, smem, s); break;
+      TACO_SORTED_CASE(0, 0, 0) TACO_SORTED_CASE(0, 0, 1) TACO_SORTED_CASE(0, 1, 0) TACO_SORTED_CASE(0, 1, 1)
+      TACO_SORTED_CASE(1, 0, 0) TACO_SORTED_CASE(1, 0, 1) TACO_SORTED_CASE(1, 1, 0) TACO_SORTED_CASE(1, 1, 1)
+      TACO_SORTED_CASE(2, 0, 0) TACO_SORTED_CASE(2, 0, 1) TACO_SORTED_CASE(2, 1, 0) TACO_SORTED_CASE(2, 1, 1)
+#undef TACO_SORTED_CASE
     }
     if (rc == TACO_OK && costs_out != nullptr && !fused_cost)
       rc = taco_tour_cost(n, m_local, tours_out, 0, dist, costs_out, stream);
