@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define TACO_ABI_VERSION 2
+#define TACO_ABI_VERSION 3
 
 /* status codes (return values and status[0]) */
 #define TACO_OK 0
@@ -160,7 +160,8 @@ int taco_eta_power(int64_t count, const double *eta, double beta, double *out,
                    void *stream);
 
 /*
- * Tour construction, fast path (device Philox4x32-10 stream).
+ * Tour construction, fast path (device Philox2x32-10 stream; key
+ * H(seed) + iteration, counter ((city >> 1) | step << 16, ant), word city & 1).
  * Replaces colony.construct_tours colony.py:87-154 (IR / AdaIR branch) with
  * the deviate block of rng.step_exponentials rng.py:42-49 replaced by the
  * on-chip keyed uniform u(seed, iteration, step, ant, city) and the log-domain
@@ -168,8 +169,9 @@ int taco_eta_power(int64_t count, const double *eta, double beta, double *out,
  * Ants [ant_offset, ant_offset + m_local) are built; tours_out is
  * m_local x n int32.  variant: TACO_CONSTRUCT_SORTED (needs sw/si) or
  * TACO_CONSTRUCT_DENSE (needs w, ldw).  When costs_out is given, the tour
- * lengths are accumulated during construction from dist (n x n f64) in numpy's
- * pairwise order (model.batch_costs model.py:292-295, bit-exact).
+ * lengths from dist (n x n f64) are computed in numpy's pairwise order
+ * (model.batch_costs model.py:292-295, bit-exact), during construction or by
+ * a k_tour_cost pass on the same stream.
  * scan_count (nullable, device u64) is incremented by the number of 32-entry
  * global table windows the SORTED variant read (traffic probe for the
  * roofline report).  state (nullable): iteration from state->iteration.
@@ -190,8 +192,8 @@ int taco_construct(int n, int m_local, int ant_offset, int variant,
  * the first j with cumsum(P[cur] * unvisited)_j / total > u, bit-exact with
  * the reference's sequential cumsum rule (a certified parallel scan, with an
  * exact sequential recount when the crossing is within rounding distance).
- * u is one 53-bit Philox4x32-10 uniform per (step, ant) (counter word 0 =
- * 0xffffffff) in place of rng.step_uniforms (rng.py:52-62).  Start cities and
+ * u is one 53-bit Philox2x32-10 uniform per (step, ant) (counter
+ * (0xffff | step << 16, ant)) in place of rng.step_uniforms (rng.py:52-62).  Start cities and
  * the fused tour length are as in taco_construct.  exact_count (nullable,
  * device u64) accumulates the steps that took the sequential recount;
  * force_exact != 0 makes every step take it (test hook).  state as in
@@ -229,9 +231,10 @@ int taco_uniforms(int count, const uint32_t *step, const uint32_t *ant,
                   const uint32_t *city, uint64_t seed, uint32_t iteration,
                   float *u_out, void *stream);
 
-/* Philox4x32-10 bijection on `count` (counter, key) pairs (KAT hook). */
-int taco_philox4x32_10(int count, const uint32_t *ctr4, const uint32_t *key2,
-                       uint32_t *out4, void *stream);
+/* Philox2x32-10 (Random123) on `count` (counter[2], key) pairs: the
+ * generator of the device stream (KAT hook). */
+int taco_philox2x32_10(int count, const uint32_t *ctr2, const uint32_t *key,
+                       uint32_t *out2, void *stream);
 
 /*
  * Reference-stream selection step (bit-exact parity mode).  One lockstep

@@ -14,30 +14,41 @@ from __future__ import annotations
 
 import numpy as np
 
-M0, M1 = 0xD2511F53, 0xCD9E8D57
-W0, W1 = 0x9E3779B9, 0xBB67AE85
+PHILOX_M = 0xD256D193  # Random123 PHILOX_M2x32_0
+PHILOX_W = 0x9E3779B9  # PHILOX_W32_0
 MASK32 = 0xFFFFFFFF
+MASK64 = 0xFFFFFFFFFFFFFFFF
+RW_LOW = 0xFFFF  # counter low half of the RW thresholds (k_roulette.cu)
 
 
-def philox4x32_10(ctr: np.ndarray, key: np.ndarray) -> np.ndarray:
-    """Random123 Philox4x32-10 on (N, 4) counters and (N, 2) or (2,) keys."""
-    c = [np.asarray(ctr[..., i], dtype=np.uint64) for i in range(4)]
-    key = np.asarray(key, dtype=np.uint64)
-    k0 = np.broadcast_to(key[..., 0], c[0].shape).copy()
-    k1 = np.broadcast_to(key[..., 1], c[0].shape).copy()
+def philox2x32_10(ctr: np.ndarray, key) -> np.ndarray:
+    """Random123 Philox2x32-10 on (N, 2) counters and (N,) or scalar keys
+    (taco_common.cuh philox2x32_10)."""
+    x0 = np.asarray(ctr[..., 0], dtype=np.uint64)
+    x1 = np.asarray(ctr[..., 1], dtype=np.uint64)
+    k = np.broadcast_to(np.asarray(key, dtype=np.uint64), x0.shape).copy()
     for _ in range(10):
-        p0 = c[0] * M0
-        p1 = c[2] * M1
-        hi0, lo0 = p0 >> 32, p0 & MASK32
-        hi1, lo1 = p1 >> 32, p1 & MASK32
-        c = [hi1 ^ c[1] ^ k0, lo1, hi0 ^ c[3] ^ k1, lo0]
-        k0 = (k0 + W0) & MASK32
-        k1 = (k1 + W1) & MASK32
-    return np.stack(c, axis=-1).astype(np.uint32)
+        prod = x0 * np.uint64(PHILOX_M)
+        hi, lo = prod >> np.uint64(32), prod & np.uint64(MASK32)
+        x0, x1 = hi ^ k ^ x1, lo
+        k = (k + np.uint64(PHILOX_W)) & np.uint64(MASK32)
+    return np.stack([x0, x1], axis=-1).astype(np.uint32)
 
 
-def seed_key(seed: int) -> np.ndarray:
-    return np.array([seed & MASK32, (seed >> 32) & MASK32], dtype=np.uint64)
+def seed_hash32(seed: int) -> int:
+    """H(seed): xor-fold of the MurmurHash3 64-bit finalizer (taco_common.cuh)."""
+    f = seed & MASK64
+    f ^= f >> 33
+    f = (f * 0xFF51AFD7ED558CCD) & MASK64
+    f ^= f >> 33
+    f = (f * 0xC4CEB9FE1A85EC53) & MASK64
+    f ^= f >> 33
+    return (f ^ (f >> 32)) & MASK32
+
+
+def stream_key(seed: int, iteration: int) -> int:
+    """Philox key of one iteration: H(seed) + iteration (mod 2^32)."""
+    return (seed_hash32(seed) + iteration) & MASK32
 
 
 def bits_to_uniform(x: np.ndarray) -> np.ndarray:
@@ -47,36 +58,33 @@ def bits_to_uniform(x: np.ndarray) -> np.ndarray:
 
 
 def uniforms(seed: int, iteration: int, step, ant, city) -> np.ndarray:
-    """u(seed, iteration, step, ant, city); arrays broadcast together."""
+    """u(seed, iteration, step, ant, city); arrays broadcast together.
+    Counter ((city >> 1) | step << 16, ant), word city & 1."""
     step, ant, city = np.broadcast_arrays(np.asarray(step, dtype=np.uint64),
                                           np.asarray(ant, dtype=np.uint64),
                                           np.asarray(city, dtype=np.uint64))
-    ctr = np.stack([city >> 2, step, ant, np.full_like(city, iteration & MASK32)], axis=-1)
-    words = philox4x32_10(ctr, seed_key(seed))
-    pick = np.take_along_axis(words, (city & 3).astype(np.int64)[..., None], axis=-1)[..., 0]
+    ctr = np.stack([((city >> np.uint64(1)) | (step << np.uint64(16))) & np.uint64(MASK32), ant], axis=-1)
+    words = philox2x32_10(ctr, stream_key(seed, iteration))
+    pick = np.where((city & np.uint64(1)) == 1, words[..., 1], words[..., 0])
     return bits_to_uniform(pick)
 
 
 def starts(seed: int, iteration: int, ants, n: int) -> np.ndarray:
-    """Device start cities: Lemire bound of word 0 of counter (0, 0, ant, it)."""
+    """Device start cities: Lemire bound of word 0 of counter (0, ant)."""
     ants = np.asarray(ants, dtype=np.uint64)
-    z = np.zeros_like(ants)
-    ctr = np.stack([z, z, ants, np.full_like(ants, iteration & MASK32)], axis=-1)
-    x = philox4x32_10(ctr, seed_key(seed))[..., 0].astype(np.uint64)
+    ctr = np.stack([np.zeros_like(ants), ants], axis=-1)
+    x = philox2x32_10(ctr, stream_key(seed, iteration))[..., 0].astype(np.uint64)
     return ((x * np.uint64(n)) >> np.uint64(32)).astype(np.int64)
 
 
-RW_COUNTER = 0xFFFFFFFF  # counter word 0 of the RW thresholds (k_roulette.cu)
-
-
 def rw_uniform(seed: int, iteration: int, step, ant) -> np.ndarray:
-    """Device RW threshold: 53 bits of Philox4x32-10 counter
-    (0xffffffff, step, ant, it), words 0 and 1, as numpy's random():
+    """Device RW threshold: 53 bits of Philox2x32-10 counter
+    (0xffff | step << 16, ant), as numpy's random():
     ((x >> 5) * 2^26 + (y >> 6)) / 2^53."""
     step = np.asarray(step, dtype=np.uint64).ravel()
     ant = np.asarray(ant, dtype=np.uint64).ravel()
-    ctr = np.stack([np.full_like(step, RW_COUNTER), step, ant, np.full_like(step, iteration & MASK32)], axis=-1)
-    r = philox4x32_10(ctr, seed_key(seed)).astype(np.uint64)
+    ctr = np.stack([(np.uint64(RW_LOW) | (step << np.uint64(16))) & np.uint64(MASK32), ant], axis=-1)
+    r = philox2x32_10(ctr, stream_key(seed, iteration)).astype(np.uint64)
     k = ((r[:, 0] >> np.uint64(5)) << np.uint64(26)) | (r[:, 1] >> np.uint64(6))
     return k.astype(np.float64) * 2.0**-53
 

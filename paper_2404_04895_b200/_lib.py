@@ -54,7 +54,7 @@ SIGNATURES = {
         _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _p, _p]),
     "taco_starts": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u32, _p, _p]),
     "taco_uniforms": (_c_int, [_c_int, _p, _p, _p, _c_u64, _c_u32, _p, _p]),
-    "taco_philox4x32_10": (_c_int, [_c_int, _p, _p, _p, _p]),
+    "taco_philox2x32_10": (_c_int, [_c_int, _p, _p, _p, _p]),
     "taco_select_parity": (_c_int, [_c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p]),
     "taco_replay_workspace_bytes": (_c_size, [_c_int, _c_int]),
     "taco_select_replay": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u64, _p, _p, _p, _p, _p, _c_size, _p, _p,
@@ -75,7 +75,7 @@ SIGNATURES = {
     "taco_shard_elites": (_c_int, [_c_int, _c_int, _p, _c_int, _c_int, _p, _p, _p, _p, _p]),
 }
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 
 class TacoLibraryMissing(ImportError):

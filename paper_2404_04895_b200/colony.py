@@ -87,7 +87,7 @@ def construct_tours(p, inst, params, iteration: int, chunk_size: int | None = No
                     probe=None, *, stream: str = "device", variant: str = "sorted") -> TourBatch:
     """Build m complete tours in n-1 lockstep selection rounds (colony.py:87-154).
 
-    stream="device" (default): keyed on-chip Philox4x32-10 uniforms and the
+    stream="device" (default): keyed on-chip Philox2x32-10 uniforms and the
     product-form rule argmax(W * u) — the fast path.
     stream="replay": the reference's own stream, regenerated on the device —
     the per-step Philox4x64 keys of SeedSequence(seed, spawn_key=(0, it, step))

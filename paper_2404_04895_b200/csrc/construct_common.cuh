@@ -91,10 +91,6 @@ __device__ __forceinline__ bool is_visited(const uint32_t *vis, uint32_t j) {
 
 }  // namespace taco
 
-static inline void split_seed(uint64_t seed, uint32_t *k0, uint32_t *k1) {
-  *k0 = (uint32_t)(seed & 0xffffffffu);
-  *k1 = (uint32_t)(seed >> 32);
-}
 
 static inline int sm_count() {
   static int cached = 0;

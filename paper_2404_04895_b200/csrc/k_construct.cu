@@ -6,7 +6,7 @@
 //
 // Fast-path rule: next = argmax_j { W[cur, j] * u(step, ant, j) }
 // over unvisited j with W[cur, j] > 0, first (lowest j) of ties, where
-// W = fp32(P^(1/gamma)) and u is the keyed Philox4x32-10 uniform.  This is the
+// W = fp32(P^(1/gamma)) and u is the keyed Philox2x32-10 uniform.  This is the
 // product form of the reference's argmax(log P / gamma - E) with E = -log u.
 //
 // Two variants compute the identical argmax:
@@ -27,19 +27,6 @@
 #include "construct_common.cuh"
 
 namespace taco {
-
-__device__ __forceinline__ uint32_t score_key(float w, uint32_t j, int step, uint32_t gant, uint32_t iteration,
-                                              const PhiloxKeys &ks) {
-  const U4 r = philox4x32_10(U4{j >> 2, (uint32_t)step, gant, iteration}, ks);
-  return __float_as_uint(__fmul_rn(w, bits_to_uniform(word_of(r, j & 3)))) + 1u;
-}
-
-// candidate key of table entry (w, j): (bits(w * u) + 1) or 0 when excluded
-__device__ __forceinline__ uint32_t entry_key(float w, uint32_t j, float best, const uint32_t *vis, int step,
-                                              uint32_t gant, uint32_t iteration, const PhiloxKeys &ks) {
-  if (!(w > 0.0f && w >= best) || is_visited(vis, j)) return 0u;
-  return score_key(w, j, step, gant, iteration, ks);
-}
 
 // Shared-memory layout of the sorted kernel (dynamic):
 //   int2   leaves[n_leaves]
@@ -115,10 +102,8 @@ __device__ __forceinline__ void score_window_u(float w, uint32_t j, const uint32
 
 template <bool VIS8>
 __device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t *vis, uint32_t step,
-                                             uint32_t gant, uint32_t it, const PhiloxKeys &ks, float &best,
-                                             uint32_t &bestj) {
-  score_window_u<VIS8>(w, j, vis, best, bestj,
-                       [&] { return word_of_sel(philox4x32_10(U4{j >> 2, step, gant, it}, ks), j & 3); });
+                                             uint32_t gant, const RoundKeys &rk, float &best, uint32_t &bestj) {
+  score_window_u<VIS8>(w, j, vis, best, bestj, [&] { return sel_word(j, step, gant, rk); });
 }
 
 // The first window of the next row is issued as soon as the step's winner is
@@ -157,11 +142,12 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
   if (__shfl_sync(kFull, lane == 0 ? (int)chain_stopped_construct(a.status) : 0, 0)) return;  // fail-stop
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
+  const RoundKeys rk = round_keys(a.ks, it);
   const uint32_t un = (uint32_t)n;  // n <= 65535, so every row offset fits in 32 bits
   const float *__restrict__ sw = a.sw;
   const uint16_t *__restrict__ si = a.si;
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
-  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, un);
+  const uint32_t start = start_city(un, gant, rk);
   __syncwarp();
   if (lane == 0) mark_visited<VIS8>(vis, start);
   __syncwarp();
@@ -201,8 +187,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
         const uint32_t sink = consume(wg) ^ jg;
         const long long pb = clock64();
         const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
-        const U4 r = philox4x32_10(U4{jg >> 2, step, gant, it}, a.ks);
-        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(word_of(r, jg & 3)))) + 1u : 0u;
+        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(sel_word(jg, step, gant, rk)))) + 1u : 0u;
         const uint32_t k2 = consume(__uint_as_float(key));
         const long long pc = clock64();
         const uint32_t mkey = __reduce_max_sync(kFull, k2);
@@ -216,7 +201,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
         }
       }
 #endif
-      score_window<VIS8>(wg, jg, vis, step, gant, it, a.ks, best, bestj);
+      score_window<VIS8>(wg, jg, vis, step, gant, rk, best, bestj);
       if (PROBE) ++windows;
       // entries after this window have W <= bucket_ceiling(window's last W)
       const float wl = __shfl_sync(kFull, wg, 31);
@@ -368,8 +353,9 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
   bool alive = ant < a.m_local;
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
+  const RoundKeys rk = round_keys(a.ks, it);
   const uint32_t un = (uint32_t)n, ld = (uint32_t)a.ld;
-  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, un);
+  const uint32_t start = start_city(un, gant, rk);
   int32_t *trow = a.tours + (size_t)ant * n;
   GroupCost gc;
   gc.acc = cost_mem + (size_t)g * (8 + kCostStack);
@@ -422,10 +408,8 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
     if (__any_sync(kFull, any)) {
 #pragma unroll
       for (int e = 0; e < E; ++e) {
-        const U4 r = philox4x32_10(U4{j[e] >> 2, step, gant, it}, a.ks);
-        // word_of (branchy) here: measured 2.5% faster than word_of_sel in this kernel
         const uint32_t key =
-            cand[e] ? __float_as_uint(__fmul_rn(w[e], bits_to_uniform(word_of(r, j[e] & 3)))) + 1u : 0u;
+            cand[e] ? __float_as_uint(__fmul_rn(w[e], bits_to_uniform(sel_word(j[e], step, gant, rk)))) + 1u : 0u;
         const unsigned long long pe = ((unsigned long long)key << 32) | (uint32_t)~j[e];
         p = pe > p ? pe : p;
       }
@@ -516,8 +500,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   if (__shfl_sync(kFull, lane == 0 ? (int)chain_stopped_construct(a.status) : 0, 0)) return;  // fail-stop
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
+  const RoundKeys rk = round_keys(a.ks, it);
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
-  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, (uint32_t)n);
+  const uint32_t start = start_city((uint32_t)n, gant, rk);
   __syncwarp();
   if (lane == 0) mark_visited<false>(vis, start);
   __syncwarp();
@@ -530,9 +515,6 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   const int nq = (n + 3) >> 2;
   for (int step = 1; step < n; ++step) {
     const float4 *row = reinterpret_cast<const float4 *>(a.w + (size_t)cur * a.ldw);
-    // x-independent half of Philox rounds 1-2, once per step (dense kernel
-    // only: measured 2.3% faster here, 2.5% slower in the sorted kernels)
-    const PhiloxStep ps = philox_step((uint32_t)step, gant, a.ks);
     uint32_t lkey = 0u, lj = 0xffffffffu;
 #pragma unroll 4
     for (int q = lane; q < nq; q += 32) {
@@ -543,9 +525,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
       const float wmax = fmaxf(fmaxf(wv.x, wv.y), fmaxf(wv.z, wv.w));
       const bool any = (nib != 0xfu) && wmax > 0.0f && (lkey == 0u || wmax >= __uint_as_float(lkey - 1u));
       if (any) {
-        const U4 r = philox4x32_10_x((uint32_t)q, it, ps, a.ks);
+        // cities 4q..4q+3: the blocks of j >> 1 = 2q and 2q + 1
+        const uint2 r0 = philox2x32_10(sel_counter(4u * q, (uint32_t)step), gant, rk);
+        const uint2 r1 = philox2x32_10(sel_counter(4u * q + 2u, (uint32_t)step), gant, rk);
         const float wc[4] = {wv.x, wv.y, wv.z, wv.w};
-        const uint32_t rc[4] = {r.x, r.y, r.z, r.w};
+        const uint32_t rc[4] = {r0.x, r0.y, r1.x, r1.y};
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           const uint32_t j = 4u * q + c;
@@ -582,30 +566,24 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   }
 }
 
-__global__ void k_starts(int n, int m_local, int ant_offset, uint32_t k0, uint32_t k1,
-                         uint32_t iteration, int32_t *out) {
+__global__ void k_starts(int n, int m_local, int ant_offset, PhiloxKeys ks, uint32_t iteration, int32_t *out) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a < m_local) out[a] = (int32_t)start_city((uint32_t)n, (uint32_t)(ant_offset + a), iteration, k0, k1);
+  if (a < m_local) out[a] = (int32_t)start_city((uint32_t)n, (uint32_t)(ant_offset + a), round_keys(ks, iteration));
 }
 
 __global__ void k_uniforms(int count, const uint32_t *step, const uint32_t *ant, const uint32_t *city,
-                           uint32_t k0, uint32_t k1, uint32_t iteration, float *out) {
+                           PhiloxKeys ks, uint32_t iteration, float *out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
-  const uint32_t j = city[t];
-  const U4 r = philox4x32_10(U4{j >> 2, step[t], ant[t], iteration}, k0, k1);
-  out[t] = bits_to_uniform(word_of(r, j & 3));
+  out[t] = bits_to_uniform(sel_word(city[t], step[t], ant[t], round_keys(ks, iteration)));
 }
 
 __global__ void k_philox(int count, const uint32_t *ctr, const uint32_t *key, uint32_t *out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
-  const U4 r = philox4x32_10(U4{ctr[4 * t], ctr[4 * t + 1], ctr[4 * t + 2], ctr[4 * t + 3]}, key[2 * t],
-                             key[2 * t + 1]);
-  out[4 * t] = r.x;
-  out[4 * t + 1] = r.y;
-  out[4 * t + 2] = r.z;
-  out[4 * t + 3] = r.w;
+  const uint2 r = philox2x32_10(ctr[2 * t], ctr[2 * t + 1], key[t]);
+  out[2 * t] = r.x;
+  out[2 * t + 1] = r.y;
 }
 
 // One lockstep round of the reference's log-domain selection (parity mode).
@@ -808,10 +786,8 @@ extern "C" int taco_starts(int n, int m_local, int ant_offset, uint64_t seed, ui
                            int32_t *starts_out, void *stream) {
   if (n < 1 || m_local < 0 || starts_out == nullptr) return TACO_ERR_ARG;
   if (m_local == 0) return TACO_OK;
-  uint32_t k0, k1;
-  split_seed(seed, &k0, &k1);
   k_starts<<<(m_local + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      n, m_local, ant_offset, k0, k1, iteration, starts_out);
+      n, m_local, ant_offset, philox_keys(seed), iteration, starts_out);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }
@@ -820,19 +796,17 @@ extern "C" int taco_uniforms(int count, const uint32_t *step, const uint32_t *an
                              uint64_t seed, uint32_t iteration, float *u_out, void *stream) {
   if (count < 0) return TACO_ERR_ARG;
   if (count == 0) return TACO_OK;
-  uint32_t k0, k1;
-  split_seed(seed, &k0, &k1);
-  k_uniforms<<<(count + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(count, step, ant, city, k0,
-                                                                                     k1, iteration, u_out);
+  k_uniforms<<<(count + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      count, step, ant, city, philox_keys(seed), iteration, u_out);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }
 
-extern "C" int taco_philox4x32_10(int count, const uint32_t *ctr4, const uint32_t *key2, uint32_t *out4,
+extern "C" int taco_philox2x32_10(int count, const uint32_t *ctr2, const uint32_t *key, uint32_t *out2,
                                   void *stream) {
   if (count < 0) return TACO_ERR_ARG;
   if (count == 0) return TACO_OK;
-  k_philox<<<(count + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(count, ctr4, key2, out4);
+  k_philox<<<(count + 255) / 256, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(count, ctr2, key, out2);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }

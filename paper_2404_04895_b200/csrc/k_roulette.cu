@@ -25,9 +25,10 @@
 // l+96 of each tile, all four in flight before any is used), parks per-lane tile
 // partials in shared memory and folds them per tile afterwards, so no
 // cross-lane dependency stalls the loads.  Pass B re-reads only the crossing
-// tile with lane l owning the 8 contiguous columns [t*256 + 8l, +8).  Device stream: one 53-bit uniform per
-// (step, ant) from Philox4x32-10 counter (0xffffffff, step, ant, iteration) —
-// a counter word the IR/AdaIR stream never uses (its word 0 is j/4 < 16384).
+// tile with lane l owning the 8 contiguous columns [t*256 + 8l, +8).  Device
+// stream: one 53-bit uniform per (step, ant) from the Philox2x32-10 counter
+// (0xffff | step << 16, ant) — a low half the IR/AdaIR stream never uses (its
+// low half is j >> 1 <= 0x7fff); see taco_common.cuh.
 #include "construct_common.cuh"
 
 namespace taco {
@@ -38,13 +39,6 @@ constexpr int kRwChunk = 32;  // tiles per pass-A chunk
 // per-warp lane partials of one chunk (rows padded to 33 against bank conflicts)
 __host__ __device__ __forceinline__ size_t rw_part_bytes(int ntiles) {
   return (size_t)8 * 33 * (ntiles < kRwChunk ? ntiles : kRwChunk);
-}
-constexpr uint32_t kRwCounter = 0xffffffffu;
-
-__device__ __forceinline__ double rw_uniform(uint32_t step, uint32_t gant, uint32_t it, const PhiloxKeys &ks) {
-  const U4 r = philox4x32_10(U4{kRwCounter, step, gant, it}, ks);
-  const uint64_t k = ((uint64_t)(r.x >> 5) << 26) | (uint64_t)(r.y >> 6);  // 53 bits, as numpy's random()
-  return (double)k * 0x1p-53;
 }
 
 // Symmetric butterfly sum: every lane ends with the same bits (a + b == b + a).
@@ -319,8 +313,9 @@ __global__ void __launch_bounds__(WARPS * 32, 7) k_construct_rw(const __grid_con
   if (__shfl_sync(kFull, lane == 0 ? (int)chain_stopped_construct(a.status) : 0, 0)) return;  // fail-stop
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
+  const RoundKeys rk = round_keys(a.ks, it);
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
-  const uint32_t start = lemire_bound(philox4x32_10(U4{0u, 0u, gant, it}, a.ks).x, (uint32_t)n);
+  const uint32_t start = start_city((uint32_t)n, gant, rk);
   __syncwarp();
   if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
   __syncwarp();
@@ -332,7 +327,7 @@ __global__ void __launch_bounds__(WARPS * 32, 7) k_construct_rw(const __grid_con
   uint32_t cur = start;
   unsigned exact_steps = 0;
   for (int step = 1; step < n; ++step) {
-    const double u = rw_uniform((uint32_t)step, gant, it, a.ks);
+    const double u = rw_threshold((uint32_t)step, gant, rk);
     const BitmaskRow row{a.p + (size_t)cur * n, vis, n};
     bool exact = false;
     const int j = rw_pick<VEC>(row, n, a.ntiles, u, tile_tot, part, lane, a.force_exact != 0, &exact);
@@ -395,7 +390,7 @@ __global__ void __launch_bounds__(WARPS * 32)
 __global__ void k_rw_uniforms(int count, const uint32_t *step, const uint32_t *ant, PhiloxKeys ks,
                               uint32_t iteration, double *out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < count) out[t] = rw_uniform(step[t], ant[t], iteration, ks);
+  if (t < count) out[t] = rw_threshold(step[t], ant[t], round_keys(ks, iteration));
 }
 
 }  // namespace taco

@@ -1,4 +1,4 @@
-// Shared device helpers for libtaco: Philox4x32-10, the keyed uniform stream,
+// Shared device helpers for libtaco: Philox2x32-10, the keyed uniform stream,
 // numpy-order pairwise summation, status recording.
 #pragma once
 
@@ -10,104 +10,88 @@
 namespace taco {
 
 // ---------------------------------------------------------------------------
-// Philox4x32-10 (Salmon et al., Random123).  Known-answer vectors are pinned
-// in tests/test_oracle_golden.py and tests/test_gpu_parity.py.
+// The device construction stream: Philox2x32-10 (Salmon et
+// al., Random123; known-answer vectors pinned in tests/test_oracle_golden.py
+// and tests/test_gpu_parity.py).
+//   key(seed, it) = H(seed) + it (mod 2^32), H = xor-fold of the MurmurHash3
+//                   64-bit finalizer of the seed: distinct iterations of a run
+//                   never share a key
+//   selection u(step >= 1, ant, city j):
+//                   counter ((j >> 1) | step << 16, ant), word j & 1
+//                   (n <= 65535: j >> 1 <= 0x7fff, step <= 0xfffe)
+//   start city:     counter (0, ant) (step 0 never selects), word 0, Lemire
+//   RW threshold:   counter (0xffff | step << 16, ant), 53 bits of both words
+//   u = ((x >> 9) + 0.5) * 2^-23 in (0, 1), exact in fp32
+// One block is a chain of 10 (IMAD.WIDE, LOP3) pairs: half the instructions
+// of a Philox4x32-10 block, of which the sorted scan used one word per lane.
 // ---------------------------------------------------------------------------
-constexpr uint32_t kPhiloxM0 = 0xD2511F53u;
-constexpr uint32_t kPhiloxM1 = 0xCD9E8D57u;
-constexpr uint32_t kPhiloxW0 = 0x9E3779B9u;
-constexpr uint32_t kPhiloxW1 = 0xBB67AE85u;
+constexpr uint32_t kPhiloxM = 0xD256D193u;  // Philox2x32 multiplier
+constexpr uint32_t kPhiloxW = 0x9E3779B9u;  // key bump (Weyl)
+constexpr uint32_t kRwLow = 0xffffu;        // counter low half of the RW thresholds
 
-struct U4 {
-  uint32_t x, y, z, w;
-};
-
-__device__ __forceinline__ U4 philox4x32_10(U4 c, uint32_t k0, uint32_t k1) {
-#pragma unroll
-  for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = kPhiloxM0 * c.x;
-    const uint32_t hi0 = __umulhi(kPhiloxM0, c.x);
-    const uint32_t lo1 = kPhiloxM1 * c.z;
-    const uint32_t hi1 = __umulhi(kPhiloxM1, c.z);
-    c = U4{hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0};
-    k0 += kPhiloxW0;
-    k1 += kPhiloxW1;
-  }
-  return c;
-}
-
-// Precomputed key schedule (k + r*W for r = 0..9).  Passed by value inside
-// kernel parameter structs, so after unrolling every round key is a
-// constant-bank operand of the LOP3: no registers, no per-call key adds.
+// per-seed key schedule H(seed) + r*W, r = 0..9 (kernel parameter)
 struct PhiloxKeys {
-  uint32_t k0[10], k1[10];
+  uint32_t k[10];
 };
+
+// round keys of one iteration: k[r] + it (registers, formed once per kernel)
+struct RoundKeys {
+  uint32_t k[10];
+};
+
+inline uint32_t seed_hash32(uint64_t seed) {
+  uint64_t f = seed;
+  f ^= f >> 33;
+  f *= 0xff51afd7ed558ccdull;
+  f ^= f >> 33;
+  f *= 0xc4ceb9fe1a85ec53ull;
+  f ^= f >> 33;
+  return (uint32_t)(f ^ (f >> 32));
+}
 
 inline PhiloxKeys philox_keys(uint64_t seed) {
   PhiloxKeys s;
-  uint32_t a = (uint32_t)(seed & 0xffffffffu), b = (uint32_t)(seed >> 32);
+  uint32_t a = seed_hash32(seed);
   for (int r = 0; r < 10; ++r) {
-    s.k0[r] = a;
-    s.k1[r] = b;
-    a += kPhiloxW0;
-    b += kPhiloxW1;
+    s.k[r] = a;
+    a += kPhiloxW;
   }
   return s;
 }
 
-__device__ __forceinline__ U4 philox4x32_10(U4 c, const PhiloxKeys &ks) {
+__host__ __device__ __forceinline__ RoundKeys round_keys(const PhiloxKeys &ks, uint32_t it) {
+  RoundKeys rk;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) rk.k[r] = ks.k[r] + it;
+  return rk;
+}
+
+__device__ __forceinline__ uint2 philox2x32_10(uint32_t x0, uint32_t x1, const RoundKeys &rk) {
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
-    const uint32_t lo0 = kPhiloxM0 * c.x;
-    const uint32_t hi0 = __umulhi(kPhiloxM0, c.x);
-    const uint32_t lo1 = kPhiloxM1 * c.z;
-    const uint32_t hi1 = __umulhi(kPhiloxM1, c.z);
-    c = U4{hi1 ^ c.y ^ ks.k0[r], lo1, hi0 ^ c.w ^ ks.k1[r], lo0};
+    const uint32_t hi = __umulhi(kPhiloxM, x0);
+    const uint32_t lo = kPhiloxM * x0;
+    x0 = hi ^ rk.k[r] ^ x1;
+    x1 = lo;
   }
-  return c;
+  return make_uint2(x0, x1);
 }
 
-// Philox4x32-10 on counter (x, step, ant, it) with the x-independent work of
-// rounds 1-2 hoisted: per (step, ant), round 1's ant product and round 2's
-// first product do not depend on x (= city >> 2), so a window of candidates
-// only runs the x-dependent half of those rounds.  Same output bits.
-struct PhiloxStep {
-  uint32_t c1x, c1y;    // round-1 words 0, 1
-  uint32_t hi0_k1, lo0;  // round-2 product of c1x: hi ^ key, lo
-};
-
-__device__ __forceinline__ PhiloxStep philox_step(uint32_t step, uint32_t ant, const PhiloxKeys &ks) {
-  PhiloxStep p;
-  p.c1x = __umulhi(kPhiloxM1, ant) ^ step ^ ks.k0[0];
-  p.c1y = kPhiloxM1 * ant;
-  p.hi0_k1 = __umulhi(kPhiloxM0, p.c1x) ^ ks.k1[1];
-  p.lo0 = kPhiloxM0 * p.c1x;
-  return p;
-}
-
-__device__ __forceinline__ U4 philox4x32_10_x(uint32_t x, uint32_t it, const PhiloxStep &p,
-                                              const PhiloxKeys &ks) {
-  // round 1: only the x product
-  const uint32_t c1z = __umulhi(kPhiloxM0, x) ^ it ^ ks.k1[0];
-  const uint32_t c1w = kPhiloxM0 * x;
-  // round 2: only the c1z product
-  U4 c{__umulhi(kPhiloxM1, c1z) ^ p.c1y ^ ks.k0[1], kPhiloxM1 * c1z, p.hi0_k1 ^ c1w, p.lo0};
+// plain-key form (known-answer hook)
+__device__ __forceinline__ uint2 philox2x32_10(uint32_t x0, uint32_t x1, uint32_t key) {
 #pragma unroll
-  for (int r = 2; r < 10; ++r) {
-    const uint32_t lo0 = kPhiloxM0 * c.x;
-    const uint32_t hi0 = __umulhi(kPhiloxM0, c.x);
-    const uint32_t lo1 = kPhiloxM1 * c.z;
-    const uint32_t hi1 = __umulhi(kPhiloxM1, c.z);
-    c = U4{hi1 ^ c.y ^ ks.k0[r], lo1, hi0 ^ c.w ^ ks.k1[r], lo0};
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi = __umulhi(kPhiloxM, x0);
+    const uint32_t lo = kPhiloxM * x0;
+    x0 = hi ^ key ^ x1;
+    x1 = lo;
+    key += kPhiloxW;
   }
-  return c;
+  return make_uint2(x0, x1);
 }
 
-// The device construction stream:
-//   key     = (seed & 0xffffffff, seed >> 32)
-//   counter = (city >> 2, step, ant, iteration)      selection, step >= 1
-//   counter = (0, 0, ant, iteration), word 0         start city (step 0)
-//   u       = ((x >> 9) + 0.5) * 2^-23  in (0, 1), exact in fp32
+__device__ __forceinline__ uint32_t sel_counter(uint32_t j, uint32_t step) { return (j >> 1) | (step << 16); }
+
 __device__ __forceinline__ float bits_to_uniform(uint32_t x) {
   // 1 + k 2^-23 (k = x >> 9) built from bits, minus (1 - 2^-24): both steps
   // exact (Sterbenz), so u = (k + 1/2) 2^-23 without an int->float conversion
@@ -119,10 +103,6 @@ __device__ __forceinline__ uint32_t lemire_bound(uint32_t x, uint32_t n) {
   return (uint32_t)(((uint64_t)x * (uint64_t)n) >> 32);
 }
 
-__device__ __forceinline__ uint32_t word_of(const U4 &v, uint32_t i) {
-  return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
-}
-
 // selp: a predicated select the compiler cannot turn back into a branch
 __device__ __forceinline__ uint32_t select_u32(uint32_t pred, uint32_t a, uint32_t b) {
   uint32_t r;
@@ -132,18 +112,21 @@ __device__ __forceinline__ uint32_t select_u32(uint32_t pred, uint32_t a, uint32
   return r;
 }
 
-// word i of a Philox block without divergence (lanes of a window pick
-// different words): all four words are formed, then two levels of selp
-__device__ __forceinline__ uint32_t word_of_sel(const U4 &v, uint32_t i) {
-  const uint32_t lo = select_u32(i & 1u, v.y, v.x);
-  const uint32_t hi = select_u32(i & 1u, v.w, v.z);
-  return select_u32(i & 2u, hi, lo);
+// the selection uniform's raw word for city j at (step, ant)
+__device__ __forceinline__ uint32_t sel_word(uint32_t j, uint32_t step, uint32_t ant, const RoundKeys &rk) {
+  const uint2 r = philox2x32_10(sel_counter(j, step), ant, rk);
+  return select_u32(j & 1u, r.y, r.x);
 }
 
-__device__ __forceinline__ uint32_t start_city(uint32_t n, uint32_t ant, uint32_t iteration,
-                                               uint32_t k0, uint32_t k1) {
-  U4 r = philox4x32_10(U4{0u, 0u, ant, iteration}, k0, k1);
-  return lemire_bound(r.x, n);
+__device__ __forceinline__ uint32_t start_city(uint32_t n, uint32_t ant, const RoundKeys &rk) {
+  return lemire_bound(philox2x32_10(0u, ant, rk).x, n);
+}
+
+// RW threshold: ((x >> 5) 2^26 + (y >> 6)) 2^-53, numpy's random() layout
+__device__ __forceinline__ double rw_threshold(uint32_t step, uint32_t ant, const RoundKeys &rk) {
+  const uint2 r = philox2x32_10(kRwLow | (step << 16), ant, rk);
+  const uint64_t k = ((uint64_t)(r.x >> 5) << 26) | (uint64_t)(r.y >> 6);
+  return (double)k * 0x1p-53;
 }
 
 // ---------------------------------------------------------------------------

@@ -88,7 +88,7 @@ class Solver:
     ``AcoParams.for_instance`` (alpha, beta, rho, n_ants / m, k, selection,
     seed, gamma_schedule, q0_tau, max_iters).
     construct: "sorted" (pruned scan, default) or "dense" (full-row stream).
-    stream: "device" (default, the on-chip Philox4x32 stream) or "replay":
+    stream: "device" (default, the on-chip Philox2x32 stream) or "replay":
     every iteration replays the reference's own numpy streams on the device
     (colony.construct_tours(stream="replay")) with the reference's log-domain
     rule, so a run reproduces antbatch's run_experiment bit for bit (tours,

@@ -107,7 +107,7 @@ def test_spin_edges_u_zero_one_and_known_answers(golden):
 
 def test_rw_device_uniforms_match_restatement():
     g = np.random.default_rng(2)
-    step = g.integers(1, 70000, 5000)
+    step = g.integers(1, 65535, 5000)  # steps < n <= 65535
     ant = g.integers(0, 2**31, 5000)
     seed = 2**50 + 7
     assert np.array_equal(trng.device_rw_uniforms(seed, 9, step, ant), fastpath.rw_uniform(seed, 9, step, ant))

@@ -2,7 +2,7 @@
 
 * oracle.reference_port reproduces the golden vectors produced by running the
   reference package itself (tests/golden/make_golden.py) bit for bit.
-* oracle.fastpath's Philox4x32-10 reproduces the Random123 known-answer
+* oracle.fastpath's Philox2x32-10 reproduces the Random123 known-answer
   vectors, and its pairwise-sum restatement equals numpy's ndarray.sum.
 """
 
@@ -112,18 +112,36 @@ def test_probability_known_answer():
 # ---------------------------------------------------------------------------
 # fast-path restatement
 # ---------------------------------------------------------------------------
-KAT = [  # Random123 philox4x32-10 known-answer vectors
-    ((0, 0, 0, 0), (0, 0), (0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8)),
-    ((0xFFFFFFFF,) * 4, (0xFFFFFFFF,) * 2, (0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD)),
-    ((0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344), (0xA4093822, 0x299F31D0),
-     (0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1)),
+KAT = [  # Random123 philox2x32-10 known-answer vectors (kat_vectors)
+    ((0, 0), 0, (0xFF1DAE59, 0x6CD10DF2)),
+    ((0xFFFFFFFF, 0xFFFFFFFF), 0xFFFFFFFF, (0x2C3F628B, 0xAB4FD7AD)),
+    ((0x243F6A88, 0x85A308D3), 0x13198A2E, (0xDD7CE038, 0xF62A4C12)),
 ]
 
 
 @pytest.mark.parametrize("ctr,key,want", KAT)
 def test_philox_known_answers(ctr, key, want):
-    got = fastpath.philox4x32_10(np.array([ctr], dtype=np.uint64), np.array(key, dtype=np.uint64))[0]
+    got = fastpath.philox2x32_10(np.array([ctr], dtype=np.uint64), key)[0]
     assert tuple(int(v) for v in got) == want
+
+
+def test_stream_keys_and_counters():
+    # H(seed) is a fixed function (MurmurHash3 fmix64, xor-folded); the
+    # iteration offsets it, so the iterations of one run never share a key
+    assert fastpath.seed_hash32(0) == 0
+    h = fastpath.seed_hash32(12345)
+    assert fastpath.stream_key(12345, 7) == (h + 7) & 0xFFFFFFFF
+    assert len({fastpath.stream_key(3, it) for it in range(5000)}) == 5000
+    assert len({fastpath.seed_hash32(s) for s in range(100_000)}) == 100_000  # fmix64 is a bijection
+    # the start counter (0, ant) and RW counters (0xffff | step << 16, ant)
+    # never collide with a selection counter ((j >> 1) | step << 16, ant),
+    # step >= 1, j >> 1 <= 0x7fff
+    sel_low = np.arange(0, 65535) >> 1
+    assert sel_low.max() < fastpath.RW_LOW
+    u = fastpath.uniforms(9, 2, np.array([1, 1, 2]), np.array([0, 0, 0]), np.array([4, 5, 4]))
+    w = fastpath.philox2x32_10(np.array([[2 | 1 << 16, 0], [2 | 2 << 16, 0]], dtype=np.uint64),
+                               fastpath.stream_key(9, 2))
+    assert np.array_equal(u, fastpath.bits_to_uniform(np.array([w[0, 0], w[0, 1], w[1, 0]])))
 
 
 def test_uniform_conversion_is_exact_and_open():
