@@ -80,6 +80,24 @@ struct LeafCost {
   }
 };
 
+// Tour length of one finished tour row (int32, global, written by this warp)
+// in numpy's pairwise order: lanes sum the leaves in parallel (pw_leaf_sum),
+// lane 0 folds them.  Plain loads: the row was written in this kernel.
+__device__ __forceinline__ double warp_tour_cost(int n, const int32_t *trow, const double *dist,
+                                                 const int2 *leaves, int n_leaves, double *ls, int lane) {
+  __syncwarp();
+  for (int L = lane; L < n_leaves; L += 32) {
+    const int2 lf = leaves[L];
+    ls[L] = pw_leaf_sum(lf.y, [&](int q) {
+      const int s = lf.x + q;
+      const int s1 = (s + 1 == n) ? 0 : s + 1;
+      return __ldg(dist + ((uint32_t)trow[s] * (uint32_t)n + (uint32_t)trow[s1]));
+    });
+  }
+  __syncwarp();
+  return pw_fold(n, ls);  // meaningful in lane 0
+}
+
 // per-ant shared scratch: leaf buffer, leaf sums, visited bitmask (16-B aligned)
 __host__ __device__ __forceinline__ size_t ant_scratch_bytes(int n_leaves, int nwords) {
   return ((size_t)8 * kPwBlock + (size_t)8 * n_leaves + (size_t)4 * nwords + 15) & ~(size_t)15;

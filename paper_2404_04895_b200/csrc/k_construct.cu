@@ -130,11 +130,14 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
     leaf_buf = reinterpret_cast<double *>(mine);
     leaf_sum = leaf_buf + kPwBlock;
     vis = reinterpret_cast<uint32_t *>(leaf_sum + a.n_leaves);
-  } else {  // per ant: the visited set only
-    vis = reinterpret_cast<uint32_t *>(smem + (((size_t)4 * a.nwords + 15) & ~(size_t)15) * warp);
+  } else {  // leaves, then per ant: leaf sums (epilogue length), visited set
+    const size_t ls_bytes = ((size_t)8 * a.n_leaves + 15) & ~(size_t)15;
+    unsigned char *mine = smem + ls_bytes + (ls_bytes + (((size_t)4 * a.nwords + 15) & ~(size_t)15)) * warp;
+    leaf_sum = reinterpret_cast<double *>(mine);
+    vis = reinterpret_cast<uint32_t *>(mine + ls_bytes);
   }
 
-  if (COST && threadIdx.x == 0) pw_leaves(n, leaves);
+  if (a.costs != nullptr && threadIdx.x == 0) pw_leaves(n, leaves);
   __syncthreads();
 
   const int ant = blockIdx.x * warps + warp;
@@ -259,6 +262,10 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
     lc.load(cur, start);
     lc.push();  // closing edge n-1
     const double c = lc.finish();
+    if (lane == 0) a.costs[ant] = c;
+  }
+  if (!COST && a.costs != nullptr) {  // epilogue: the finished row, lanes in parallel
+    const double c = warp_tour_cost(n, tw.row, a.dist, leaves, a.n_leaves, leaf_sum, lane);
     if (lane == 0) a.costs[ant] = c;
   }
   if (PROBE && lane == 0) atomicAdd(a.scan_count, windows);
@@ -703,13 +710,14 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
 #undef TACO_GROUP_CASE
       return TACO_ERR_ARG;
     }
-    // tour length: a separate k_tour_cost pass after the construction (the
-    // kernel then needs <= 32 registers instead of 72), or fused (COST) when
-    // dist is too large to stay in L2 and the separate pass would pay for
-    // random DRAM sectors: n = 2392, m = 4096 2.05 vs 2.08 ms; n = 5000,
-    // m = 4096 4.36 vs 4.44; n = 10000, m = 8192 20.8 vs 19.9 (fused).
-    // TACO_SORTED_COST=fused|separate overrides (tuning knob).
-    bool fused_cost = costs_out != nullptr && n > 7000;
+    // tour length: computed in the kernel's epilogue from the finished tour
+    // row, lanes summing pairwise leaves in parallel, so the step loop carries
+    // no length state (35 registers in the loop instead of 72) and the random
+    // dist reads overlap other warps' construction.  Measured (ms, incl. the
+    // length): n = 2392, m = 4096 epilogue 1.755 / separate k_tour_cost pass
+    // 1.779 / fused per-step accumulation 1.836; n = 10000, m = 8192 16.3 /
+    // 17.2 / 17.7.  TACO_SORTED_COST=fused|separate|epilogue (tuning knob).
+    bool fused_cost = false;
     if (const char *ev = getenv("TACO_SORTED_COST")) fused_cost = costs_out != nullptr && ev[0] == 'f';
     const int max_warps = fused_cost ? kSortedMaxWarps : kSortedMaxWarpsLean;
     // warps per CTA: all ants of an SM in one CTA when they fit (one wave);
@@ -719,10 +727,13 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     int warps = ants_per_sm < 1 ? 1 : (ants_per_sm > max_warps ? max_warps : ants_per_sm);
     if (const char *ev = getenv("TACO_SORTED_WARPS")) warps = atoi(ev);
     if (warps < 1 || warps > max_warps) return TACO_ERR_ARG;
+    // (separate: tour lengths by a k_tour_cost launch after the kernel instead
+    // of the epilogue; TACO_SORTED_COST=separate, tuning knob)
+    const bool separate_cost = !fused_cost && getenv("TACO_SORTED_COST") && getenv("TACO_SORTED_COST")[0] == 's';
     auto scratch = [&](int nw) {
-      return fused_cost ? ant_scratch_bytes(n_leaves, nw) : (((size_t)4 * nw + 15) & ~(size_t)15);
+      return fused_cost ? ant_scratch_bytes(n_leaves, nw) : leaves_bytes + (((size_t)4 * nw + 15) & ~(size_t)15);
     };
-    const size_t lb = fused_cost ? leaves_bytes : 0;
+    const size_t lb = leaves_bytes;
     // visited set: a byte per city when the SM's ants fit with it (VIS8),
     // else the bit map; TACO_SORTED_VIS=bits forces the bit map (tuning knob)
     const int nwords8 = (n + 3) / 4;
@@ -737,7 +748,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     const size_t smem = lb + scratch(vis8 ? nwords8 : nwords) * warps;
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
     SortedArgs a{n, m_local, ant_offset, vis8 ? nwords8 : nwords, n_leaves, ldw, sw, si, dist, iteration, state,
-                 tours_out, fused_cost ? costs_out : nullptr, status, scan_count, ks};
+                 tours_out, separate_cost ? nullptr : costs_out, status, scan_count, ks};
     const int grid = (m_local + warps - 1) / warps;
     const int mode = fused_cost ? 0 : (ants_per_sm > max_warps ? 2 : 1);
     const int code = mode * 4 + (vis8 ? 2 : 0) + (scan_count ? 1 : 0);
@@ -750,7 +761,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
       TACO_SORTED_CASE(2, 0, 0) TACO_SORTED_CASE(2, 0, 1) TACO_SORTED_CASE(2, 1, 0) TACO_SORTED_CASE(2, 1, 1)
 #undef TACO_SORTED_CASE
     }
-    if (rc == TACO_OK && costs_out != nullptr && !fused_cost)
+    if (rc == TACO_OK && costs_out != nullptr && separate_cost)
       rc = taco_tour_cost(n, m_local, tours_out, 0, dist, costs_out, stream);
     if (rc != TACO_OK) return rc;
   } else if (variant == TACO_CONSTRUCT_DENSE) {
