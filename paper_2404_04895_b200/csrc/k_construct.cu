@@ -281,7 +281,6 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
 // the same bucket-ceiling stop as k_construct_sorted: identical tours.
 // ---------------------------------------------------------------------------
 constexpr int kGroupWarps = 4;
-constexpr int kCostStack = 24;  // pairwise-fold stack depth (tree height <= ~12)
 
 struct GroupArgs {
   int n, m_local, ant_offset, nwords, n_leaves, ld;
@@ -297,41 +296,6 @@ struct GroupArgs {
   PhiloxKeys ks;
 };
 
-// per-ant tour length in numpy's pairwise order, owned by the group's lane 0:
-// eight strided accumulators and the fold stack live in shared memory
-struct GroupCost {
-  double *acc;  // [8]
-  double *stk;  // [kCostStack]
-  int L, i, len, main_end, sp;
-  double res;
-
-  __device__ __forceinline__ void open(const int2 *leaves) {
-    len = leaves[L].y;
-    main_end = len >= 8 ? len - (len % 8) : 0;
-    i = 0;
-    res = 0.0;
-  }
-  __device__ __forceinline__ void push(double d, const int2 *leaves, const uint8_t *merges, int n_leaves) {
-    if (i < main_end) {
-      const int q = i & 7;
-      acc[q] = (i < 8) ? d : __dadd_rn(acc[q], d);
-    } else {
-      res = __dadd_rn(res, d);
-    }
-    if (++i == main_end)
-      res = __dadd_rn(__dadd_rn(__dadd_rn(acc[0], acc[1]), __dadd_rn(acc[2], acc[3])),
-                      __dadd_rn(__dadd_rn(acc[4], acc[5]), __dadd_rn(acc[6], acc[7])));
-    if (i == len) {  // leaf complete: push it and close the tree nodes it ends
-      stk[sp++] = res;
-      for (int k = merges[L]; k > 0; --k) {
-        const double right = stk[--sp];
-        const double left = stk[--sp];
-        stk[sp++] = __dadd_rn(left, right);
-      }
-      if (++L < n_leaves) open(leaves);
-    }
-  }
-};
 
 template <int G, int E, bool PROBE>
 __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __grid_constant__ GroupArgs a) {
@@ -342,15 +306,14 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n, L = a.n_leaves;
   int2 *leaves = reinterpret_cast<int2 *>(smem);
-  uint8_t *merges = reinterpret_cast<uint8_t *>(smem + 8 * (size_t)L);
-  size_t off = (8 * (size_t)L + (size_t)L + 15) & ~(size_t)15;
+  const size_t off = (8 * (size_t)L + 15) & ~(size_t)15;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const size_t per_warp = (((size_t)4 * a.nwords * A + 15) & ~(size_t)15) + (size_t)8 * A * (8 + kCostStack);
+  const size_t per_warp = (((size_t)4 * a.nwords * A + 15) & ~(size_t)15) + off;
   unsigned char *wp = smem + off + per_warp * warp;
   uint32_t *vis = reinterpret_cast<uint32_t *>(wp);  // [nwords][A]: conflict-free per ant
-  double *cost_mem = reinterpret_cast<double *>(wp + (((size_t)4 * a.nwords * A + 15) & ~(size_t)15));
-  if (threadIdx.x == 0) pw_leaves_merges(n, leaves, merges);
+  double *leaf_sum = reinterpret_cast<double *>(wp + (((size_t)4 * a.nwords * A + 15) & ~(size_t)15));
+  if (threadIdx.x == 0) pw_leaves(n, leaves);
   for (int q = lane; q < a.nwords * A; q += 32) vis[q] = 0u;
   __syncthreads();
 
@@ -364,14 +327,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
   const uint32_t un = (uint32_t)n, ld = (uint32_t)a.ld;
   const uint32_t start = start_city(un, gant, rk);
   int32_t *trow = a.tours + (size_t)ant * n;
-  GroupCost gc;
-  gc.acc = cost_mem + (size_t)g * (8 + kCostStack);
-  gc.stk = gc.acc + 8;
-  gc.L = 0;
-  gc.sp = 0;
-  const bool with_cost = a.costs != nullptr;
-  if (with_cost) gc.open(leaves);
-  double pending = 0.0;
+  bool complete = false;  // this group's tour reached n cities
   if (alive && gl == 0) {
     vis[(start >> 5) * A + g] |= 1u << (start & 31);
     trow[0] = (int32_t)start;
@@ -449,27 +405,30 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
         if (gl == 0) {
           vis[(bestj >> 5) * A + g] |= 1u << (bestj & 31);
           trow[step] = (int32_t)bestj;
-          if (with_cost) {
-            if (step > 1) gc.push(pending, leaves, merges, L);  // edge step-2
-            pending = __ldg(a.dist + (size_t)cur * n + bestj);   // edge step-1
-          }
         }
         cur = bestj;
         ++step;
         chunk = 0;
         best = -1.0f;
         bestj = 0xffffffffu;
-        if (step == un) {  // tour complete: close it and fold its length
-          if (gl == 0 && with_cost) {
-            gc.push(pending, leaves, merges, L);                          // edge n-2
-            gc.push(__ldg(a.dist + (size_t)cur * n + start), leaves, merges, L);  // closing edge
-            a.costs[ant] = gc.stk[0];
-          }
+        if (step == un) {  // tour complete
+          complete = true;
           alive = false;
         }
       }
     }
     __syncwarp();
+  }
+  // tour lengths of the warp's complete tours, the whole warp per tour
+  // (pairwise leaves across lanes; the step loop carries no length state)
+  if (a.costs != nullptr) {
+    const int ant0 = (blockIdx.x * kGroupWarps + warp) * A;
+#pragma unroll 1
+    for (int q = 0; q < A; ++q) {
+      if (!__shfl_sync(kFull, (int)complete, q * G)) continue;
+      const double c = warp_tour_cost(n, a.tours + (size_t)(ant0 + q) * n, a.dist, leaves, L, leaf_sum, lane);
+      if (lane == 0) a.costs[ant0 + q] = c;
+    }
   }
   if (PROBE && gl == 0 && ant < a.m_local) atomicAdd(a.scan_count, (chunks * CH + 16) / 32);
 }
@@ -683,8 +642,8 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     }
     if (G > 0) {
       const size_t A = 32 / G;
-      const size_t per_warp = (((size_t)4 * nwords * A + 15) & ~(size_t)15) + (size_t)8 * A * (8 + kCostStack);
-      const size_t smem = ((8 * (size_t)n_leaves + (size_t)n_leaves + 15) & ~(size_t)15) + per_warp * kGroupWarps;
+      const size_t per_warp = (((size_t)4 * nwords * A + 15) & ~(size_t)15) + leaves_bytes;
+      const size_t smem = leaves_bytes + per_warp * kGroupWarps;
       if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
       GroupArgs ga{n, m_local, ant_offset, nwords, n_leaves, ldw, sw, si, dist, iteration, state,
                    tours_out, costs_out, status, scan_count, ks};

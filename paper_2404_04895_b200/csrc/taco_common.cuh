@@ -230,46 +230,6 @@ __device__ inline int pw_leaves(int n, int2 *leaves) {
   return count;
 }
 
-// Leaves in order plus, for each leaf, how many internal nodes of the
-// pairwise tree complete right after it (post-order).  Summing leaves with a
-// stack and popping merges[L] pairs after leaf L reproduces the recursion's
-// (left + right) additions exactly.  Returns the leaf count.
-__device__ inline int pw_leaves_merges(int n, int2 *leaves, uint8_t *merges) {
-  int stack_off[40], stack_len[40], stack_state[40];
-  int sp = 0, nl = 0;
-  stack_off[0] = 0;
-  stack_len[0] = n;
-  stack_state[0] = 0;
-  sp = 1;
-  while (sp) {
-    const int top = sp - 1;
-    const int off = stack_off[top], len = stack_len[top];
-    if (len <= kPwBlock) {
-      leaves[nl] = make_int2(off, len);
-      merges[nl] = 0;
-      ++nl;
-      --sp;
-    } else if (stack_state[top] == 0) {
-      stack_state[top] = 1;
-      stack_off[sp] = off;
-      stack_len[sp] = pw_split(len);
-      stack_state[sp] = 0;
-      ++sp;
-    } else if (stack_state[top] == 1) {
-      stack_state[top] = 2;
-      const int n2 = pw_split(len);
-      stack_off[sp] = off + n2;
-      stack_len[sp] = len - n2;
-      stack_state[sp] = 0;
-      ++sp;
-    } else {
-      ++merges[nl - 1];  // this node closes right after its last leaf
-      --sp;
-    }
-  }
-  return nl;
-}
-
 // Sum one leaf exactly as numpy's pairwise_sum base cases do.
 // `at(i)` returns element i of the leaf.
 template <typename F>

@@ -25,6 +25,7 @@ ap.add_argument("--m", type=int, default=4096)
 ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--variant", default="sorted", help="sorted | dense | rw")
+ap.add_argument("--no-costs", action="store_true", help="tours only (no tour lengths)")
 args = ap.parse_args()
 
 inst = taco.euclidean_instance(np.random.default_rng(0).uniform(0, 2000, (args.n, 2)))
@@ -37,7 +38,7 @@ s.check()
 torch.cuda.synchronize()
 dev = s.dev
 tours = torch.zeros((args.m, args.n), dtype=torch.int32, device=dev)
-costs = torch.zeros(args.m, dtype=torch.float64, device=dev)
+costs = None if args.no_costs else torch.zeros(args.m, dtype=torch.float64, device=dev)
 st = _device.new_status(dev)
 scan = torch.zeros(1, dtype=torch.int64, device=dev)
 variant = _lib.CONSTRUCT_SORTED if args.variant == "sorted" else _lib.CONSTRUCT_DENSE
