@@ -178,8 +178,16 @@ def _dist_init(gpus: int):
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # TACO_BENCH_SMOKE=1: every rank on cuda:0 over gloo (host-side
+        # collectives, no kernel waits on another rank's): a functional check
+        # of the N > 1 path on a one-GPU box, not a measurement
+        if os.environ.get("TACO_BENCH_SMOKE") == "1":
+            local = 0
+            torch.cuda.set_device(0)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return rank, world, local
 
 
@@ -337,7 +345,8 @@ def run_ours(args) -> dict | None:
 
     it_per_s = 1000.0 / ms_per_step
     peak, peak_kind = _peaks()
-    launches_per_iter = 5 + (0 if rw else 1) + (1 if solver.graph else 0)
+    sharded = solver.shard.world > 1
+    launches_per_iter = 5 + (0 if rw else 1) + (1 if solver.graph else 0) + (1 if sharded else 0)
     m_local = solver.shard.count
     # roofline.achieved = ALGORITHMIC bytes per launch / launch time, with the
     # per-unit figure of SURVEY §8(d): each ant streams its current row of the
@@ -392,6 +401,7 @@ def run_ours(args) -> dict | None:
                               f"{'rw' if rw else args.construct} (or the lane-group variant), k_elite_rank, "
                               "k_track_best, k_elite_neighbors, k_row_update"
                               f"{'' if rw else ', k_row_sort'}{', k_iter_advance' if solver.graph else ''}"
+                              f"{', k_shard_elites (+ NCCL collectives)' if sharded else ''}"
                               f"{' (+ CUB radix-sort kernels: m > 16384)' if m > 16384 else ''}; "
                               f"{'replayed as one CUDA graph per iteration' if solver.graph else 'eager launches'}"),
         "best_length": best_len,
