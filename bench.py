@@ -234,16 +234,22 @@ def run_ours(args) -> dict | None:
 
     # ---- e2e: solve from host buffers through the public API ---------------
     # headline e2e: host coordinates (pinned) -> device_euclidean_instance
-    # (16n B H2D, dist/eta built on the device) -> Solver -> K x step(), each
-    # step reading status + best length + best tour back in one D2H copy.
-    # e2e_host_instance: the same from a host TspInstance (dist + eta H2D).
+    # (16n B H2D, dist/eta built on the device) -> Solver -> K iterations of
+    # Solver.iterate(), each iteration's status + best length + best tour read
+    # back in one D2H copy (pipelined: the next iteration is queued first).
+    # e2e_host_instance: the same from a host TspInstance (dist + eta H2D);
+    # e2e_step: the device instance with K blocking step() calls instead.
     coords_pinned = torch.from_numpy(coords).pin_memory()
 
-    def e2e_run(make_instance, steps):
+    def e2e_run(make_instance, steps, blocking=False):
         solver_ = taco.Solver(make_instance(), params, construct=args.construct)
         out = None
-        for _ in range(steps):
-            out = solver_.step()
+        if blocking:
+            for _ in range(steps):
+                out = solver_.step()
+        else:
+            for _it, tour_, len_ in solver_.iterate(steps):
+                out = (tour_, len_)
         return out
 
     def dev_inst():
@@ -255,14 +261,15 @@ def run_ours(args) -> dict | None:
     torch.cuda.synchronize()
     # each e2e figure is the median of three complete runs (instance, Solver,
     # K steps): millisecond-scale host timings pick up scheduler / GC noise
-    e2e_times = {"device_instance": [], "host_instance": []}
+    e2e_times = {"device_instance": [], "host_instance": [], "step": []}
     for _rep in range(3):
-        for name, make in (("device_instance", dev_inst), ("host_instance", lambda: inst)):
+        for name, make, blocking in (("device_instance", dev_inst, False), ("host_instance", lambda: inst, False),
+                                     ("step", dev_inst, True)):
             gc.collect()
             _barrier(world)
             with sampler.window() if sampler else _null():
                 t0 = time.perf_counter()
-                best_tour, best_len = e2e_run(make, args.steps)
+                best_tour, best_len = e2e_run(make, args.steps, blocking)
                 torch.cuda.synchronize()
                 e2e_times[name].append(_max_over_ranks(time.perf_counter() - t0, world))
             _device._INSTANCES.clear()
@@ -390,12 +397,16 @@ def run_ours(args) -> dict | None:
         "e2e": {"value": args.steps / e2e_times["device_instance"], "unit": "iterations/s",
                 "h2d_bytes_per_step": (n * 2 * 8) / args.steps,
                 "d2h_bytes_per_step": 32 + n * 4,
-                "what": ("pinned host coords -> device_euclidean_instance -> Solver -> K x step(), each returning "
-                         "status + best length + best tour in one D2H copy; median of 3 complete runs")},
+                "what": ("pinned host coords -> device_euclidean_instance -> Solver -> K iterations of "
+                         "Solver.iterate(), each iteration's status + best length + best tour read back in one "
+                         "D2H copy (the next iteration queued before the read); median of 3 complete runs")},
         "e2e_host_instance": {"value": args.steps / e2e_times["host_instance"], "unit": "iterations/s",
                               "h2d_bytes_per_step": (2 * n * n * 8) / args.steps,
                               "d2h_bytes_per_step": 32 + n * 4,
-                              "what": "host TspInstance (dist + eta H2D) -> Solver -> K x step()"},
+                              "what": "host TspInstance (dist + eta H2D) -> Solver -> Solver.iterate(K)"},
+        "e2e_step": {"value": args.steps / e2e_times["step"], "unit": "iterations/s",
+                     "h2d_bytes_per_step": (n * 2 * 8) / args.steps, "d2h_bytes_per_step": 32 + n * 4,
+                     "what": "as e2e, with K blocking Solver.step() calls (host waits for every iteration)"},
         "gpu_launches": args.steps * launches_per_iter,
         "gpu_launches_note": (f"{launches_per_iter} libtaco kernels per iteration: k_construct_"
                               f"{'rw' if rw else args.construct} (or the lane-group variant), k_elite_rank, "

@@ -464,6 +464,35 @@ class Solver:
         self.step_async()
         return self._read_back()
 
+    def iterate(self, iters: int):
+        """Run ``iters`` iterations, yielding ``(iteration, best_tour,
+        best_length)`` after each one — the same values ``step()`` returns.
+
+        Pipelined: iteration t+1 is already queued on the device when the
+        result of iteration t is read (an async D2H copy into a pinned double
+        buffer, waited on by event), so the device never idles on the host.
+        The reference's per-iteration records (bench.py:199-207) come out of
+        this loop at device speed."""
+        bufs = [torch.empty_like(self._io_host).pin_memory() for _ in range(2)]
+        events = [torch.cuda.Event(), torch.cuda.Event()]
+        pending = None
+        for t in range(int(iters)):
+            self.step_async()
+            b = t & 1
+            bufs[b].copy_(self._io, non_blocking=True)
+            events[b].record()
+            if pending is not None:
+                yield self._decode_io(*pending)
+            pending = (bufs[b], events[b], self.iteration - 1)
+        if pending is not None:
+            yield self._decode_io(*pending)
+
+    def _decode_io(self, buf: torch.Tensor, event, iteration: int):
+        event.synchronize()
+        raw = buf.numpy()
+        self._raise_status(int(raw[0:4].view(np.int32)[0]))
+        return (iteration, raw[32:].view(np.int32).astype(np.int64), float(raw[16:24].view(np.float64)[0]))
+
     def _read_back(self) -> tuple[np.ndarray, float]:
         self._io_host.copy_(self._io)  # synchronizes the stream
         raw = self._io_host.numpy()

@@ -552,3 +552,20 @@ def test_solver_split_update_path_is_bit_identical(monkeypatch, selection):
     assert np.array_equal(split.pheromone().tau, fused.pheromone().tau)
     assert split.best()[1] == fused.best()[1]
     assert np.array_equal(split.last_batch().tours, fused.last_batch().tours)
+
+
+def test_iterate_yields_what_step_returns():
+    """Solver.iterate (pipelined: iteration t+1 queued before t is read)
+    yields exactly the per-iteration results of blocking step() calls, in
+    graph and eager mode."""
+    inst = euclid(91, 60)
+    for graph in (True, False):
+        params = taco.AcoParams(m=32, k=3, selection="adair", seed=5, gamma_schedule=taco.GammaSchedule(1.5, 1.0, 7))
+        a = taco.Solver(inst, params, graph=graph)
+        want = [a.step() for _ in range(7)]
+        b = taco.Solver(inst, params, graph=graph)
+        got = list(b.iterate(7))
+        assert [g[0] for g in got] == list(range(7))
+        for (tw, lw), (_, tg, lg) in zip(want, got):
+            assert np.array_equal(tw, tg) and lw == lg
+        assert np.array_equal(a.pheromone().tau, b.pheromone().tau)
