@@ -161,7 +161,7 @@ int taco_eta_power(int64_t count, const double *eta, double beta, double *out,
 
 /*
  * Tour construction, fast path (device Philox2x32-10 stream; key
- * H(seed) + iteration, counter ((city >> 1) | step << 16, ant), word city & 1).
+ * H(seed) + iteration, counter (ant, (city >> 1) | step << 16), word city & 1).
  * Replaces colony.construct_tours colony.py:87-154 (IR / AdaIR branch) with
  * the deviate block of rng.step_exponentials rng.py:42-49 replaced by the
  * on-chip keyed uniform u(seed, iteration, step, ant, city) and the log-domain
@@ -193,7 +193,7 @@ int taco_construct(int n, int m_local, int ant_offset, int variant,
  * the reference's sequential cumsum rule (a certified parallel scan, with an
  * exact sequential recount when the crossing is within rounding distance).
  * u is one 53-bit Philox2x32-10 uniform per (step, ant) (counter
- * (0xffff | step << 16, ant)) in place of rng.step_uniforms (rng.py:52-62).  Start cities and
+ * (ant, 0xffff | step << 16)) in place of rng.step_uniforms (rng.py:52-62).  Start cities and
  * the fused tour length are as in taco_construct.  exact_count (nullable,
  * device u64) accumulates the steps that took the sequential recount;
  * force_exact != 0 makes every step take it (test hook).  state as in

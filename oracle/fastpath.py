@@ -59,31 +59,31 @@ def bits_to_uniform(x: np.ndarray) -> np.ndarray:
 
 def uniforms(seed: int, iteration: int, step, ant, city) -> np.ndarray:
     """u(seed, iteration, step, ant, city); arrays broadcast together.
-    Counter ((city >> 1) | step << 16, ant), word city & 1."""
+    Counter (ant, (city >> 1) | step << 16), word city & 1."""
     step, ant, city = np.broadcast_arrays(np.asarray(step, dtype=np.uint64),
                                           np.asarray(ant, dtype=np.uint64),
                                           np.asarray(city, dtype=np.uint64))
-    ctr = np.stack([((city >> np.uint64(1)) | (step << np.uint64(16))) & np.uint64(MASK32), ant], axis=-1)
+    ctr = np.stack([ant, ((city >> np.uint64(1)) | (step << np.uint64(16))) & np.uint64(MASK32)], axis=-1)
     words = philox2x32_10(ctr, stream_key(seed, iteration))
     pick = np.where((city & np.uint64(1)) == 1, words[..., 1], words[..., 0])
     return bits_to_uniform(pick)
 
 
 def starts(seed: int, iteration: int, ants, n: int) -> np.ndarray:
-    """Device start cities: Lemire bound of word 0 of counter (0, ant)."""
+    """Device start cities: Lemire bound of word 0 of counter (ant, 0)."""
     ants = np.asarray(ants, dtype=np.uint64)
-    ctr = np.stack([np.zeros_like(ants), ants], axis=-1)
+    ctr = np.stack([ants, np.zeros_like(ants)], axis=-1)
     x = philox2x32_10(ctr, stream_key(seed, iteration))[..., 0].astype(np.uint64)
     return ((x * np.uint64(n)) >> np.uint64(32)).astype(np.int64)
 
 
 def rw_uniform(seed: int, iteration: int, step, ant) -> np.ndarray:
     """Device RW threshold: 53 bits of Philox2x32-10 counter
-    (0xffff | step << 16, ant), as numpy's random():
+    (ant, 0xffff | step << 16), as numpy's random():
     ((x >> 5) * 2^26 + (y >> 6)) / 2^53."""
     step = np.asarray(step, dtype=np.uint64).ravel()
     ant = np.asarray(ant, dtype=np.uint64).ravel()
-    ctr = np.stack([(np.uint64(RW_LOW) | (step << np.uint64(16))) & np.uint64(MASK32), ant], axis=-1)
+    ctr = np.stack([ant, (np.uint64(RW_LOW) | (step << np.uint64(16))) & np.uint64(MASK32)], axis=-1)
     r = philox2x32_10(ctr, stream_key(seed, iteration)).astype(np.uint64)
     k = ((r[:, 0] >> np.uint64(5)) << np.uint64(26)) | (r[:, 1] >> np.uint64(6))
     return k.astype(np.float64) * 2.0**-53

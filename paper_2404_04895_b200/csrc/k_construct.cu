@@ -102,8 +102,8 @@ __device__ __forceinline__ void score_window_u(float w, uint32_t j, const uint32
 
 template <bool VIS8>
 __device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t *vis, uint32_t step,
-                                             uint32_t gant, const RoundKeys &rk, float &best, uint32_t &bestj) {
-  score_window_u<VIS8>(w, j, vis, best, bestj, [&] { return sel_word(j, step, gant, rk); });
+                                             const AntKey &ak, const RoundKeys &rk, float &best, uint32_t &bestj) {
+  score_window_u<VIS8>(w, j, vis, best, bestj, [&] { return sel_word(j, step, ak, rk); });
 }
 
 // The first window of the next row is issued as soon as the step's winner is
@@ -146,11 +146,12 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   const RoundKeys rk = round_keys(a.ks, it);
+  const AntKey ak = ant_key(gant, rk);
   const uint32_t un = (uint32_t)n;  // n <= 65535, so every row offset fits in 32 bits
   const float *__restrict__ sw = a.sw;
   const uint16_t *__restrict__ si = a.si;
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
-  const uint32_t start = start_city(un, gant, rk);
+  const uint32_t start = start_city(un, ak, rk);
   __syncwarp();
   if (lane == 0) mark_visited<VIS8>(vis, start);
   __syncwarp();
@@ -190,7 +191,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
         const uint32_t sink = consume(wg) ^ jg;
         const long long pb = clock64();
         const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
-        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(sel_word(jg, step, gant, rk)))) + 1u : 0u;
+        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(sel_word(jg, step, ak, rk)))) + 1u : 0u;
         const uint32_t k2 = consume(__uint_as_float(key));
         const long long pc = clock64();
         const uint32_t mkey = __reduce_max_sync(kFull, k2);
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
         }
       }
 #endif
-      score_window<VIS8>(wg, jg, vis, step, gant, rk, best, bestj);
+      score_window<VIS8>(wg, jg, vis, step, ak, rk, best, bestj);
       if (PROBE) ++windows;
       // entries after this window have W <= bucket_ceiling(window's last W)
       const float wl = __shfl_sync(kFull, wg, 31);
@@ -324,8 +325,9 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   const RoundKeys rk = round_keys(a.ks, it);
+  const AntKey ak = ant_key(gant, rk);
   const uint32_t un = (uint32_t)n, ld = (uint32_t)a.ld;
-  const uint32_t start = start_city(un, gant, rk);
+  const uint32_t start = start_city(un, ak, rk);
   int32_t *trow = a.tours + (size_t)ant * n;
   bool complete = false;  // this group's tour reached n cities
   if (alive && gl == 0) {
@@ -372,7 +374,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const uint32_t key =
-            cand[e] ? __float_as_uint(__fmul_rn(w[e], bits_to_uniform(sel_word(j[e], step, gant, rk)))) + 1u : 0u;
+            cand[e] ? __float_as_uint(__fmul_rn(w[e], bits_to_uniform(sel_word(j[e], step, ak, rk)))) + 1u : 0u;
         const unsigned long long pe = ((unsigned long long)key << 32) | (uint32_t)~j[e];
         p = pe > p ? pe : p;
       }
@@ -467,8 +469,9 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   const RoundKeys rk = round_keys(a.ks, it);
+  const AntKey ak = ant_key(gant, rk);
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
-  const uint32_t start = start_city((uint32_t)n, gant, rk);
+  const uint32_t start = start_city((uint32_t)n, ak, rk);
   __syncwarp();
   if (lane == 0) mark_visited<false>(vis, start);
   __syncwarp();
@@ -492,8 +495,8 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
       const bool any = (nib != 0xfu) && wmax > 0.0f && (lkey == 0u || wmax >= __uint_as_float(lkey - 1u));
       if (any) {
         // cities 4q..4q+3: the blocks of j >> 1 = 2q and 2q + 1
-        const uint2 r0 = philox2x32_10(sel_counter(4u * q, (uint32_t)step), gant, rk);
-        const uint2 r1 = philox2x32_10(sel_counter(4u * q + 2u, (uint32_t)step), gant, rk);
+        const uint2 r0 = philox_ant(sel_counter(4u * q, (uint32_t)step), ak, rk);
+        const uint2 r1 = philox_ant(sel_counter(4u * q + 2u, (uint32_t)step), ak, rk);
         const float wc[4] = {wv.x, wv.y, wv.z, wv.w};
         const uint32_t rc[4] = {r0.x, r0.y, r1.x, r1.y};
 #pragma unroll
@@ -534,14 +537,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
 
 __global__ void k_starts(int n, int m_local, int ant_offset, PhiloxKeys ks, uint32_t iteration, int32_t *out) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
-  if (a < m_local) out[a] = (int32_t)start_city((uint32_t)n, (uint32_t)(ant_offset + a), round_keys(ks, iteration));
+  if (a >= m_local) return;
+  const RoundKeys rk = round_keys(ks, iteration);
+  out[a] = (int32_t)start_city((uint32_t)n, ant_key((uint32_t)(ant_offset + a), rk), rk);
 }
 
 __global__ void k_uniforms(int count, const uint32_t *step, const uint32_t *ant, const uint32_t *city,
                            PhiloxKeys ks, uint32_t iteration, float *out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= count) return;
-  out[t] = bits_to_uniform(sel_word(city[t], step[t], ant[t], round_keys(ks, iteration)));
+  const RoundKeys rk = round_keys(ks, iteration);
+  out[t] = bits_to_uniform(sel_word(city[t], step[t], ant_key(ant[t], rk), rk));
 }
 
 __global__ void k_philox(int count, const uint32_t *ctr, const uint32_t *key, uint32_t *out) {

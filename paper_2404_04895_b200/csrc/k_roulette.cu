@@ -27,7 +27,7 @@
 // cross-lane dependency stalls the loads.  Pass B re-reads only the crossing
 // tile with lane l owning the 8 contiguous columns [t*256 + 8l, +8).  Device
 // stream: one 53-bit uniform per (step, ant) from the Philox2x32-10 counter
-// (0xffff | step << 16, ant) — a low half the IR/AdaIR stream never uses (its
+// (ant, 0xffff | step << 16) — a low half the IR/AdaIR stream never uses (its
 // low half is j >> 1 <= 0x7fff); see taco_common.cuh.
 #include "construct_common.cuh"
 
@@ -314,8 +314,9 @@ __global__ void __launch_bounds__(WARPS * 32, 7) k_construct_rw(const __grid_con
   const uint32_t gant = (uint32_t)(a.ant_offset + ant);
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
   const RoundKeys rk = round_keys(a.ks, it);
+  const AntKey ak = ant_key(gant, rk);
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
-  const uint32_t start = start_city((uint32_t)n, gant, rk);
+  const uint32_t start = start_city((uint32_t)n, ak, rk);
   __syncwarp();
   if (lane == 0) vis[start >> 5] |= 1u << (start & 31);
   __syncwarp();
@@ -327,7 +328,7 @@ __global__ void __launch_bounds__(WARPS * 32, 7) k_construct_rw(const __grid_con
   uint32_t cur = start;
   unsigned exact_steps = 0;
   for (int step = 1; step < n; ++step) {
-    const double u = rw_threshold((uint32_t)step, gant, rk);
+    const double u = rw_threshold((uint32_t)step, ak, rk);
     const BitmaskRow row{a.p + (size_t)cur * n, vis, n};
     bool exact = false;
     const int j = rw_pick<VEC>(row, n, a.ntiles, u, tile_tot, part, lane, a.force_exact != 0, &exact);
@@ -390,7 +391,9 @@ __global__ void __launch_bounds__(WARPS * 32)
 __global__ void k_rw_uniforms(int count, const uint32_t *step, const uint32_t *ant, PhiloxKeys ks,
                               uint32_t iteration, double *out) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < count) out[t] = rw_threshold(step[t], ant[t], round_keys(ks, iteration));
+  if (t >= count) return;
+  const RoundKeys rk = round_keys(ks, iteration);
+  out[t] = rw_threshold(step[t], ant_key(ant[t], rk), rk);
 }
 
 }  // namespace taco

@@ -17,10 +17,12 @@ namespace taco {
 //                   64-bit finalizer of the seed: distinct iterations of a run
 //                   never share a key
 //   selection u(step >= 1, ant, city j):
-//                   counter ((j >> 1) | step << 16, ant), word j & 1
+//                   counter (ant, (j >> 1) | step << 16), word j & 1
 //                   (n <= 65535: j >> 1 <= 0x7fff, step <= 0xfffe)
-//   start city:     counter (0, ant) (step 0 never selects), word 0, Lemire
-//   RW threshold:   counter (0xffff | step << 16, ant), 53 bits of both words
+//   start city:     counter (ant, 0) (step 0 never selects), word 0, Lemire
+//   RW threshold:   counter (ant, 0xffff | step << 16), 53 bits of both words
+// Counter word 0 is the ant, so round 1's product is one per ant (AntKey) and
+// a window's chain starts at round 2: 9 dependent multiplies per uniform.
 //   u = ((x >> 9) + 0.5) * 2^-23 in (0, 1), exact in fp32
 // One block is a chain of 10 (IMAD.WIDE, LOP3) pairs: half the instructions
 // of a Philox4x32-10 block, of which the sorted scan used one word per lane.
@@ -92,6 +94,28 @@ __device__ __forceinline__ uint2 philox2x32_10(uint32_t x0, uint32_t x1, uint32_
 
 __device__ __forceinline__ uint32_t sel_counter(uint32_t j, uint32_t step) { return (j >> 1) | (step << 16); }
 
+// round 1 of Philox2x32-10 on counter (ant, c): hi(M ant) ^ k0 ^ c, lo(M ant)
+struct AntKey {
+  uint32_t hk, lo;  // hi(M * ant) ^ k[0], lo(M * ant)
+};
+
+__device__ __forceinline__ AntKey ant_key(uint32_t ant, const RoundKeys &rk) {
+  return AntKey{__umulhi(kPhiloxM, ant) ^ rk.k[0], kPhiloxM * ant};
+}
+
+// Philox2x32-10 of counter (ant, c), rounds 2..10
+__device__ __forceinline__ uint2 philox_ant(uint32_t c, const AntKey &ak, const RoundKeys &rk) {
+  uint32_t x0 = ak.hk ^ c, x1 = ak.lo;
+#pragma unroll
+  for (int r = 1; r < 10; ++r) {
+    const uint32_t hi = __umulhi(kPhiloxM, x0);
+    const uint32_t lo = kPhiloxM * x0;
+    x0 = hi ^ rk.k[r] ^ x1;
+    x1 = lo;
+  }
+  return make_uint2(x0, x1);
+}
+
 __device__ __forceinline__ float bits_to_uniform(uint32_t x) {
   // 1 + k 2^-23 (k = x >> 9) built from bits, minus (1 - 2^-24): both steps
   // exact (Sterbenz), so u = (k + 1/2) 2^-23 without an int->float conversion
@@ -113,18 +137,18 @@ __device__ __forceinline__ uint32_t select_u32(uint32_t pred, uint32_t a, uint32
 }
 
 // the selection uniform's raw word for city j at (step, ant)
-__device__ __forceinline__ uint32_t sel_word(uint32_t j, uint32_t step, uint32_t ant, const RoundKeys &rk) {
-  const uint2 r = philox2x32_10(sel_counter(j, step), ant, rk);
+__device__ __forceinline__ uint32_t sel_word(uint32_t j, uint32_t step, const AntKey &ak, const RoundKeys &rk) {
+  const uint2 r = philox_ant(sel_counter(j, step), ak, rk);
   return select_u32(j & 1u, r.y, r.x);
 }
 
-__device__ __forceinline__ uint32_t start_city(uint32_t n, uint32_t ant, const RoundKeys &rk) {
-  return lemire_bound(philox2x32_10(0u, ant, rk).x, n);
+__device__ __forceinline__ uint32_t start_city(uint32_t n, const AntKey &ak, const RoundKeys &rk) {
+  return lemire_bound(philox_ant(0u, ak, rk).x, n);
 }
 
 // RW threshold: ((x >> 5) 2^26 + (y >> 6)) 2^-53, numpy's random() layout
-__device__ __forceinline__ double rw_threshold(uint32_t step, uint32_t ant, const RoundKeys &rk) {
-  const uint2 r = philox2x32_10(kRwLow | (step << 16), ant, rk);
+__device__ __forceinline__ double rw_threshold(uint32_t step, const AntKey &ak, const RoundKeys &rk) {
+  const uint2 r = philox_ant(kRwLow | (step << 16), ak, rk);
   const uint64_t k = ((uint64_t)(r.x >> 5) << 26) | (uint64_t)(r.y >> 6);
   return (double)k * 0x1p-53;
 }

@@ -133,13 +133,13 @@ def test_stream_keys_and_counters():
     assert fastpath.stream_key(12345, 7) == (h + 7) & 0xFFFFFFFF
     assert len({fastpath.stream_key(3, it) for it in range(5000)}) == 5000
     assert len({fastpath.seed_hash32(s) for s in range(100_000)}) == 100_000  # fmix64 is a bijection
-    # the start counter (0, ant) and RW counters (0xffff | step << 16, ant)
-    # never collide with a selection counter ((j >> 1) | step << 16, ant),
+    # the start counter (ant, 0) and RW counters (ant, 0xffff | step << 16)
+    # never collide with a selection counter (ant, (j >> 1) | step << 16),
     # step >= 1, j >> 1 <= 0x7fff
     sel_low = np.arange(0, 65535) >> 1
     assert sel_low.max() < fastpath.RW_LOW
     u = fastpath.uniforms(9, 2, np.array([1, 1, 2]), np.array([0, 0, 0]), np.array([4, 5, 4]))
-    w = fastpath.philox2x32_10(np.array([[2 | 1 << 16, 0], [2 | 2 << 16, 0]], dtype=np.uint64),
+    w = fastpath.philox2x32_10(np.array([[0, 2 | 1 << 16], [0, 2 | 2 << 16]], dtype=np.uint64),
                                fastpath.stream_key(9, 2))
     assert np.array_equal(u, fastpath.bits_to_uniform(np.array([w[0, 0], w[0, 1], w[1, 0]])))
 
