@@ -6,22 +6,24 @@ The reference has no solver object; its iteration is the loop body of
     construct_tours -> select_elite -> accumulate_increments -> apply_update
     -> compute_probability_matrix
 The Solver runs exactly that sequence per ``step()`` with all state resident in
-HBM and five kernel launches per iteration:
+HBM and six kernel launches per iteration:
 
-    1. taco_construct        tours (m x n int32) from the fp32 selection table,
-                             with their lengths accumulated on the fly in
-                             numpy's pairwise order
+    1. taco_construct        tours (m x n int32) from the row-sorted fp32
+                             selection table; the kernel's epilogue sums each
+                             tour's length in numpy's pairwise order
        [multi-GPU: all-gather of the m lengths over NCCL]
-    3. taco_elite_order      stable radix argsort of the lengths
-    4. taco_track_best       best-so-far tour / length on device
-       taco_elite_neighbors  (prev, next) of every city in the k elite tours
+    2. taco_elite_order      stable rank of the lengths
+    3. taco_track_best       best-so-far tour / length on device
+    4. taco_elite_neighbors  (prev, next) of every city in the k elite tours
        [multi-GPU: taco_shard_elites + SUM all-reduce of the k elite tours]
-    5. taco_row_update       deposit + evaporation + P + W(gamma of it+1)
+    5. taco_row_update       deposit + evaporation + P + W(gamma of it+1), then
+    6. (k_row_sort)          the row-sorted table the next construction scans
        [multi-GPU, row-partitioned: this rank's rows only, then an in-place
         all-gather of the selection table and of the status words]
 
 The host synchronizes only when a result is read (``step()`` returns the best
-tour and length; ``run()`` reads once at the end).
+tour and length; ``iterate()`` reads every iteration's result while the next
+one runs; ``run()`` reads once at the end).
 
 On one GPU the iteration is captured once as a CUDA graph and replayed
 (``graph=True``, the default there): the iteration number and the next 1/gamma
