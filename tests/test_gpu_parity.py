@@ -58,6 +58,16 @@ def test_device_uniforms_and_starts_match_restatement():
     assert np.array_equal(u, fastpath.uniforms(seed, 77, step, ant, city))
     assert np.array_equal(trng.device_starts(seed, 3, 2392, 4096, ant_offset=100),
                           fastpath.starts(seed, 3, np.arange(100, 4196), 2392))
+    # the counter's extremes (n <= 65535: city, step <= 65534), 32-bit ants,
+    # iterations and seeds whose key wraps around 2^32
+    step = np.array([1, 65534, 65534, 1, 40000, 2])
+    city = np.array([65534, 65534, 0, 1, 65533, 32768])
+    ant = np.array([0, 2**32 - 1, 2**31, 7, 123456789, 2**32 - 2])
+    for seed_, it in ((0, 0), (2**64 - 1, 2**32 - 1), (5, 2**31 + 3)):
+        assert np.array_equal(trng.device_uniforms(seed_, it, step, ant, city),
+                              fastpath.uniforms(seed_, it, step, ant, city))
+        assert np.array_equal(trng.device_starts(seed_, it, 65535, 64, ant_offset=2**31 - 64),
+                              fastpath.starts(seed_, it, np.arange(2**31 - 64, 2**31), 65535))
 
 
 # ---------------------------------------------------------------------------
