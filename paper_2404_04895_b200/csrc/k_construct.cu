@@ -485,14 +485,22 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   for (int step = 1; step < n; ++step) {
     const float4 *row = reinterpret_cast<const float4 *>(a.w + (size_t)cur * a.ldw);
     uint32_t lkey = 0u, lj = 0xffffffffu;
+    uint32_t wkey = 0u;  // the warp's running best key (refreshed every 32 groups)
+    const int rounds = (nq + 31) >> 5;
 #pragma unroll 4
-    for (int q = lane; q < nq; q += 32) {
-      const float4 wv = __ldg(row + q);
-      const uint32_t nib = (vis[q >> 3] >> ((q & 7) * 4)) & 0xfu;
-      // a score is w * u < w, so a group whose largest W cannot reach this
-      // lane's running best (key - 1 as float) cannot change the argmax
+    for (int t = 0; t < rounds; ++t) {
+      const int q = lane + 32 * t;
+      float4 wv = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      uint32_t nib = 0xfu;
+      if (q < nq) {
+        wv = __ldg(row + q);
+        nib = (vis[q >> 3] >> ((q & 7) * 4)) & 0xfu;
+      }
+      // a score is w * u < w, so a group whose largest W is below the warp's
+      // running best score (key - 1 as float) cannot reach or tie the argmax
       const float wmax = fmaxf(fmaxf(wv.x, wv.y), fmaxf(wv.z, wv.w));
-      const bool any = (nib != 0xfu) && wmax > 0.0f && (lkey == 0u || wmax >= __uint_as_float(lkey - 1u));
+      const uint32_t thr = lkey > wkey ? lkey : wkey;
+      const bool any = (nib != 0xfu) && wmax > 0.0f && (thr == 0u || wmax >= __uint_as_float(thr - 1u));
       if (any) {
         // cities 4q..4q+3: the blocks of j >> 1 = 2q and 2q + 1
         const uint2 r0 = philox_ant(sel_counter(4u * q, (uint32_t)step), ak, rk);
@@ -511,6 +519,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
           }
         }
       }
+      wkey = __reduce_max_sync(kFull, lkey);
     }
     const uint32_t mkey = __reduce_max_sync(kFull, lkey);
     if (mkey == 0u) {
