@@ -1,7 +1,7 @@
 """TensorACO-B200 benchmark (driver contract: one JSON line on rank 0).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c3] [--construct sorted|dense]
+                    [--config c3] [--construct auto|sorted|dense]
 
 A "step" is one full ACO iteration of the hot path (bench.py:199-206 of the
 reference): construct m tours -> lengths -> stable elite sort -> index-mapped
@@ -220,6 +220,8 @@ def run_ours(args) -> dict | None:
     from paper_2404_04895_b200 import _device, _lib
 
     n, m, selection = CONFIGS[args.config]
+    if args.construct == "auto":  # the Solver's own choice (full-row kernel for tiny rows)
+        args.construct = "dense" if n < taco.Solver.DENSE_MAX_N else "sorted"
     k = max(1, m // 10)
     period = args.warmup + args.steps
     # NVML clock sampler (rank 0): samples only inside the timed regions
@@ -276,7 +278,9 @@ def run_ours(args) -> dict | None:
     e2e_times = {k: float(np.median(v)) for k, v in e2e_times.items()}
 
     # ---- device-timed value ------------------------------------------------
-    solver = taco.Solver(inst, params, construct=args.construct)
+    # steady state of a long run: graph replays (where the Solver uses them)
+    # from the first timed iteration on
+    solver = taco.Solver(inst, params, construct=args.construct, graph_warmup=0)
     for _ in range(args.warmup):
         solver.step_async()
     solver.check()
@@ -488,7 +492,7 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="c3")
-    ap.add_argument("--construct", choices=("sorted", "dense"), default="sorted")
+    ap.add_argument("--construct", choices=("auto", "sorted", "dense"), default="auto")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm processes (0: all host cores)")

@@ -89,7 +89,8 @@ class Solver:
     distance matrix, or a device instance (``device_euclidean_instance``).  params: an AcoParams, or keyword overrides of
     ``AcoParams.for_instance`` (alpha, beta, rho, n_ants / m, k, selection,
     seed, gamma_schedule, q0_tau, max_iters).
-    construct: "sorted" (pruned scan, default) or "dense" (full-row stream).
+    construct: "auto" (default: "dense" for n < DENSE_MAX_N, else "sorted"),
+    "sorted" (pruned scan of the row-sorted table) or "dense" (full-row stream).
     stream: "device" (default, the on-chip Philox2x32 stream) or "replay":
     every iteration replays the reference's own numpy streams on the device
     (colony.construct_tours(stream="replay")) with the reference's log-domain
@@ -103,14 +104,22 @@ class Solver:
     graph: replay a captured CUDA graph per iteration (default: on for a
     single-GPU device-stream colony with n*m < 2^16, where launch
     overhead matters; the sharded and replay modes always run eagerly).
+    graph_warmup: eager iterations before the first capture (default
+    GRAPH_WARMUP = 32: a short run does not pay a capture it cannot
+    amortize; 0 captures at the second iteration).
     """
 
     GRAPH_BATCH = 8  # iterations per graph replay in run()
+    GRAPH_WARMUP = 32  # eager iterations before the first capture
     GRAPH_MAX_WORK = 1 << 16  # default graph mode below this many (city x ant) selections per iteration
     FUSED_MAX_N = 27000  # the fused row kernel stages a row of n doubles in shared memory
+    # construct="auto": the full-row kernel below this n (no row sort; n = 51,
+    # m = 64: 0.040 vs 0.044 ms per iteration; even at n = 100; sorted from 200)
+    DENSE_MAX_N = 96
 
-    def __init__(self, instance, params=None, *, construct: str = "sorted", stream: str = "device",
-                 group=None, graph: bool | None = None, update: str | None = None, **overrides):
+    def __init__(self, instance, params=None, *, construct: str = "auto", stream: str = "device",
+                 group=None, graph: bool | None = None, update: str | None = None,
+                 graph_warmup: int | None = None, **overrides):
         if isinstance(instance, _device.DeviceInstance):  # built on the device (from_coords)
             self.inst, device_inst = None, instance
         else:
@@ -118,8 +127,10 @@ class Solver:
         self.n = n = int(device_inst.n if device_inst is not None else self.inst.n)
         self.params = p = _as_params(params, n, overrides)
         self.rw = Selection(p.selection) is Selection.RW  # roulette wheel spins on P itself
-        if construct not in ("sorted", "dense"):
-            raise ValueError(f"construct must be 'sorted' or 'dense', got {construct!r}")
+        if construct not in ("auto", "sorted", "dense"):
+            raise ValueError(f"construct must be 'auto', 'sorted' or 'dense', got {construct!r}")
+        if construct == "auto":  # tiny rows: the full-row kernel needs no sorted table
+            construct = "dense" if n < self.DENSE_MAX_N else "sorted"
         lib = _lib.load()
         if construct == "sorted" and n > lib.taco_max_sorted_n():
             construct = "dense"
@@ -230,6 +241,7 @@ class Solver:
             raise ValueError("CUDA-graph replay covers the single-GPU device-stream solver")
         self.graph = use_graph
         self._graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self._eager_left = self.GRAPH_WARMUP if graph_warmup is None else int(graph_warmup)
         # P / W for iteration 0 from the initial pheromone (bench.py:191-192);
         # the reference raises NumericalUnderflow right there
         self._rebuild_tables(evaporate=False, gamma_next=construction_gamma(p, 0))
@@ -309,13 +321,14 @@ class Solver:
     def _replay(self, iters: int) -> None:
         g = self._graphs.get(iters)
         if g is None:
-            if not self._graphs and not getattr(self, "_warm", False):
-                # first use: run eagerly (same launches, same device state) so
-                # one-time host work (kernel attributes, device queries) happens
-                # outside any capture
+            if self._eager_left > 0:
+                # the first GRAPH_WARMUP iterations run eagerly (same launches,
+                # same device state): one-time host work (kernel attributes,
+                # device queries) stays outside any capture, and a short run
+                # does not pay a capture (~2 ms) it cannot amortize
                 for _ in range(iters):
                     self._enqueue(None, None)
-                self._warm = True
+                self._eager_left -= iters
                 return
             g = self._capture(iters)
         g.replay()

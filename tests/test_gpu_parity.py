@@ -431,7 +431,7 @@ def test_graph_replay_equals_eager_solver(selection):
     n, m = 45, 20
     inst = euclid(12, n)
     params = taco.AcoParams(m=m, k=3, selection=selection, seed=5, gamma_schedule=taco.GammaSchedule(1.5, 1.0, 6))
-    g = taco.Solver(inst, params, graph=True)
+    g = taco.Solver(inst, params, graph=True, graph_warmup=1)
     e = taco.Solver(inst, params, graph=False)
     for _ in range(3):  # step(): eager warm-up, then 1-iteration graph replays
         assert g.step()[1] == e.step()[1]
@@ -442,6 +442,13 @@ def test_graph_replay_equals_eager_solver(selection):
     assert np.array_equal(g.pheromone().tau, e.pheromone().tau)
     assert np.array_equal(g.last_batch().costs, e.last_batch().costs)
     assert int(g.best_iter.item()) == int(e.best_iter.item())
+    # default warm-up: GRAPH_WARMUP eager iterations, then captured batches
+    d = taco.Solver(inst, params)
+    assert d.graph
+    bd = d.run(22 + 2 * taco.Solver.GRAPH_WARMUP)
+    be = e.run(2 * taco.Solver.GRAPH_WARMUP)
+    assert bd[1] == be[1] and np.array_equal(d.pheromone().tau, e.pheromone().tau)
+    assert len(d._graphs) > 0
 
 
 @pytest.mark.parametrize("selection", ["adair", "rw"])
@@ -569,11 +576,11 @@ def test_iterate_yields_what_step_returns():
     yields exactly the per-iteration results of blocking step() calls, in
     graph and eager mode."""
     inst = euclid(91, 60)
-    for graph in (True, False):
+    for graph, warm in ((True, 0), (True, None), (False, None)):
         params = taco.AcoParams(m=32, k=3, selection="adair", seed=5, gamma_schedule=taco.GammaSchedule(1.5, 1.0, 7))
-        a = taco.Solver(inst, params, graph=graph)
+        a = taco.Solver(inst, params, graph=graph, graph_warmup=warm)
         want = [a.step() for _ in range(7)]
-        b = taco.Solver(inst, params, graph=graph)
+        b = taco.Solver(inst, params, graph=graph, graph_warmup=warm)
         got = list(b.iterate(7))
         assert [g[0] for g in got] == list(range(7))
         for (tw, lw), (_, tg, lg) in zip(want, got):
