@@ -216,7 +216,11 @@ class Solver:
         self.rowsum = torch.zeros(n, dtype=torch.float64, device=dev)
         # rows longer than the fused kernel's shared-memory row use the split
         # update, with its delta / tau^alpha eta^beta workspaces
-        self._split_update = n > self.FUSED_MAX_N
+        # the split kernels also win for large elite sets at n >= 4000: their
+        # deposit spreads a row's 2k additions over warp-per-row blocks
+        # (n = 5000: k = 6553 1.52 vs 2.42 ms, k = 3276 1.11 vs 1.43, k = 1638
+        # 0.90 vs 0.94; n = 2392, k = 1638 and n = 10000, k = 819 stay fused)
+        self._split_update = n > self.FUSED_MAX_N or (n >= 4000 and p.k >= 1500 and not self.partitioned)
         self._delta_ws = torch.empty((n, n), dtype=torch.float64, device=dev) if self._split_update else None
         self._unnorm_ws = torch.empty((n, n), dtype=torch.float64, device=dev) if self._split_update else None
         self.status = self._io[0:16].view(torch.int32)
