@@ -205,7 +205,14 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
         }
       }
 #endif
-      score_window<VIS8>(wg, jg, vis, step, ak, rk, best, bestj);
+      if (base == 0) {
+        // first window: Philox issued ahead of the visited lookup and the vote
+        uint32_t x = sel_word(jg, step, ak, rk);
+        asm volatile("" : "+r"(x));
+        score_window_u<VIS8>(wg, jg, vis, best, bestj, [&] { return x; });
+      } else {
+        score_window<VIS8>(wg, jg, vis, step, ak, rk, best, bestj);
+      }
       if (PROBE) ++windows;
       // entries after this window have W <= bucket_ceiling(window's last W)
       const float wl = __shfl_sync(kFull, wg, 31);
