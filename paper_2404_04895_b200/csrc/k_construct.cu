@@ -368,6 +368,14 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
 #pragma unroll
       for (int e = 0; e < E; ++e) w[e] = 0.0f, j[e] = 0u;
     }
+    // Philox issued ahead of the visited lookups and the vote (with A ants per
+    // warp the vote almost never skips the chunk)
+    uint32_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      x[e] = sel_word(j[e], step, ak, rk);
+      asm volatile("" : "+r"(x[e]));
+    }
     bool cand[E];
     bool any = false;
 #pragma unroll
@@ -381,7 +389,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
 #pragma unroll
       for (int e = 0; e < E; ++e) {
         const uint32_t key =
-            cand[e] ? __float_as_uint(__fmul_rn(w[e], bits_to_uniform(sel_word(j[e], step, ak, rk)))) + 1u : 0u;
+            cand[e] ? __float_as_uint(__fmul_rn(w[e], bits_to_uniform(x[e]))) + 1u : 0u;
         const unsigned long long pe = ((unsigned long long)key << 32) | (uint32_t)~j[e];
         p = pe > p ? pe : p;
       }
