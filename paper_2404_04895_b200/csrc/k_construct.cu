@@ -219,10 +219,17 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
           best = __uint_as_float(mkey - 1u);
         }
       } else if (base == 0) {
-        // first window: Philox issued ahead of the visited lookup and the vote
+        // first window: Philox issued ahead of the visited lookup and the vote;
+        // best is still -1, so no running-best test and the window's best wins
         uint32_t x = sel_word(jg, step, ak, rk);
         asm volatile("" : "+r"(x));
-        score_window_u<VIS8>(wg, jg, vis, best, bestj, [&] { return x; });
+        const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
+        if (__any_sync(kFull, cand)) {
+          const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(x))) + 1u : 0u;
+          const uint32_t mkey = __reduce_max_sync(kFull, key);
+          bestj = __reduce_min_sync(kFull, key == mkey ? jg : 0xffffffffu);
+          best = __uint_as_float(mkey - 1u);
+        }
       } else {
         score_window<VIS8>(wg, jg, vis, step, ak, rk, best, bestj);
       }
