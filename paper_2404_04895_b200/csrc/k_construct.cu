@@ -205,20 +205,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
         }
       }
 #endif
-      if (MODE == 2 && base == 0) {
-        // first window, > 32 ants/SM: no vote, the max reduction itself says
-        // whether a lane had a candidate (best is still -1, so the window's
-        // best entry wins outright).  C4 16.0 -> 15.6 ms; slower with few
-        // ants per SM (n = 1000, m = 1024: 0.476 -> 0.522 ms), hence MODE 2 only.
-        const uint32_t x = sel_word(jg, step, ak, rk);
-        const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
-        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(x))) + 1u : 0u;
-        const uint32_t mkey = __reduce_max_sync(kFull, key);
-        if (mkey != 0u) {
-          bestj = __reduce_min_sync(kFull, key == mkey ? jg : 0xffffffffu);
-          best = __uint_as_float(mkey - 1u);
-        }
-      } else if (base == 0) {
+      if (base == 0) {
         // first window: Philox issued ahead of the visited lookup and the vote;
         // best is still -1, so no running-best test and the window's best wins
         uint32_t x = sel_word(jg, step, ak, rk);
