@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define TACO_ABI_VERSION 3
+#define TACO_ABI_VERSION 4
 
 /* status codes (return values and status[0]) */
 #define TACO_OK 0
@@ -58,12 +58,16 @@ extern "C" {
  * by-value argument), so one captured iteration replays unchanged;
  * taco_iter_advance moves the state to the next iteration on the stream.
  * inv_gamma is 1/gamma of the selection table built at the END of the
- * iteration, i.e. for iteration + 1 (the W the next construction reads).
+ * iteration, i.e. for iteration + 1 (the W the next construction reads);
+ * inv_gamma_cur is 1/gamma of the iteration itself (the table the
+ * construction reads; its f64 fallback needs it).
  */
 typedef struct taco_iter_state {
   uint32_t iteration;
   uint32_t reserved;
   double inv_gamma;
+  double inv_gamma_cur;
+  double reserved2;
 } taco_iter_state;
 
 int taco_abi_version(void);
@@ -174,7 +178,15 @@ int taco_eta_power(int64_t count, const double *eta, double beta, double *out,
  * a k_tour_cost pass on the same stream.
  * scan_count (nullable, device u64) is incremented by the number of 32-entry
  * global table windows the SORTED variant read (traffic probe for the
- * roofline report).  state (nullable): iteration from state->iteration.
+ * roofline report).
+ * No W > 0 candidate left (W underflows below 2^-126 of its row's best, e.g.
+ * for gamma < 1): the step is decided in f64 among the unvisited cities with
+ * v = fb_a[cur, j]^fb_alpha (* fb_b[cur, j]) > 0 by log(v) * inv_gamma +
+ * log(u) (fb_a = P, or tau with fb_b = eta^beta; n x n, row pitch n); with
+ * none (or fb_a NULL), city 0 if unvisited — numpy's argmax of an all -inf
+ * row (selection.py:152-155) — else TACO_NO_CANDIDATE (colony.py:149).
+ * state (nullable): iteration from state->iteration, inv_gamma from
+ * state->inv_gamma_cur.
  */
 int taco_construct(int n, int m_local, int ant_offset, int variant,
                    const float *w, int ldw,
@@ -182,6 +194,8 @@ int taco_construct(int n, int m_local, int ant_offset, int variant,
                    uint64_t seed, uint32_t iteration,
                    const double *dist, int32_t *tours_out, double *costs_out,
                    int32_t *status, unsigned long long *scan_count,
+                   const double *fb_a, double fb_alpha, const double *fb_b,
+                   double inv_gamma,
                    const taco_iter_state *state, void *stream);
 
 /*
@@ -248,6 +262,18 @@ int taco_select_parity(int n, int m, int step, const double *logw,
                        const double *e_block, int64_t *current,
                        uint8_t *visited, int64_t *tours,
                        int32_t *status, void *stream);
+
+/*
+ * argmax_select_block (selection.py:143-155) drop-in: next_out[a] =
+ * argmax_j(logw[current[a], j] - e_block[a, j]) with visited (m x n u8) cities
+ * at -inf, first of ties, 0 for an all -inf row; scores_out (nullable, m x n
+ * f64) receives the masked scores like the reference's scratch buffer.
+ * Nothing else is updated (no visited mark, no assertion).
+ */
+int taco_argmax_select_block(int n, int m, const double *logw,
+                             const int64_t *current, const double *e_block,
+                             const uint8_t *visited, double *scores_out,
+                             int64_t *next_out, void *stream);
 
 /*
  * Reference-stream replay: the same round as
@@ -340,12 +366,14 @@ int taco_shard_elites(int n, int k, const int32_t *order, int ant_offset,
 
 /*
  * Best-so-far tracking for Solver.step(): if costs[order[0]] < *best_cost,
- * copy that tour to best_tour and update best_cost / best_iter.
+ * copy that tour to best_tour and update best_cost / best_iter.  Nothing is
+ * touched when status (nullable) records a stopped iteration (status[3]).
  */
 int taco_track_best(int n, const int32_t *tours, const double *costs,
                     const int32_t *order, double *best_cost,
                     int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
-                    const taco_iter_state *state, void *stream);
+                    const int32_t *status, const taco_iter_state *state,
+                    void *stream);
 
 /*
  * End of a graph-replayed iteration: state->iteration += 1 and

@@ -1,0 +1,257 @@
+/* ORACLE (test infrastructure only): C restatement of the engine's device
+ * stream and product-form selection rule, for parity checks at the BASELINE
+ * sizes, where the numpy restatement (oracle/fastpath.py) is too slow.
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg load
+ * this library (through oracle/fastpath_c.py); the product never does.
+ *
+ * What it restates (the reference rule it approximates is
+ * argmax_j(log P[cur, j] / gamma - E[a, j]) over unvisited j, first of ties,
+ * selection.py:143-155 / colony.py:126-152 of /root/reference/pkg/src/antbatch):
+ *   - Philox2x32-10 (Random123), key = H(seed) + iteration, counter
+ *     (ant, (j >> 1) | step << 16), word j & 1;  u = ((x >> 9) + 1/2) 2^-23
+ *   - start city: Lemire bound of word 0 of counter (ant, 0)
+ *   - next = argmax_j fp32(W[cur, j] * u_j) over unvisited j with W > 0,
+ *     lowest j on ties (a FULL scan: no sorted table, no pruning)
+ *   - no W > 0 candidate left: the f64 fallback, argmax over unvisited j with
+ *     v_j > 0 of log(v_j) * inv_gamma + log(u_j), v = A[cur, j]^alpha (* B[cur, j]);
+ *     none either: city 0 when it is unvisited (numpy's argmax of an all -inf
+ *     row, selection.py:152-155), else the "selector chose a visited city"
+ *     failure (colony.py:149)
+ * Compiled without FMA contraction or fast-math so every float operation is
+ * one IEEE round-to-nearest, as on the device.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define PHILOX_M 0xD256D193u
+#define PHILOX_W 0x9E3779B9u
+
+uint32_t fpo_seed_hash32(uint64_t seed) {
+  uint64_t f = seed;
+  f ^= f >> 33;
+  f *= 0xff51afd7ed558ccdull;
+  f ^= f >> 33;
+  f *= 0xc4ceb9fe1a85ec53ull;
+  f ^= f >> 33;
+  return (uint32_t)(f ^ (f >> 32));
+}
+
+static inline void philox2x32_10(uint32_t x0, uint32_t x1, uint32_t key, uint32_t out[2]) {
+  for (int r = 0; r < 10; ++r) {
+    const uint64_t prod = (uint64_t)PHILOX_M * x0;
+    const uint32_t hi = (uint32_t)(prod >> 32), lo = (uint32_t)prod;
+    x0 = hi ^ key ^ x1;
+    x1 = lo;
+    key += PHILOX_W;
+  }
+  out[0] = x0;
+  out[1] = x1;
+}
+
+void fpo_philox(int count, const uint32_t *ctr2, const uint32_t *key, uint32_t *out2) {
+  for (int t = 0; t < count; ++t) philox2x32_10(ctr2[2 * t], ctr2[2 * t + 1], key[t], out2 + 2 * t);
+}
+
+static inline float bits_to_uniform(uint32_t x) {
+  /* (k + 1/2) 2^-23, k = x >> 9: exact in fp32 */
+  return (float)(x >> 9) * 0x1p-23f + 0x1p-24f;
+}
+
+static inline uint32_t start_city(uint32_t ant, uint32_t key, uint32_t n) {
+  uint32_t r[2];
+  philox2x32_10(ant, 0u, key, r);
+  return (uint32_t)(((uint64_t)r[0] * n) >> 32);
+}
+
+/* the raw words of cities 2q, 2q+1 at (step, ant) */
+static inline void pair_words(uint32_t q, uint32_t step, uint32_t ant, uint32_t key, uint32_t r[2]) {
+  philox2x32_10(ant, q | (step << 16), key, r);
+}
+
+static inline double fb_value(const double *a, double alpha, const double *b, size_t off) {
+  /* numpy's scalar-power dispatch for the exponents the engine uses */
+  const double x = a[off];
+  double v;
+  if (alpha == 1.0)
+    v = x;
+  else if (alpha == 2.0)
+    v = x * x;
+  else if (alpha == 0.0)
+    v = 1.0;
+  else if (alpha == 0.5)
+    v = sqrt(x);
+  else
+    v = pow(x, alpha);
+  return b ? v * b[off] : v;
+}
+
+/* One ant's tour.  Returns 0, or 2 when the selector is left without a city
+ * (the reference's assertion).  scratch: n bytes. */
+static int one_tour(const float *w, int n, int ldw, uint32_t key, uint32_t ant, const double *fb_a,
+                    double fb_alpha, const double *fb_b, double inv_gamma, int32_t *tour, uint8_t *seen,
+                    int64_t *fallbacks) {
+  memset(seen, 0, (size_t)n);
+  uint32_t cur = start_city(ant, key, (uint32_t)n);
+  seen[cur] = 1;
+  tour[0] = (int32_t)cur;
+  for (uint32_t step = 1; step < (uint32_t)n; ++step) {
+    const float *row = w + (size_t)cur * ldw;
+    float best = -1.0f;
+    int bj = -1;
+    for (int q = 0; 2 * q < n; ++q) {
+      const int j0 = 2 * q, j1 = 2 * q + 1;
+      const int c0 = !seen[j0] && row[j0] > 0.0f;
+      const int c1 = j1 < n && !seen[j1] && row[j1] > 0.0f;
+      if (!c0 && !c1) continue;
+      uint32_t r[2];
+      pair_words((uint32_t)q, step, ant, key, r);
+      if (c0) {
+        const float s = row[j0] * bits_to_uniform(r[0]);
+        if (s > best) best = s, bj = j0;
+      }
+      if (c1) {
+        const float s = row[j1] * bits_to_uniform(r[1]);
+        if (s > best) best = s, bj = j1;
+      }
+    }
+    if (bj < 0) { /* f64 fallback, then numpy's all -inf argmax */
+      if (fallbacks) ++*fallbacks;
+      double fbest = -INFINITY;
+      if (fb_a != NULL) {
+        for (int j = 0; j < n; ++j) {
+          if (seen[j]) continue;
+          const double v = fb_value(fb_a, fb_alpha, fb_b, (size_t)cur * n + j);
+          if (!(v > 0.0)) continue;
+          uint32_t r[2];
+          pair_words((uint32_t)j >> 1, step, ant, key, r);
+          const double s = log(v) * inv_gamma + log((double)bits_to_uniform(r[j & 1]));
+          if (s > fbest) fbest = s, bj = j;
+        }
+      }
+      if (bj < 0) {
+        if (seen[0]) return 2;
+        bj = 0;
+      }
+    }
+    seen[bj] = 1;
+    tour[step] = bj;
+    cur = (uint32_t)bj;
+  }
+  return 0;
+}
+
+/* Tours of the given global ant ids.  Returns 0, or 2 and the first failing
+ * row index in *fail_row.  fb_a may be NULL (no fallback source). */
+int fpo_build_tours(const float *w, int n, int ldw, uint64_t seed, uint32_t iteration, const int64_t *ants,
+                    int count, const double *fb_a, double fb_alpha, const double *fb_b, double inv_gamma,
+                    int32_t *tours_out, int64_t *fallbacks, int *fail_row) {
+  const uint32_t key = fpo_seed_hash32(seed) + iteration;
+  int rc = 0;
+  int64_t fb_total = 0;
+  *fail_row = -1;
+#pragma omp parallel reduction(+ : fb_total)
+  {
+    uint8_t *seen = (uint8_t *)malloc((size_t)n);
+#pragma omp for schedule(dynamic, 1)
+    for (int a = 0; a < count; ++a) {
+      int64_t fb = 0;
+      const int r = one_tour(w, n, ldw, key, (uint32_t)ants[a], fb_a, fb_alpha, fb_b, inv_gamma,
+                             tours_out + (size_t)a * n, seen, &fb);
+      fb_total += fb;
+      if (r != 0) {
+#pragma omp critical
+        {
+          if (rc == 0 || a < *fail_row) *fail_row = a;
+          rc = r;
+        }
+      }
+    }
+    free(seen);
+  }
+  if (fallbacks) *fallbacks = fb_total;
+  return rc;
+}
+
+/* Selection-level agreement along given tours (the device's): at every step
+ * of every ant, with the ant's current city and visited set, compare the
+ * recorded choice with
+ *   [0] the product rule restated here (must agree everywhere),
+ *   [1] the reference's log-domain rule log(P)/gamma + log(u) on the SAME
+ *       23-bit uniforms, logw = log(P)/gamma as numpy computes it and
+ *       log(u_k) from `logu_table` (numpy's log of the 2^23 values),
+ *   [2] the log rule on REFINED uniforms u53 = (k + f) 2^-23, f a 53-bit
+ *       fraction from an independent Philox stream (key ^ 0xA5A5A5A5): the
+ *       same bin as u, so [2] measures what the 23-bit grid and fp32 W cost
+ *       against a ~53-bit-resolution rule like the reference's (E from
+ *       numpy's 53-bit ziggurat).
+ * out[0] = selections compared, out[1..3] = mismatches of [0], [1], [2];
+ * out[4] = steps of [2] where the refined winner had W below 2^-24 of the
+ * recorded winner's W (the uniform floor's truncation). */
+void fpo_count_mismatches(const float *w, int n, int ldw, const double *logw, const double *logu_table,
+                          uint64_t seed, uint32_t iteration, const int64_t *ants, int count,
+                          const int32_t *tours, int64_t *out) {
+  const uint32_t key = fpo_seed_hash32(seed) + iteration;
+  const uint32_t key2 = key ^ 0xA5A5A5A5u;
+  int64_t sel = 0, mm_prod = 0, mm_log = 0, mm_ref = 0, trunc = 0;
+#pragma omp parallel reduction(+ : sel, mm_prod, mm_log, mm_ref, trunc)
+  {
+    uint8_t *seen = (uint8_t *)malloc((size_t)n);
+#pragma omp for schedule(dynamic, 1)
+    for (int a = 0; a < count; ++a) {
+      const uint32_t ant = (uint32_t)ants[a];
+      const int32_t *tour = tours + (size_t)a * n;
+      memset(seen, 0, (size_t)n);
+      uint32_t cur = (uint32_t)tour[0];
+      seen[cur] = 1;
+      for (uint32_t step = 1; step < (uint32_t)n; ++step) {
+        const float *row = w + (size_t)cur * ldw;
+        const double *lrow = logw + (size_t)cur * n;
+        float pbest = -1.0f;
+        int pj = -1, lj = 0, rj = 0; /* numpy: an all -inf row's argmax is 0 */
+        double lbest = -INFINITY, rbest = -INFINITY;
+        for (int q = 0; 2 * q < n; ++q) {
+          uint32_t r[2], f[2];
+          int any = 0;
+          for (int e = 0; e < 2; ++e) any |= (2 * q + e < n) && !seen[2 * q + e];
+          if (!any) continue;
+          pair_words((uint32_t)q, step, ant, key, r);
+          for (int e = 0; e < 2; ++e) {
+            const int j = 2 * q + e;
+            if (j >= n || seen[j]) continue;
+            if (row[j] > 0.0f) {
+              const float s = row[j] * bits_to_uniform(r[e]);
+              if (s > pbest) pbest = s, pj = j;
+            }
+            const double ls = lrow[j] + logu_table[r[e] >> 9];
+            if (ls > lbest) lbest = ls, lj = j;
+            /* refined uniform: same bin (k = x >> 9), 53-bit position inside it */
+            philox2x32_10(ant ^ 0x80000000u, (uint32_t)j | (step << 16), key2, f);
+            const uint64_t frac = (((uint64_t)f[0] << 32) | f[1]) >> 11;
+            const double u53 = ((double)(r[e] >> 9) + (double)frac * 0x1p-53) * 0x1p-23;
+            const double rs = lrow[j] + log(u53 > 0.0 ? u53 : 0x1p-80);
+            if (rs > rbest) rbest = rs, rj = j;
+          }
+        }
+        const int got = tour[step];
+        ++sel;
+        mm_prod += (pj >= 0 ? pj : got) != got;
+        mm_log += lj != got;
+        if (rj != got) {
+          ++mm_ref;
+          if (row[rj] < row[got] * 0x1p-24f) ++trunc;
+        }
+        seen[got] = 1;
+        cur = (uint32_t)got;
+      }
+    }
+    free(seen);
+  }
+  out[0] = sel;
+  out[1] = mm_prod;
+  out[2] = mm_log;
+  out[3] = mm_ref;
+  out[4] = trunc;
+}

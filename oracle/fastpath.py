@@ -116,19 +116,40 @@ def rw_tours(p: np.ndarray, seed: int, iteration: int, ants) -> np.ndarray:
 
 
 def selection_table(p: np.ndarray, g: float) -> np.ndarray:
-    """W = fp32(P^(1/g)) as the device builds it: exact conversion for g == 1,
-    else fp32(exp2(log2(P)/g)) in f64 (k_row_update.cu selection_weight).
+    """W = fp32(2^-e_i P^(1/g)) as the device builds it (taco_common.cuh
+    selection_weight): P^(1/g) is the exact value for g == 1, else
+    exp2(log2(P)/g) in f64; e_i = ilogb of row i's largest P^(1/g), so the
+    row maximum lands in [1, 2); entries below FLT_MIN after scaling are 0.
     numpy's log2/exp2 may differ from CUDA's by an ulp before the fp32
     rounding, so parity tests feed the device-built W to `build_tours`."""
-    if g == 1.0:
-        return p.astype(np.float32)
+    p = np.asarray(p, dtype=np.float64)
     with np.errstate(divide="ignore"):
-        return np.exp2((1.0 / g) * np.log2(p)).astype(np.float32)
+        x = p.copy() if g == 1.0 else np.exp2((1.0 / g) * np.log2(p))
+        pmax = p.max(axis=1)
+        xmax = pmax if g == 1.0 else np.exp2((1.0 / g) * np.log2(pmax))
+    e = np.where((xmax > 0) & np.isfinite(xmax), np.frexp(xmax)[1] - 1, 0)
+    e = np.clip(e, -1000, 1000)
+    w = (x * np.ldexp(1.0, -e)[:, None]).astype(np.float32)
+    w[w < np.float32(2.0**-126)] = 0.0
+    return w
 
 
-def build_tours(w: np.ndarray, seed: int, iteration: int, ants) -> np.ndarray:
+def _fallback_value(a: np.ndarray, alpha: float, b) -> np.ndarray:
+    """v = A^alpha (* B) with numpy's scalar-power dispatch (the kernels'
+    numpy_scalar_power)."""
+    v = a if alpha == 1.0 else (a * a if alpha == 2.0 else np.power(a, alpha))
+    return v if b is None else v * b
+
+
+def build_tours(w: np.ndarray, seed: int, iteration: int, ants, fallback=None, inv_gamma: float = 1.0) -> np.ndarray:
     """Full-scan product-form construction for the given global ant ids:
-    next = argmax_j W[cur, j] * u over unvisited j with W > 0, first of ties."""
+    next = argmax_j W[cur, j] * u over unvisited j with W > 0, first of ties.
+
+    No W > 0 candidate left: argmax over unvisited j with v_j > 0 of
+    log(v_j) * inv_gamma + log(u_j) in f64, v = A[cur]^alpha (* B[cur]) with
+    fallback = (A, alpha, B or None); none either (or no source): city 0
+    when unvisited — numpy's argmax of an all -inf row (selection.py:152-155)
+    — else the reference's assertion (colony.py:149)."""
     n = w.shape[0]
     ants = np.asarray(ants, dtype=np.int64)
     a = ants.size
@@ -141,12 +162,26 @@ def build_tours(w: np.ndarray, seed: int, iteration: int, ants) -> np.ndarray:
     cities = np.arange(n, dtype=np.uint64)
     for step in range(1, n):
         u = uniforms(seed, iteration, step, ants[:, None], cities[None, :])
-        wr = w[cur]
+        wr = w[cur][:, :n]
         score = wr * u  # float32 x float32, round to nearest
         score[seen | (wr <= 0)] = np.float32(-1.0)
         nxt = score.argmax(axis=1)
-        if (score[rows, nxt] < 0).any():
-            raise AssertionError("selector chose a visited city")
+        for r in np.flatnonzero(score[rows, nxt] < 0):  # no W > 0 candidate
+            pick = -1
+            if fallback is not None:
+                v = _fallback_value(fallback[0][cur[r]], fallback[1],
+                                    None if fallback[2] is None else fallback[2][cur[r]])
+                ok = ~seen[r] & (v > 0)
+                if ok.any():
+                    with np.errstate(divide="ignore"):
+                        s = np.log(v) * inv_gamma + np.log(u[r].astype(np.float64))
+                    s[~ok] = -np.inf
+                    pick = int(s.argmax())
+            if pick < 0:
+                if seen[r, 0]:
+                    raise AssertionError("selector chose a visited city")
+                pick = 0
+            nxt[r] = pick
         seen[rows, nxt] = True
         tours[:, step] = nxt
         cur = nxt

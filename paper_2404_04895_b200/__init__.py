@@ -42,7 +42,7 @@ from .pheromone import (
     increment_matrix,
     select_elite,
 )
-from .selection import AllZeroWeights, gamma_at, scaled_log_weights
+from .selection import AllZeroWeights, argmax_select_block, gamma_at, scaled_log_weights
 from .solver import Solver
 from ._device import DeviceInstance, UnsupportedEdgeWeightType, device_build_instance
 
@@ -55,7 +55,7 @@ __all__ = [
     "NumericalUnderflow", "PheromoneState", "ProbabilityMatrix", "Selection", "Solver", "TAU_MIN",
     "TourBatch", "TspInstance", "accumulate_increments", "apply_update", "batch_costs",
     "compute_probability_matrix", "construct_tours", "edge_index_matrix", "euclidean_instance",
-    "gamma_at", "increment_matrix", "init_starts", "instance_from_distances", "scaled_log_weights",
+    "gamma_at", "argmax_select_block", "increment_matrix", "init_starts", "instance_from_distances", "scaled_log_weights",
     "select_elite", "tour_cost", "DeviceInstance", "device_euclidean_instance",
     "device_build_instance", "UnsupportedEdgeWeightType",
 ]

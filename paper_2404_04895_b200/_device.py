@@ -227,12 +227,18 @@ def selection_table_from_p(p: torch.Tensor, inv_gamma: float, tables: SelectionT
 def construct(n: int, m_local: int, ant_offset: int, variant: int, tables: SelectionTables,
               seed: int, iteration: int, tours_out: torch.Tensor, status: torch.Tensor,
               scan_count: torch.Tensor | None = None, dist: torch.Tensor | None = None,
-              costs_out: torch.Tensor | None = None, state: torch.Tensor | None = None) -> None:
-    """Build tours (and, with dist + costs_out, their lengths) on the device."""
+              costs_out: torch.Tensor | None = None, state: torch.Tensor | None = None,
+              fallback: tuple | None = None, inv_gamma: float = 1.0) -> None:
+    """Build tours (and, with dist + costs_out, their lengths) on the device.
+
+    fallback: (A, alpha, B or None) device f64 (n, n) tensors, the source of
+    the f64 decision when no W > 0 candidate is left (include/taco.h); None:
+    only the all -inf rule (city 0 when unvisited)."""
+    fb_a, fb_alpha, fb_b = fallback if fallback is not None else (None, 1.0, None)
     code = _lib.load().taco_construct(
         n, m_local, ant_offset, variant, ptr(tables.w), tables.ldw, ptr(tables.sw), ptr(tables.si),
         int(seed), int(iteration) & 0xFFFFFFFF, ptr(dist), ptr(tours_out), ptr(costs_out), ptr(status),
-        ptr(scan_count), ptr(state), stream_handle())
+        ptr(scan_count), ptr(fb_a), float(fb_alpha), ptr(fb_b), float(inv_gamma), ptr(state), stream_handle())
     check(code, "taco_construct")
 
 

@@ -51,11 +51,13 @@ SIGNATURES = {
     "taco_selection_table": (_c_int, [_c_int, _p, _c_f64, _p, _c_int, _p, _p, _p]),
     "taco_eta_power": (_c_int, [_c_i64, _p, _c_f64, _p, _p]),
     "taco_construct": (_c_int, [
-        _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p, _p, _p]),
+        _c_int, _c_int, _c_int, _c_int, _p, _c_int, _p, _p, _c_u64, _c_u32, _p, _p, _p, _p, _p,
+        _p, _c_f64, _p, _c_f64, _p, _p]),
     "taco_starts": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u32, _p, _p]),
     "taco_uniforms": (_c_int, [_c_int, _p, _p, _p, _c_u64, _c_u32, _p, _p]),
     "taco_philox2x32_10": (_c_int, [_c_int, _p, _p, _p, _p]),
     "taco_select_parity": (_c_int, [_c_int, _c_int, _c_int, _p, _p, _p, _p, _p, _p, _p]),
+    "taco_argmax_select_block": (_c_int, [_c_int, _c_int, _p, _p, _p, _p, _p, _p, _p]),
     "taco_replay_workspace_bytes": (_c_size, [_c_int, _c_int]),
     "taco_select_replay": (_c_int, [_c_int, _c_int, _c_int, _c_u64, _c_u64, _p, _p, _p, _p, _p, _c_size, _p, _p,
                                     _p]),
@@ -70,12 +72,12 @@ SIGNATURES = {
     "taco_elite_workspace_bytes": (_c_size, [_c_int]),
     "taco_elite_order": (_c_int, [_c_int, _p, _p, _p, _c_size, _p]),
     "taco_elite_neighbors": (_c_int, [_c_int, _c_int, _p, _c_int, _p, _p, _p, _p, _p]),
-    "taco_track_best": (_c_int, [_c_int, _p, _p, _p, _p, _p, _p, _c_u32, _p, _p]),
+    "taco_track_best": (_c_int, [_c_int, _p, _p, _p, _p, _p, _p, _c_u32, _p, _p, _p]),
     "taco_iter_advance": (_c_int, [_p, _p, _c_int, _p]),
     "taco_shard_elites": (_c_int, [_c_int, _c_int, _p, _c_int, _c_int, _p, _p, _p, _p, _p]),
 }
 
-ABI_VERSION = 3
+ABI_VERSION = 4
 
 
 class TacoLibraryMissing(ImportError):

@@ -144,7 +144,9 @@ def _construct_device_stream(p_host, n, m, seed, iteration, gamma, dev, variant,
     costs = torch.empty(m, dtype=torch.float64, device=dev)
     status = _device.new_status(dev)
     code = _lib.CONSTRUCT_SORTED if variant == "sorted" else _lib.CONSTRUCT_DENSE
-    _device.construct(n, m, 0, code, tables, seed, iteration, tours, status, dist=dist, costs_out=costs)
+    # f64 fallback source when no W > 0 candidate is left: P itself
+    _device.construct(n, m, 0, code, tables, seed, iteration, tours, status, dist=dist, costs_out=costs,
+                      fallback=(p_t, 1.0, None), inv_gamma=1.0 / gamma)
     _raise_construct_status(status)
     return tours, costs
 

@@ -98,6 +98,64 @@ __device__ __forceinline__ double warp_tour_cost(int n, const int32_t *trow, con
   return pw_fold(n, ls);  // meaningful in lane 0
 }
 
+// ---------------------------------------------------------------------------
+// No W > 0 candidate left.  The reference keeps choosing in the log domain
+// among every unvisited city with P > 0 (selection.py:143-155), however small
+// P^(1/gamma) is; W can be 0 where fp32 cannot hold the ratio to the row's
+// best (taco_common.cuh selection_weight: below 2^-126 of it, e.g. gamma < 1).
+// The fallback scores those cities in f64, log(v_j) / gamma + log(u_j) with
+// v = A[cur, j]^alpha (* B[cur, j]) — P itself, or the row's unnormalized
+// tau^alpha eta^beta (same argmax up to rounding: log of the row sum is a
+// shared shift) — on the same uniforms u_j, first of ties.  Nothing with
+// v > 0 either: numpy's argmax of an all -inf row is city 0 (selection.py:
+// 152-155), which is taken when unvisited; otherwise the reference asserts
+// (colony.py:149) and 0xffffffff is returned.  Rare (never seen with
+// gamma >= 1 on the BASELINE configs), so it is a plain strided scan.
+// ---------------------------------------------------------------------------
+struct Fallback {
+  const double *a;  // n x n, row pitch n (nullable: only the all -inf rule)
+  const double *b;  // nullable multiplier
+  double alpha;
+  double inv_gamma;
+};
+
+// the iteration's 1/gamma from the device state when given (graph replay)
+__device__ __forceinline__ Fallback fallback_of(const Fallback &f, const taco_iter_state *state) {
+  Fallback r = f;
+  if (state != nullptr) r.inv_gamma = state->inv_gamma_cur;
+  return r;
+}
+
+// G lanes (gl = lane index in the group) pick for one ant; every lane of the
+// warp must call (shuffles), `active` marks groups that need the pick.
+template <int G, class Visited>
+__device__ __forceinline__ uint32_t fallback_pick(const Fallback &f, uint32_t n, uint32_t cur, uint32_t step,
+                                               const AntKey &ak, const RoundKeys &rk, int gl, bool active,
+                                               Visited visited) {
+  double best = -INFINITY;
+  uint32_t bj = 0xffffffffu;
+  if (active && f.a != nullptr) {
+    for (uint32_t j = (uint32_t)gl; j < n; j += G) {
+      if (visited(j)) continue;
+      const size_t off = (size_t)cur * n + j;
+      double v = numpy_scalar_power(f.a[off], f.alpha);
+      if (f.b != nullptr) v = __dmul_rn(v, f.b[off]);
+      if (!(v > 0.0)) continue;
+      const double u = (double)bits_to_uniform(sel_word(j, step, ak, rk));
+      const double sc = __dadd_rn(__dmul_rn(log(v), f.inv_gamma), log(u));
+      if (sc > best || bj == 0xffffffffu) best = sc, bj = j;
+    }
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) {
+    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const uint32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+    if (oj != 0xffffffffu && (bj == 0xffffffffu || ob > best || (ob == best && oj < bj))) best = ob, bj = oj;
+  }
+  if (active && bj == 0xffffffffu && !visited(0u)) bj = 0;
+  return bj;
+}
+
 // per-ant shared scratch: leaf buffer, leaf sums, visited bitmask (16-B aligned)
 __host__ __device__ __forceinline__ size_t ant_scratch_bytes(int n_leaves, int nwords) {
   return ((size_t)8 * kPwBlock + (size_t)8 * n_leaves + (size_t)4 * nwords + 15) & ~(size_t)15;
@@ -110,16 +168,7 @@ __device__ __forceinline__ bool is_visited(const uint32_t *vis, uint32_t j) {
 }  // namespace taco
 
 
-static inline int sm_count() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
-      cached = 148;
-  }
-  return cached;
-}
+static inline int sm_count() { return taco::device_sm_count(); }
 
 static inline int set_smem(const void *fn, size_t bytes) {
   if (bytes <= 48 * 1024) return TACO_OK;

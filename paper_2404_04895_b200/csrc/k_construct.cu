@@ -44,6 +44,7 @@ struct SortedArgs {
   int32_t *status;
   unsigned long long *scan_count;
   PhiloxKeys ks;
+  Fallback fb;  // no W > 0 candidate left (construct_common.cuh)
 };
 
 constexpr int kSortedMaxWarps = 28;      // fused tour length: 72 registers per thread
@@ -238,9 +239,13 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
 #ifdef TACO_STEP_PROFILE
     const long long t2 = clock64();
 #endif
-    if (bestj == 0xffffffffu) {
-      if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
-      return;
+    if (bestj == 0xffffffffu) {  // no W > 0 candidate: f64 fallback / all -inf rule
+      bestj = fallback_pick<32>(fallback_of(a.fb, a.state), un, cur, step, ak, rk, lane, true,
+                                [&](uint32_t j) { return visited_at<VIS8>(vis, j); });
+      if (bestj == 0xffffffffu) {
+        if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
+        return;
+      }
     }
     // next row's first window: issued before this step's bookkeeping
     {
@@ -309,6 +314,7 @@ struct GroupArgs {
   int32_t *status;
   unsigned long long *scan_count;  // optional traffic probe (32-entry windows)
   PhiloxKeys ks;
+  Fallback fb;
 };
 
 
@@ -420,6 +426,13 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
     chunk += CH;
     const bool step_done = alive && ((bucket_ceiling(wl) < best) || (wl <= 0.0f) || (chunk >= un));
 
+    // ---- no W > 0 candidate: f64 fallback / all -inf rule (whole warp) -----
+    const bool need_fb = step_done && bestj == 0xffffffffu;
+    if (__any_sync(kFull, need_fb)) {
+      const uint32_t fj = fallback_pick<G>(fallback_of(a.fb, a.state), un, cur, step, ak, rk, gl, need_fb,
+                                           [&](uint32_t j) { return ((vis[(j >> 5) * A + g] >> (j & 31)) & 1u) != 0; });
+      if (need_fb) bestj = fj;
+    }
     // ---- groups whose step is decided move to the next city ----------------
     if (step_done) {
       if (bestj == 0xffffffffu) {
@@ -467,6 +480,7 @@ struct DenseArgs {
   double *costs;
   int32_t *status;
   PhiloxKeys ks;
+  Fallback fb;
 };
 
 // Shared memory: int2 leaves[n_leaves]; per ant: double leaf_buf[kPwBlock],
@@ -544,11 +558,17 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
       wkey = __reduce_max_sync(kFull, lkey);
     }
     const uint32_t mkey = __reduce_max_sync(kFull, lkey);
-    if (mkey == 0u) {
-      if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
-      return;
+    uint32_t bestj;
+    if (mkey == 0u) {  // no W > 0 candidate: f64 fallback / all -inf rule
+      bestj = fallback_pick<32>(fallback_of(a.fb, a.state), (uint32_t)n, cur, (uint32_t)step, ak, rk, lane, true,
+                                [&](uint32_t j) { return is_visited(vis, j); });
+      if (bestj == 0xffffffffu) {
+        if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
+        return;
+      }
+    } else {
+      bestj = __reduce_min_sync(kFull, lkey == mkey ? lj : 0xffffffffu);
     }
-    const uint32_t bestj = __reduce_min_sync(kFull, lkey == mkey ? lj : 0xffffffffu);
     if (lane == 0) vis[bestj >> 5] |= 1u << (bestj & 31);
     if (step > 1) lc.push();
     lc.load(cur, bestj);
@@ -631,9 +651,55 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
 }
 
+// argmax_select_block (selection.py:143-155) as its own drop-in: scores =
+// take(logw, current) - e_block, visited := -inf, row argmax (first of ties,
+// an all -inf row gives 0).  No visited update and no assertion: those belong
+// to construct_tours (colony.py:149-152).
+template <int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    k_argmax_block(int n, int m, const double *__restrict__ logw, const int64_t *__restrict__ current,
+                   const double *__restrict__ e_block, const uint8_t *__restrict__ visited, double *scores,
+                   int64_t *next_out) {
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  const int a = blockIdx.x * WARPS + warp;
+  if (a >= m) return;
+  const double *lr = logw + (size_t)current[a] * n;
+  const double *er = e_block + (size_t)a * n;
+  const uint8_t *vr = visited + (size_t)a * n;
+  double best = -INFINITY;
+  int bj = 0x7fffffff;
+  for (int j = lane; j < n; j += 32) {
+    const double s = vr[j] ? -INFINITY : __dsub_rn(lr[j], er[j]);
+    if (scores != nullptr) scores[(size_t)a * n + j] = s;
+    if (s > best) best = s, bj = j;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+    const double ob = __shfl_xor_sync(kFull, best, off);
+    const int oj = __shfl_xor_sync(kFull, bj, off);
+    if (ob > best || (ob == best && oj < bj)) best = ob, bj = oj;
+  }
+  if (lane == 0) next_out[a] = bj == 0x7fffffff ? 0 : bj;
+}
+
 }  // namespace taco
 
 using namespace taco;
+
+extern "C" int taco_argmax_select_block(int n, int m, const double *logw, const int64_t *current,
+                                        const double *e_block, const uint8_t *visited, double *scores_out,
+                                        int64_t *next_out, void *stream) {
+  if (n < 1 || m < 0 || (m > 0 && (logw == nullptr || current == nullptr || e_block == nullptr ||
+                                   visited == nullptr || next_out == nullptr)))
+    return TACO_ERR_ARG;
+  if (m == 0) return TACO_OK;
+  constexpr int WARPS = 8;
+  k_argmax_block<WARPS><<<(m + WARPS - 1) / WARPS, WARPS * 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      n, m, logw, current, e_block, visited, scores_out, next_out);
+  TACO_CUDA_CHECK_LAUNCH();
+  return TACO_OK;
+}
 
 
 template <bool PROBE, bool VIS8, int MODE>
@@ -646,8 +712,11 @@ static int launch_sorted(const SortedArgs &a, int grid, int threads, size_t smem
 extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, const float *w, int ldw,
                               const float *sw, const uint16_t *si, uint64_t seed, uint32_t iteration,
                               const double *dist, int32_t *tours_out, double *costs_out, int32_t *status,
-                              unsigned long long *scan_count, const taco_iter_state *state, void *stream) {
+                              unsigned long long *scan_count, const double *fb_a, double fb_alpha,
+                              const double *fb_b, double inv_gamma, const taco_iter_state *state, void *stream) {
   if (n < 3 || n > 65535 || m_local < 0 || ant_offset < 0 || tours_out == nullptr) return TACO_ERR_ARG;
+  if (fb_b != nullptr && fb_a == nullptr) return TACO_ERR_ARG;
+  const Fallback fb{fb_a, fb_b, fb_alpha, inv_gamma};
   if (costs_out != nullptr && dist == nullptr) return TACO_ERR_ARG;
   if (m_local == 0) return TACO_OK;
   const PhiloxKeys ks = philox_keys(seed);
@@ -683,7 +752,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
       const size_t smem = leaves_bytes + per_warp * kGroupWarps;
       if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
       GroupArgs ga{n, m_local, ant_offset, nwords, n_leaves, ldw, sw, si, dist, iteration, state,
-                   tours_out, costs_out, status, scan_count, ks};
+                   tours_out, costs_out, status, scan_count, ks, fb};
       const int ants_per_cta = (int)A * kGroupWarps;
       const int grid = (m_local + ants_per_cta - 1) / ants_per_cta;
 #define TACO_GROUP_CASE(GG, EE)                                                                         \
@@ -744,7 +813,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     const size_t smem = lb + scratch(vis8 ? nwords8 : nwords) * warps;
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
     SortedArgs a{n, m_local, ant_offset, vis8 ? nwords8 : nwords, n_leaves, ldw, sw, si, dist, iteration, state,
-                 tours_out, separate_cost ? nullptr : costs_out, status, scan_count, ks};
+                 tours_out, separate_cost ? nullptr : costs_out, status, scan_count, ks, fb};
     const int grid = (m_local + warps - 1) / warps;
     const int mode = fused_cost ? 0 : (ants_per_sm > max_warps ? 2 : 1);
     const int code = mode * 4 + (vis8 ? 2 : 0) + (scan_count ? 1 : 0);
@@ -768,7 +837,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
     if (set_smem((const void *)k_construct_dense<WARPS>, smem) != TACO_OK) return TACO_ERR_CUDA;
     DenseArgs a{n, m_local, ant_offset, ldw, nwords, n_leaves, w, dist, iteration, state, tours_out, costs_out,
-                status, ks};
+                status, ks, fb};
     k_construct_dense<WARPS><<<(m_local + WARPS - 1) / WARPS, WARPS * 32, smem, s>>>(a);
   } else {
     return TACO_ERR_ARG;

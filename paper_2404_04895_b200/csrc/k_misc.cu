@@ -112,9 +112,10 @@ __global__ void k_shard_elites(int n, int k, const int32_t *__restrict__ order, 
 
 __global__ void k_track_best(int n, const int32_t *tours, const double *costs, const int32_t *order,
                              double *best_cost, int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
-                             const taco_iter_state *state) {
+                             const int32_t *status, const taco_iter_state *state) {
   __shared__ int s_take;
   __shared__ int s_ant;
+  if (chain_stopped_update(status)) return;  // a failed construction: no best from its rows
   if (threadIdx.x == 0) {
     const int a = order[0];
     const double c = costs[a];
@@ -302,10 +303,10 @@ extern "C" int taco_shard_elites(int n, int k, const int32_t *order, int ant_off
 
 extern "C" int taco_track_best(int n, const int32_t *tours, const double *costs, const int32_t *order,
                                double *best_cost, int32_t *best_tour, int32_t *best_iter, uint32_t iteration,
-                               const taco_iter_state *state, void *stream) {
+                               const int32_t *status, const taco_iter_state *state, void *stream) {
   if (n < 1) return TACO_ERR_ARG;
   k_track_best<<<1, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(n, tours, costs, order, best_cost,
-                                                                      best_tour, best_iter, iteration, state);
+                                                                      best_tour, best_iter, iteration, status, state);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }
@@ -324,6 +325,7 @@ namespace taco {
 __global__ void k_iter_advance(taco_iter_state *state, const double *inv_gamma_table, int period) {
   const uint32_t next = state->iteration + 1u;
   state->iteration = next;
+  state->inv_gamma_cur = state->inv_gamma;
   state->inv_gamma = inv_gamma_table[(next + 1u) % (uint32_t)period];
 }
 }  // namespace taco

@@ -48,27 +48,6 @@ struct RowParams {
 constexpr int kDepositChunk = 512;  // elites staged in shared memory per pass
 constexpr int kBatch = 4;           // tau / eta^b loads in flight per thread
 
-// np.power(x, e) for a scalar float exponent: numpy dispatches e in
-// {-1, 0, 0.5, 1, 2} to reciprocal / ones / sqrt / copy / square (bit-exact
-// here); any other exponent uses pow (<= 1 ulp from numpy's SIMD pow).
-__device__ __forceinline__ double numpy_scalar_power(double x, double e) {
-  if (e == 1.0) return x;
-  if (e == 2.0) return __dmul_rn(x, x);
-  if (e == 0.0) return 1.0;
-  if (e == 0.5) return __dsqrt_rn(x);
-  if (e == -1.0) return __ddiv_rn(1.0, x);
-  return pow(x, e);
-}
-
-__device__ __forceinline__ float selection_weight(double p, double inv_gamma) {
-  // W = P^(1/gamma) rounded once to fp32; gamma == 1 is the exact conversion.
-  // exp2(log2(p) / gamma) in f64 is within ~2^-47 of the exact power, so the
-  // fp32 rounding equals that of a correctly rounded pow except for ~1 entry
-  // in 10^7 (one fp32 ulp); it costs 12 us instead of 35 at C3 (365 vs 737 us
-  // at n = 10000).  p = 0 gives log2 = -inf and W = 0.
-  return inv_gamma == 1.0 ? __double2float_rn(p) : __double2float_rn(exp2(inv_gamma * log2(p)));
-}
-
 // Shared-memory layout (bytes, all regions 16-B aligned):
 //   row      double[n]        delta, then unnorm (also the CUB sort workspace)
 //   plan     leaves int2[L], left/right/order u16[L], level_start int[42],
@@ -116,6 +95,7 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
   int2 *nb_stage = reinterpret_cast<int2 *>(smem + lay.stage_off);
   double *inc_stage = reinterpret_cast<double *>(nb_stage + kDepositChunk);
   __shared__ int s_meta[4];  // n_leaves, n_internal, height of the plan; fail-stop flag
+  __shared__ double s_wmax[BLOCK / 32];  // per-warp row maxima (selection-table scale)
 
   const int n = a.n;
   const int tid = threadIdx.x;
@@ -216,6 +196,7 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
     }
 
     // ---- tau' and unnormalized weights ---------------------------------------
+    double lmax = 0.0;  // the row's largest unnormalized weight (P in selection-table mode)
     for (int jb = tid; jb < n; jb += kBatch * BLOCK) {
       if (jb != tid) load_batch(jb);
 #pragma unroll
@@ -231,10 +212,12 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
         if (a.tau_out != nullptr) a.tau_out[rowoff + j] = t;
         if (a.p_given) {
           row[j] = t;
+          lmax = fmax(lmax, t);
         } else if (a.want_p) {
           double v = __dmul_rn(numpy_scalar_power(t, a.alpha), eq[u]);
           if (j == i) v = 0.0;  // np.fill_diagonal(unnorm, 0.0)
           row[j] = v;
+          lmax = fmax(lmax, v);
         }
       }
     }
@@ -242,6 +225,9 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
       __syncthreads();
       continue;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) lmax = fmax(lmax, __shfl_xor_sync(0xffffffffu, lmax, o));
+    if (lane == 0) s_wmax[tid >> 5] = lmax;
     __syncthreads();
 
     // ---- pairwise row sum (numpy order): parallel leaves, parallel fold ----
@@ -262,10 +248,16 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
 
     // ---- dense outputs (coalesced, striped) ---------------------------------
     if (a.p_out != nullptr || a.w_out != nullptr) {
+      // the row's largest P = (largest unnormalized weight) / sum: division
+      // is monotone, so this is exactly max_j P[i, j]
+      double rmax = s_wmax[0];
+#pragma unroll
+      for (int q = 1; q < BLOCK / 32; ++q) rmax = fmax(rmax, s_wmax[q]);
+      const double scale = a.w_out != nullptr ? selection_scale(__ddiv_rn(rmax, s), inv_gamma) : 1.0;
       for (int j = tid; j < n; j += BLOCK) {
         const double p = __ddiv_rn(row[j], s);
         if (a.p_out != nullptr) a.p_out[rowoff + j] = p;
-        if (a.w_out != nullptr) a.w_out[(size_t)i * a.ldw + j] = selection_weight(p, inv_gamma);
+        if (a.w_out != nullptr) a.w_out[(size_t)i * a.ldw + j] = selection_weight(p, inv_gamma, scale);
       }
       if (a.w_out != nullptr)
         for (int j = n + tid; j < a.ldw; j += BLOCK) a.w_out[(size_t)i * a.ldw + j] = 0.0f;
@@ -275,22 +267,17 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
   }
 }
 
-static int sm_count_row() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
-      cached = 148;
-  }
-  return cached;
-}
+static int sm_count_row() { return device_sm_count(); }
 
 template <int BLOCK>
 static int launch_row_t(const RowParams &a, const RowLayout &lay, cudaStream_t stream) {
-  static size_t configured = 0;
-  static int blocks_per_sm = 0;
-  static size_t blocks_for = 0;
+  // per device: the shared-memory attribute and the occupancy query
+  static size_t configured_[kMaxDevices] = {};
+  static int blocks_per_sm_[kMaxDevices] = {};
+  static size_t blocks_for_[kMaxDevices] = {};
+  const int dev = current_device();
+  size_t &configured = configured_[dev], &blocks_for = blocks_for_[dev];
+  int &blocks_per_sm = blocks_per_sm_[dev];
   if (lay.total > 48 * 1024 && lay.total > configured) {
     const cudaError_t e =
         cudaFuncSetAttribute(k_row_update<BLOCK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lay.total);
@@ -375,8 +362,11 @@ static int launch_sort_t(int n, int r0, int r1, int ldw, const float *w, float *
   using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, cub::NullType, TACO_SORT_RADIX_BITS>;
   const size_t smem = ((sizeof(typename Sort::TempStorage) + 15) & ~(size_t)15) + (size_t)4 * n;
   if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
-  static int blocks_per_sm = 0;
-  static size_t configured = 0;
+  static int blocks_per_sm_[kMaxDevices] = {};
+  static size_t configured_[kMaxDevices] = {};
+  const int dev = current_device();
+  int &blocks_per_sm = blocks_per_sm_[dev];
+  size_t &configured = configured_[dev];
   if (configured != smem) {
     if (smem > 48 * 1024) {
       const cudaError_t e =

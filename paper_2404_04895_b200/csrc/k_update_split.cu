@@ -22,16 +22,6 @@ namespace taco {
 
 constexpr unsigned kFullMask = 0xffffffffu;
 
-// numpy's np.power(x, e) for a scalar exponent (see k_row_update.cu)
-__device__ __forceinline__ double np_scalar_power(double x, double e) {
-  if (e == 1.0) return x;
-  if (e == 2.0) return __dmul_rn(x, x);
-  if (e == 0.0) return 1.0;
-  if (e == 0.5) return __dsqrt_rn(x);
-  if (e == -1.0) return __ddiv_rn(1.0, x);
-  return pow(x, e);
-}
-
 // SMEM: the warp folds into a shared-memory copy of its delta row and writes
 // it out once (short rows); otherwise the fold reads / writes global memory.
 template <int WARPS, bool SMEM>
@@ -96,7 +86,7 @@ __global__ void k_evap_unnorm(int n, const double *tau_in, double *tau_out, cons
         t = (t < 1e-12) ? 1e-12 : t;  // np.maximum(new_tau, TAU_MIN), NaN kept
         if (tau_out != nullptr) tau_out[off + j] = t;
       }
-      double v = __dmul_rn(np_scalar_power(t, alpha), eta_b[off + j]);
+      double v = __dmul_rn(numpy_scalar_power(t, alpha), eta_b[off + j]);
       if (i == j) v = 0.0;  // np.fill_diagonal(unnorm, 0.0)
       unnorm[off + j] = v;
     }
@@ -108,7 +98,7 @@ __global__ void k_evap_unnorm(int n, const double *tau_in, double *tau_out, cons
 // ((a0+a1)+(a2+a3))+((a4+a5)+(a6+a7)) by an xor butterfly (a+b == b+a, so
 // every lane of the group ends with the same bits); the len % 8 tail and
 // leaves shorter than 8 are added sequentially by the group's lane 0.
-__device__ __forceinline__ double leaf_sum8(const double *x, int len, int r) {
+__device__ __forceinline__ double leaf_sum8(const double *x, int len, int r, double &mx) {
   double acc = 0.0;
   if (len >= 8) {
     // the <= 16 elements of this accumulator are loaded before the ordered
@@ -117,6 +107,8 @@ __device__ __forceinline__ double leaf_sum8(const double *x, int len, int r) {
     double xs[kPwBlock / 8];
 #pragma unroll
     for (int q = 0; q < kPwBlock / 8; ++q) xs[q] = q < cnt ? x[8 * q + r] : 0.0;
+#pragma unroll
+    for (int q = 0; q < kPwBlock / 8; ++q) mx = fmax(mx, xs[q]);
     acc = xs[0];
 #pragma unroll
     for (int q = 1; q < kPwBlock / 8; ++q)
@@ -128,9 +120,9 @@ __device__ __forceinline__ double leaf_sum8(const double *x, int len, int r) {
   if (r == 0) {
     if (len < 8) {
       res = 0.0;
-      for (int i = 0; i < len; ++i) res = __dadd_rn(res, x[i]);
+      for (int i = 0; i < len; ++i) res = __dadd_rn(res, x[i]), mx = fmax(mx, x[i]);
     } else {
-      for (int i = len - (len % 8); i < len; ++i) res = __dadd_rn(res, x[i]);
+      for (int i = len - (len % 8); i < len; ++i) res = __dadd_rn(res, x[i]), mx = fmax(mx, x[i]);
     }
   }
   return res;
@@ -158,13 +150,16 @@ __global__ void __launch_bounds__(WARPS * 32)
   const int grp = lane >> 3, r = lane & 7;
   for (int i = blockIdx.x * WARPS + warp; i < n; i += gridDim.x * WARPS) {
     const double *row = unnorm + (size_t)i * n;
-    // leaf sums, four leaves per pass (eight lanes each)
+    // leaf sums, four leaves per pass (eight lanes each), and the row maximum
+    double mx = 0.0;
     for (int q0 = 0; q0 < n_leaves; q0 += 4) {
       const int q = q0 + grp;
       const int2 lf = q < n_leaves ? leaves[q] : make_int2(0, 0);
-      const double s = leaf_sum8(row + lf.x, lf.y, r);
+      const double s = leaf_sum8(row + lf.x, lf.y, r, mx);
       if (q < n_leaves && r == 0) lsum[q] = s;
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFullMask, mx, o));
     __syncwarp();
     double sum = 0.0;
     if (lane == 0) sum = pw_fold(n, lsum);
@@ -173,14 +168,14 @@ __global__ void __launch_bounds__(WARPS * 32)
       if (rowsum_out != nullptr) rowsum_out[i] = sum;
       if (!(isfinite(sum) && sum > 0.0)) record_status(status, TACO_UNDERFLOW, i);
     }
-    // P = unnorm / sum (colony.py:69) and the selection table
+    // P = unnorm / sum (colony.py:69) and the selection table (row scale from
+    // the largest P, taco_common.cuh selection_weight)
+    const double scale = w_out != nullptr ? selection_scale(__ddiv_rn(mx, sum), inv_gamma) : 1.0;
 #pragma unroll 4
     for (int j = lane; j < n; j += 32) {
       const double p = __ddiv_rn(row[j], sum);
       if (p_out != nullptr) p_out[(size_t)i * n + j] = p;
-      if (w_out != nullptr)
-        w_out[(size_t)i * ldw + j] =
-            inv_gamma == 1.0 ? __double2float_rn(p) : __double2float_rn(exp2(inv_gamma * log2(p)));
+      if (w_out != nullptr) w_out[(size_t)i * ldw + j] = selection_weight(p, inv_gamma, scale);
     }
     if (w_out != nullptr)
       for (int j = n + lane; j < ldw; j += 32) w_out[(size_t)i * ldw + j] = 0.0f;
@@ -188,16 +183,7 @@ __global__ void __launch_bounds__(WARPS * 32)
   }
 }
 
-static int sm_count_split() {
-  static int cached = 0;
-  if (cached == 0) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess ||
-        cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || cached <= 0)
-      cached = 148;
-  }
-  return cached;
-}
+static int sm_count_split() { return device_sm_count(); }
 
 int launch_sort_table(int n, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t s);  // k_row_update.cu
 

@@ -165,6 +165,49 @@ __device__ __forceinline__ float bucket_ceiling(float w) {
   return __uint_as_float(__float_as_uint(w) | ((1u << kSortBit) - 1u));
 }
 
+// np.power(x, e) for a scalar float exponent: numpy dispatches e in
+// {-1, 0, 0.5, 1, 2} to reciprocal / ones / sqrt / copy / square (bit-exact
+// here); any other exponent uses pow (<= 1 ulp from numpy's SIMD pow).
+__device__ __forceinline__ double numpy_scalar_power(double x, double e) {
+  if (e == 1.0) return x;
+  if (e == 2.0) return __dmul_rn(x, x);
+  if (e == 0.0) return 1.0;
+  if (e == 0.5) return __dsqrt_rn(x);
+  if (e == -1.0) return __ddiv_rn(1.0, x);
+  return pow(x, e);
+}
+
+// ---------------------------------------------------------------------------
+// Selection table entry W[i, j] = fp32(2^-e_i * P[i, j]^(1/gamma)) (DESIGN.md
+// §3.1).  The per-row power-of-two scale 2^-e_i puts the row's largest entry
+// in [1, 2): a scale shared by a row leaves every step's argmax of W * u
+// unchanged (all candidates of a step come from one row, and scaling by 2^-e
+// commutes with fp32 rounding), while the row keeps 2^126 of dynamic range
+// below its maximum whatever gamma is (gamma < 1 raises P to powers > 1).
+// Entries below FLT_MIN after scaling are stored as 0: the construction
+// kernels' f64 fallback decides among them exactly if they are all that is
+// left (construct_common.cuh).  p^(1/gamma) is exp2(log2(p) / gamma) in f64:
+// within ~2^-47 of the exact power, so the fp32 rounding equals that of a
+// correctly rounded pow except for ~1 entry in 10^7 (one fp32 ulp), at a
+// third of pow's cost; gamma == 1 is the exact conversion.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double selection_power(double p, double inv_gamma) {
+  return inv_gamma == 1.0 ? p : exp2(inv_gamma * log2(p));
+}
+
+// 2^-e for the row whose largest P is pmax (e = ilogb(pmax^(1/gamma)))
+__device__ __forceinline__ double selection_scale(double pmax, double inv_gamma) {
+  const double x = selection_power(pmax, inv_gamma);
+  int e = (x > 0.0 && x <= 1.7976931348623157e308) ? ilogb(x) : 0;
+  e = e < -1000 ? -1000 : (e > 1000 ? 1000 : e);
+  return __hiloint2double((1023 - e) << 20, 0);
+}
+
+__device__ __forceinline__ float selection_weight(double p, double inv_gamma, double scale) {
+  const float w = __double2float_rn(__dmul_rn(selection_power(p, inv_gamma), scale));
+  return w < 0x1p-126f ? 0.0f : w;  // NaN kept (the row sum already failed)
+}
+
 // ---------------------------------------------------------------------------
 // status word: [0] = first failure code, [1] = smallest offending index
 // ---------------------------------------------------------------------------
@@ -188,6 +231,10 @@ __device__ __forceinline__ void record_status(int32_t *status, int code, int ind
   if (status == nullptr) return;
   atomicCAS(status, 0, code);
   atomicMin(status + 1, index);
+  // a construction failure also stops the rest of its own iteration (best
+  // tracking, deposit, evaporation, P / W): tau stays where the reference
+  // raised (colony.py:149 fires inside construct_tours)
+  if (code == TACO_NO_CANDIDATE) atomicExch(status + 3, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -407,6 +454,27 @@ __device__ inline double pw_plan_fold(const PwPlan &p, const double *leaf_sum, d
 namespace taco {
 // last CUDA error seen by a libtaco entry point (taco_last_cuda_error)
 void note_cuda_error(cudaError_t e);
+
+// Host-side caches are per device (a process may drive several GPUs).
+constexpr int kMaxDevices = 64;
+
+inline int current_device() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) dev = 0;
+  return dev;
+}
+
+// SM count of the current device (148 on B200), cached per device
+inline int device_sm_count() {
+  static int cached[kMaxDevices] = {};
+  const int dev = current_device();
+  if (cached[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+    cached[dev] = v;
+  }
+  return cached[dev];
+}
 }  // namespace taco
 
 #define TACO_CUDA_CHECK_LAUNCH()                              \

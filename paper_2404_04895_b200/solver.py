@@ -193,7 +193,12 @@ class Solver:
             self.costs_all = torch.zeros(m, dtype=torch.float64, device=dev)
             uneven = m % world != 0
             self._pad_costs = torch.zeros(world * sh.per_rank, dtype=torch.float64, device=dev) if uneven else None
-            self.elite_tours = torch.zeros((k, n), dtype=torch.int32, device=dev)
+            # the k elite tours plus one word: every rank's construction stop
+            # flag (status[3]) rides the same SUM all-reduce, so a failure on
+            # one rank skips the same iteration's update on every rank
+            self._elite_buf = torch.zeros(k * n + 1, dtype=torch.int32, device=dev)
+            self.elite_tours = self._elite_buf[:k * n].view(k, n)
+            self._stop_flag = self._elite_buf[k * n:]
             self.elite_costs = torch.zeros(k, dtype=torch.float64, device=dev)
             self._ident_k = torch.arange(k, dtype=torch.int32, device=dev)
             self._all_tours_iteration = -1  # last_batch() gathers all tours on demand
@@ -232,7 +237,7 @@ class Solver:
         self._period = period
         self._inv_gamma = torch.tensor([1.0 / construction_gamma(p, t) for t in range(period)],
                                        dtype=torch.float64, device=dev)
-        self.state = torch.zeros(16, dtype=torch.uint8, device=dev)
+        self.state = torch.zeros(32, dtype=torch.uint8, device=dev)  # taco_iter_state
         self._write_state(0)
         # default: graphs where launch overhead is a visible share of the
         # iteration (small colonies: C1 9.5k -> 16.7k it/s; at C2 the gain is 3%
@@ -282,18 +287,6 @@ class Solver:
         if self.shard.world > 1:
             self._share_status()
 
-    def _share_status(self) -> None:
-        """Make the status words identical on every rank (device-side, no host
-        sync): a failure seen by one rank's ants or rows stops every rank's next
-        construction, and every rank raises it at the same step.  One MAX
-        all-reduce of (code << 32 | INT32_MAX - row): the highest code wins,
-        then the smallest row / ant."""
-        st = self.status
-        key = st[0:1].to(torch.int64) * (1 << 32) + (_INT32_MAX - st[1:2].to(torch.int64))
-        tdist.all_reduce(key, op=tdist.ReduceOp.MAX, group=self.group)
-        st[0:1].copy_(key >> 32)
-        st[1:2].copy_(_INT32_MAX - (key & 0xFFFFFFFF))
-
     def _gather_rows(self, buf: torch.Tensor) -> None:
         gather_rows(buf, self._part, self.group)
 
@@ -304,9 +297,11 @@ class Solver:
         share_status(self.status, self.group)
 
     def _write_state(self, it: int) -> None:
-        """Device state for iteration `it`: (it, 1/gamma(it + 1))."""
+        """Device state for iteration `it`: (it, 1/gamma(it + 1), 1/gamma(it))."""
         inv = 1.0 / construction_gamma(self.params, it + 1)
-        host = torch.frombuffer(bytearray(struct.pack("<IId", it & 0xFFFFFFFF, 0, inv)), dtype=torch.uint8)
+        cur = 1.0 / construction_gamma(self.params, it)
+        host = torch.frombuffer(bytearray(struct.pack("<IIddd", it & 0xFFFFFFFF, 0, inv, cur, 0.0)),
+                                dtype=torch.uint8)
         self.state.copy_(host)
 
     def step_async(self, timers: dict | None = None, scan_count: torch.Tensor | None = None) -> None:
@@ -374,9 +369,13 @@ class Solver:
                                  dist=self.di.dist, costs_out=self.costs_local, exact_count=self.rw_exact_steps,
                                  state=st)
         else:
+            # f64 fallback source (no W > 0 candidate left): the row's
+            # tau^alpha eta^beta, current on every rank unless row-partitioned
+            fb = None if self.partitioned else (self.tau, float(p.alpha), self.eta_b)
             _device.construct(self.n, sh.count, sh.offset, self._variant, self.tables, p.seed, it,
                               self.tours_local, self.status, scan_count, dist=self.di.dist,
-                              costs_out=self.costs_local, state=st)
+                              costs_out=self.costs_local, state=st, fallback=fb,
+                              inv_gamma=1.0 / construction_gamma(p, it))
         ev.stop("construct")
         if sh.world > 1:
             gather_costs(self.costs_local, sh, self.costs_all, self.group, self._pad_costs)
@@ -386,13 +385,15 @@ class Solver:
                                              self.tours_local.data_ptr(), self.costs_all.data_ptr(),
                                              self.elite_tours.data_ptr(), self.elite_costs.data_ptr(),
                                              _device.stream_handle()), "taco_shard_elites")
-            share_elites(self.elite_tours, self.group)
+            self._stop_flag.copy_(self.status[3:4])
+            share_elites(self._elite_buf, self.group)
+            torch.maximum(self.status[3:4], self._stop_flag, out=self.status[3:4])
             tours, costs, order = self.elite_tours, self.elite_costs, self._ident_k
         else:
             tours, costs, order = self.tours_all, self.costs_all, self.order
         _lib.check(lib.taco_track_best(self.n, tours.data_ptr(), costs.data_ptr(), order.data_ptr(),
                                        self.best_cost.data_ptr(), self.best_tour.data_ptr(),
-                                       self.best_iter.data_ptr(), it & 0xFFFFFFFF, _lib.ptr(st),
+                                       self.best_iter.data_ptr(), it & 0xFFFFFFFF, self.status.data_ptr(), _lib.ptr(st),
                                        _device.stream_handle()), "taco_track_best")
         _device.elite_neighbors(tours, order, costs, p.k, self.nbr, self.inc)
         ev.start("update")

@@ -55,7 +55,10 @@ def test_bad_arguments_are_rejected_without_a_gpu(built_lib):
 
     lib = _lib.load(built_lib)
     assert lib.taco_construct(2, 1, 0, 0, None, 0, None, None, 0, 0, None, None, None, None, None,
-                              None, None) == _lib.TACO_ERR_ARG
+                              None, 1.0, None, 1.0, None, None) == _lib.TACO_ERR_ARG
+    # a fallback multiplier without its base
+    assert lib.taco_construct(10, 1, 0, 0, None, 32, None, None, 0, 0, None, 8, None, None, None,
+                              None, 1.0, 8, 1.0, None, None) == _lib.TACO_ERR_ARG
     assert lib.taco_row_update(2, None, None, None, None, None, 0, None, None, 0, 1.0, 0, 1.0, 1.0,
                                None, None, None, 0, None, None, None, None, None) == _lib.TACO_ERR_ARG
     assert lib.taco_construct_rw(3, 1, 0, None, 0, 0, None, None, None, None, None, 0, None,

@@ -158,7 +158,7 @@ def test_fast_construction_matches_restatement(n, m, gamma):
     w = t.w[:, :n].cpu().numpy()
     # the tables hold exactly fp32(P^(1/gamma)), row-sorted descending
     if gamma == 1.0:
-        assert np.array_equal(w, p.astype(np.float32))
+        assert np.array_equal(w, fastpath.selection_table(p, 1.0))
     sw, si = t.sw[:, :n].cpu().numpy(), t.si[:, :n].cpu().numpy().astype(np.int64)
     assert (t.sw[:, n:] == 0).all()  # pad columns are never selectable
     assert np.array_equal(np.take_along_axis(w, si, axis=1), sw)

@@ -226,3 +226,76 @@ def test_synthetic_coords_match_reference():
         assert np.array_equal(coords, z[f"{tag}/coords"])
         dist, eta = ref.coord_instance(coords, "EUC_2D")
         assert np.array_equal(dist, z[f"{tag}/dist"]) and np.array_equal(eta, z[f"{tag}/eta"])
+
+
+def test_c_oracle_equals_numpy_restatement():
+    """oracle/c/fastpath.c (the parity oracle at the BASELINE sizes) == the
+    numpy restatement, including the f64 fallback and the all -inf rule."""
+    from oracle import fastpath_c
+
+    g = np.random.default_rng(4)
+    for n in (3, 7, 130, 301):
+        w = g.uniform(0.0, 1.0, (n, n)).astype(np.float32)
+        np.fill_diagonal(w, 0.0)
+        w[g.uniform(size=(n, n)) < 0.1] = 0.0
+        ldw = -(-n // 32) * 32
+        padded = np.zeros((n, ldw), dtype=np.float32)
+        padded[:, :n] = w
+        src = g.uniform(0.0, 1.0, (n, n))
+        ants = np.concatenate([np.arange(9), [2**31 + 5, 2**32 - 1]])
+        for fb in (None, (src, 1.0, None), (src, 2.0, src)):
+            try:
+                want = fastpath.build_tours(w, 77, 3, ants, fallback=fb, inv_gamma=0.25)
+            except AssertionError:  # an ant left with only zero weights and city 0 visited
+                with pytest.raises(AssertionError):
+                    fastpath_c.build_tours(padded, 77, 3, ants, n=n, fallback=fb, inv_gamma=0.25)
+                continue
+            assert np.array_equal(fastpath_c.build_tours(padded, 77, 3, ants, n=n, fallback=fb, inv_gamma=0.25), want)
+    # Philox and the key schedule
+    ctr = np.array([[0, 0], [0xFFFFFFFF, 0xFFFFFFFF], [0x243F6A88, 0x85A308D3]], dtype=np.uint64)
+    key = np.array([0, 0xFFFFFFFF, 0x13198A2E], dtype=np.uint64)
+    assert np.array_equal(fastpath_c.philox2x32_10(ctr, key), fastpath.philox2x32_10(ctr, key))
+    for seed in (0, 1, 2**40 + 3, 2**64 - 1):
+        assert fastpath_c.seed_hash32(seed) == fastpath.seed_hash32(seed)
+
+
+def test_c_oracle_all_zero_rows_follow_numpy_argmax():
+    """No W > 0 and no fallback source: city 0 while unvisited (numpy's argmax
+    of an all -inf row), else the reference's assertion (colony.py:149)."""
+    from oracle import fastpath_c
+
+    n = 20
+    w = np.zeros((n, n), dtype=np.float32)
+    side = np.arange(n) >= 10
+    w[side[:, None] == side[None, :]] = 1.0
+    np.fill_diagonal(w, 0.0)
+    st = fastpath.starts(5, 0, np.arange(64), n)
+    far = np.arange(64)[side[st]]
+    near = np.arange(64)[~side[st]]
+    t = fastpath_c.build_tours(w, 5, 0, far)
+    assert (t[:, 10] == 0).all() and np.array_equal(t, fastpath.build_tours(w, 5, 0, far))
+    with pytest.raises(AssertionError):
+        fastpath_c.build_tours(w, 5, 0, near[:1])
+    with pytest.raises(AssertionError):
+        fastpath.build_tours(w, 5, 0, near[:1])
+
+
+def test_mismatch_counter_agrees_with_the_rules():
+    from oracle import fastpath_c
+
+    n = 150
+    g = np.random.default_rng(8)
+    p = g.uniform(0.0, 1.0, (n, n))
+    np.fill_diagonal(p, 0.0)
+    p /= p.sum(axis=1, keepdims=True)
+    gamma = 1.37
+    w = fastpath.selection_table(p, gamma)
+    ants = np.arange(40)
+    tours = fastpath_c.build_tours(w, 3, 2, ants).astype(np.int32)
+    c = fastpath_c.count_mismatches(w, ref.log_table(p, gamma), 3, 2, ants, tours)
+    assert c["selections"] == 40 * (n - 1) and c["product_rule"] == 0
+    # the log rule's own tours: counted against themselves, the log rule never disagrees
+    logt = fastpath.log_rule_tours(p, gamma, 3, 2, ants).astype(np.int32)
+    c2 = fastpath_c.count_mismatches(w, ref.log_table(p, gamma), 3, 2, ants, logt)
+    assert c2["log_rule_same_u"] == 0
+    assert c["log_rule_same_u"] <= 2 and c["log_rule_u53"] <= 40
