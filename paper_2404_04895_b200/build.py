@@ -13,15 +13,19 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-OUT = os.path.join(HERE, "lib", "libtaco.so")
+OUT = os.environ.get("TACO_BUILD_OUT") or os.path.join(HERE, "lib", "libtaco.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC",
+    # A/B experiments only (scripts/ab_variant.sh): extra -D flags
+    *os.environ.get("TACO_NVCC_EXTRA", "").split(),
 ]
-OBJ_DIR = os.path.join(os.path.dirname(HERE), "build", "taco_obj")
+OBJ_DIR = os.path.join(os.path.dirname(HERE), "build",
+                       "taco_obj" if not os.environ.get("TACO_BUILD_OUT") else
+                       "taco_obj_" + os.path.basename(os.environ["TACO_BUILD_OUT"]).replace(".so", ""))
 
 
 def sources() -> list[str]:

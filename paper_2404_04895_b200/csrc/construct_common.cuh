@@ -119,34 +119,38 @@ struct Fallback {
   double inv_gamma;
 };
 
-// the iteration's 1/gamma from the device state when given (graph replay)
-__device__ __forceinline__ Fallback fallback_of(const Fallback &f, const taco_iter_state *state) {
-  Fallback r = f;
-  if (state != nullptr) r.inv_gamma = state->inv_gamma_cur;
-  return r;
-}
-
 // G lanes (gl = lane index in the group) pick for one ant; every lane of the
-// warp must call (shuffles), `active` marks groups that need the pick.
-template <int G, class Visited>
-__device__ __forceinline__ uint32_t fallback_pick(const Fallback &f, uint32_t n, uint32_t cur, uint32_t step,
-                                               const AntKey &ak, const RoundKeys &rk, int gl, bool active,
-                                               Visited visited) {
+// warp must call (shuffles), `active` marks groups that need the pick.  Kept
+// out of line with scalar arguments only (keys rebuilt from the kernel
+// parameters): inlined, or given the callers' key registers by reference, it
+// raised the register pressure of the step loop it never runs in (C3
+// construction 1.57 -> 1.69 ms).  Visited set: byte per city (vis8) or bit
+// map word (j >> 5) * stride + offset.
+static __device__ __noinline__ uint32_t fallback_pick(const Fallback *f, const PhiloxKeys *ks,
+                                               const taco_iter_state *state, uint32_t it, uint32_t gant,
+                                               uint32_t n, uint32_t cur, uint32_t step, int G, int gl, int active,
+                                               const uint32_t *vis, int vis8, int stride, int offset) {
+  auto visited = [&](uint32_t j) -> bool {
+    if (vis8) return reinterpret_cast<const uint8_t *>(vis)[j] != 0;
+    return (vis[(j >> 5) * (uint32_t)stride + (uint32_t)offset] >> (j & 31)) & 1u;
+  };
+  const double inv_gamma = state != nullptr ? state->inv_gamma_cur : f->inv_gamma;
+  const RoundKeys rk = round_keys(*ks, it);
+  const AntKey ak = ant_key(gant, rk);
   double best = -INFINITY;
   uint32_t bj = 0xffffffffu;
-  if (active && f.a != nullptr) {
-    for (uint32_t j = (uint32_t)gl; j < n; j += G) {
+  if (active && f->a != nullptr) {
+    for (uint32_t j = (uint32_t)gl; j < n; j += (uint32_t)G) {
       if (visited(j)) continue;
       const size_t off = (size_t)cur * n + j;
-      double v = numpy_scalar_power(f.a[off], f.alpha);
-      if (f.b != nullptr) v = __dmul_rn(v, f.b[off]);
+      double v = numpy_scalar_power(f->a[off], f->alpha);
+      if (f->b != nullptr) v = __dmul_rn(v, f->b[off]);
       if (!(v > 0.0)) continue;
       const double u = (double)bits_to_uniform(sel_word(j, step, ak, rk));
-      const double sc = __dadd_rn(__dmul_rn(log(v), f.inv_gamma), log(u));
+      const double sc = __dadd_rn(__dmul_rn(log(v), inv_gamma), log(u));
       if (sc > best || bj == 0xffffffffu) best = sc, bj = j;
     }
   }
-#pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) {
     const double ob = __shfl_xor_sync(0xffffffffu, best, o);
     const uint32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
@@ -154,6 +158,69 @@ __device__ __forceinline__ uint32_t fallback_pick(const Fallback &f, uint32_t n,
   }
   if (active && bj == 0xffffffffu && !visited(0u)) bj = 0;
   return bj;
+}
+
+// Rebuild one ant's whole tour by the warp (the cold path of the fast
+// kernels: their step loop leaves as soon as a step has no W > 0 candidate,
+// so neither this code nor its call weighs on the loop's registers).  Each
+// step scans the ant's FULL row — the same product rule argmax_j W * u over
+// unvisited j with W > 0, lowest j on ties, so every step the fast loop did
+// decide comes out identical — and steps without a candidate go to
+// fallback_pick.  vals / idx: the row-sorted table (sw, si) or, idx NULL,
+// the dense table; ld: their row pitch.  Visited set as in fallback_pick
+// (cleared here: nwords 32-bit words of this ant).  Returns false when the
+// reference would assert (colony.py:149).
+static __device__ __noinline__ bool rebuild_tour(const float *vals, const uint16_t *idx, int ld, uint32_t n,
+                                                 const Fallback *f, const PhiloxKeys *ks,
+                                                 const taco_iter_state *state, uint32_t it, uint32_t gant,
+                                                 uint32_t *vis, int vis8, int stride, int offset, int nwords,
+                                                 int32_t *trow, int lane) {
+  const RoundKeys rk = round_keys(*ks, it);
+  const AntKey ak = ant_key(gant, rk);
+  for (int q = lane; q < nwords; q += 32) vis[q * stride + offset] = 0u;
+  __syncwarp();
+  auto mark = [&](uint32_t j) {
+    if (vis8)
+      reinterpret_cast<uint8_t *>(vis)[j] = 1;
+    else
+      vis[(j >> 5) * (uint32_t)stride + (uint32_t)offset] |= 1u << (j & 31);
+  };
+  auto seen = [&](uint32_t j) -> bool {
+    if (vis8) return reinterpret_cast<const uint8_t *>(vis)[j] != 0;
+    return (vis[(j >> 5) * (uint32_t)stride + (uint32_t)offset] >> (j & 31)) & 1u;
+  };
+  uint32_t cur = start_city(n, ak, rk);
+  if (lane == 0) {
+    mark(cur);
+    trow[0] = (int32_t)cur;
+  }
+  __syncwarp();
+  for (uint32_t step = 1; step < n; ++step) {
+    uint32_t bkey = 0u, bj = 0xffffffffu;
+    const size_t row = (size_t)cur * (uint32_t)ld;
+    for (uint32_t k = (uint32_t)lane; k < n; k += 32) {
+      const float w = vals[row + k];
+      const uint32_t j = idx != nullptr ? (uint32_t)idx[row + k] : k;
+      if (!(w > 0.0f) || seen(j)) continue;
+      const uint32_t key = __float_as_uint(__fmul_rn(w, bits_to_uniform(sel_word(j, step, ak, rk)))) + 1u;
+      if (key > bkey || (key == bkey && j < bj)) bkey = key, bj = j;
+    }
+    const uint32_t mkey = __reduce_max_sync(0xffffffffu, bkey);
+    uint32_t nxt;
+    if (mkey != 0u) {
+      nxt = __reduce_min_sync(0xffffffffu, bkey == mkey ? bj : 0xffffffffu);
+    } else {
+      nxt = fallback_pick(f, ks, state, it, gant, n, cur, step, 32, lane, 1, vis, vis8, stride, offset);
+      if (nxt == 0xffffffffu) return false;
+    }
+    if (lane == 0) {
+      mark(nxt);
+      trow[step] = (int32_t)nxt;
+    }
+    __syncwarp();
+    cur = nxt;
+  }
+  return true;
 }
 
 // per-ant shared scratch: leaf buffer, leaf sums, visited bitmask (16-B aligned)

@@ -26,6 +26,14 @@
 
 #include "construct_common.cuh"
 
+// A/B only: -DTACO_NO_FALLBACK drops the rebuild call sites (no W > 0
+// candidate then always records TACO_NO_CANDIDATE), to measure what they cost
+#ifdef TACO_NO_FALLBACK
+#define TACO_REBUILD(...) false
+#else
+#define TACO_REBUILD(...) rebuild_tour(__VA_ARGS__)
+#endif
+
 namespace taco {
 
 // Shared-memory layout of the sorted kernel (dynamic):
@@ -171,6 +179,26 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
     wg = __ldg(sw + (cur * (uint32_t)a.ld + lane));
     jg = __ldg(si + (cur * (uint32_t)a.ld + lane));
   }
+  // the step's bookkeeping once its city is known: the next row's first
+  // window is issued before it, so that L2 round trip overlaps it
+  auto advance = [&](uint32_t bj, uint32_t stp) {
+    const uint32_t e = (uint32_t)lane;
+    wg = 0.0f;
+    jg = 0;
+    if (stp + 1 < un && e < un) {
+      wg = __ldg(sw + (bj * (uint32_t)a.ld + e));
+      jg = __ldg(si + (bj * (uint32_t)a.ld + e));
+    }
+    if (lane == 0) mark_visited<VIS8>(vis, bj);
+    if (COST) {
+      if (stp > 1) lc.push();  // edge stp-2, loaded one step ago
+      lc.load(cur, bj);        // edge stp-1
+    }
+    __syncwarp();
+    tw.put((int)stp, (int32_t)bj);
+    cur = bj;
+  };
+  bool stalled = false;  // a step without a W > 0 candidate (rebuilt below)
   for (uint32_t step = 1; step < un; ++step) {
 #ifdef TACO_STEP_PROFILE
     const long long t0 = clock64();
@@ -239,32 +267,11 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
 #ifdef TACO_STEP_PROFILE
     const long long t2 = clock64();
 #endif
-    if (bestj == 0xffffffffu) {  // no W > 0 candidate: f64 fallback / all -inf rule
-      bestj = fallback_pick<32>(fallback_of(a.fb, a.state), un, cur, step, ak, rk, lane, true,
-                                [&](uint32_t j) { return visited_at<VIS8>(vis, j); });
-      if (bestj == 0xffffffffu) {
-        if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
-        return;
-      }
+    if (bestj == 0xffffffffu) {  // no W > 0 candidate: the tour is rebuilt after the loop
+      stalled = true;
+      break;
     }
-    // next row's first window: issued before this step's bookkeeping
-    {
-      const uint32_t e = (uint32_t)lane;
-      wg = 0.0f;
-      jg = 0;
-      if (step + 1 < un && e < un) {
-        wg = __ldg(sw + (bestj * (uint32_t)a.ld + e));
-        jg = __ldg(si + (bestj * (uint32_t)a.ld + e));
-      }
-    }
-    if (lane == 0) mark_visited<VIS8>(vis, bestj);
-    if (COST) {
-      if (step > 1) lc.push();  // edge step-2, loaded one step ago
-      lc.load(cur, bestj);      // edge step-1
-    }
-    __syncwarp();
-    tw.put((int)step, (int32_t)bestj);
-    cur = bestj;
+    advance(bestj, step);
 #ifdef TACO_STEP_PROFILE
     const long long t3 = clock64();
     if (ant == 0 && lane == 0) {
@@ -275,6 +282,21 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsL
       g_step_prof[4] += nwin;
     }
 #endif
+  }
+  if (stalled) {  // cold path (construct_common.cuh rebuild_tour), off the step loop's registers
+    if (MODE == 2) {  // 32 registers: even the out-of-line call costs the loop; k_rebuild_stalled does it
+      if (lane == 0) tw.row[n - 1] = -1;  // marker (a finished tour never holds -1)
+      return;
+    }
+    if (!TACO_REBUILD(sw, si, a.ld, un, &a.fb, &a.ks, a.state, it, gant, vis, VIS8, 1, 0, a.nwords, tw.row, lane)) {
+      if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
+      return;
+    }
+    if (a.costs != nullptr) {
+      const double c = warp_tour_cost(n, tw.row, a.dist, leaves, a.n_leaves, leaf_sum, lane);
+      if (lane == 0) a.costs[ant] = c;
+    }
+    return;
   }
   tw.flush();
   if (COST && lc.active) {
@@ -350,6 +372,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
   const uint32_t start = start_city(un, ak, rk);
   int32_t *trow = a.tours + (size_t)ant * n;
   bool complete = false;  // this group's tour reached n cities
+  bool stalled = false;   // a step without a W > 0 candidate (rebuilt after the loop)
   if (alive && gl == 0) {
     vis[(start >> 5) * A + g] |= 1u << (start & 31);
     trow[0] = (int32_t)start;
@@ -426,17 +449,10 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
     chunk += CH;
     const bool step_done = alive && ((bucket_ceiling(wl) < best) || (wl <= 0.0f) || (chunk >= un));
 
-    // ---- no W > 0 candidate: f64 fallback / all -inf rule (whole warp) -----
-    const bool need_fb = step_done && bestj == 0xffffffffu;
-    if (__any_sync(kFull, need_fb)) {
-      const uint32_t fj = fallback_pick<G>(fallback_of(a.fb, a.state), un, cur, step, ak, rk, gl, need_fb,
-                                           [&](uint32_t j) { return ((vis[(j >> 5) * A + g] >> (j & 31)) & 1u) != 0; });
-      if (need_fb) bestj = fj;
-    }
     // ---- groups whose step is decided move to the next city ----------------
     if (step_done) {
-      if (bestj == 0xffffffffu) {
-        if (gl == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
+      if (bestj == 0xffffffffu) {  // no W > 0 candidate: rebuilt after the loop
+        stalled = true;
         alive = false;
       } else {
         if (gl == 0) {
@@ -456,10 +472,24 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
     }
     __syncwarp();
   }
+  const int ant0 = (blockIdx.x * kGroupWarps + warp) * A;
+  // cold path: tours that met a step without a W > 0 candidate are rebuilt by
+  // the whole warp with the fallback (construct_common.cuh rebuild_tour)
+#pragma unroll 1
+  for (int q = 0; q < A; ++q) {
+    if (!__shfl_sync(kFull, (int)stalled, q * G)) continue;
+    const bool ok = TACO_REBUILD(a.sw, a.si, a.ld, un, &a.fb, &a.ks, a.state, it,
+                                 (uint32_t)(a.ant_offset + ant0 + q), vis, 0, A, q, a.nwords,
+                                 a.tours + (size_t)(ant0 + q) * n, lane);
+    if (!ok) {
+      if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, a.ant_offset + ant0 + q);
+    } else if (g == q) {
+      complete = true;
+    }
+  }
   // tour lengths of the warp's complete tours, the whole warp per tour
   // (pairwise leaves across lanes; the step loop carries no length state)
   if (a.costs != nullptr) {
-    const int ant0 = (blockIdx.x * kGroupWarps + warp) * A;
 #pragma unroll 1
     for (int q = 0; q < A; ++q) {
       if (!__shfl_sync(kFull, (int)complete, q * G)) continue;
@@ -518,6 +548,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   lc.init(a.costs != nullptr ? a.dist : nullptr, leaves, leaf_buf, leaf_sum, n, lane);
   uint32_t cur = start;
   const int nq = (n + 3) >> 2;
+  bool stalled = false;
   for (int step = 1; step < n; ++step) {
     const float4 *row = reinterpret_cast<const float4 *>(a.w + (size_t)cur * a.ldw);
     uint32_t lkey = 0u, lj = 0xffffffffu;
@@ -558,17 +589,11 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
       wkey = __reduce_max_sync(kFull, lkey);
     }
     const uint32_t mkey = __reduce_max_sync(kFull, lkey);
-    uint32_t bestj;
-    if (mkey == 0u) {  // no W > 0 candidate: f64 fallback / all -inf rule
-      bestj = fallback_pick<32>(fallback_of(a.fb, a.state), (uint32_t)n, cur, (uint32_t)step, ak, rk, lane, true,
-                                [&](uint32_t j) { return is_visited(vis, j); });
-      if (bestj == 0xffffffffu) {
-        if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
-        return;
-      }
-    } else {
-      bestj = __reduce_min_sync(kFull, lkey == mkey ? lj : 0xffffffffu);
+    if (mkey == 0u) {  // no W > 0 candidate: the tour is rebuilt after the loop
+      stalled = true;
+      break;
     }
+    const uint32_t bestj = __reduce_min_sync(kFull, lkey == mkey ? lj : 0xffffffffu);
     if (lane == 0) vis[bestj >> 5] |= 1u << (bestj & 31);
     if (step > 1) lc.push();
     lc.load(cur, bestj);
@@ -576,12 +601,61 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
     tw.put(step, (int32_t)bestj);
     cur = bestj;
   }
+  if (stalled) {  // cold path (construct_common.cuh rebuild_tour)
+    if (!TACO_REBUILD(a.w, nullptr, a.ldw, (uint32_t)n, &a.fb, &a.ks, a.state, it, gant, vis, 0, 1, 0, a.nwords,
+                      tw.row, lane)) {
+      if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
+      return;
+    }
+    if (a.costs != nullptr) {
+      const double c = warp_tour_cost(n, tw.row, a.dist, leaves, a.n_leaves, leaf_sum, lane);
+      if (lane == 0) a.costs[ant] = c;
+    }
+    return;
+  }
   tw.flush();
   if (lc.active) {
     lc.push();
     lc.load(cur, start);
     lc.push();
     const double c = lc.finish();
+    if (lane == 0) a.costs[ant] = c;
+  }
+}
+
+// Follow-up of the MODE 2 warp kernel: ants whose tour ends in the -1 marker
+// met a step without a W > 0 candidate; one warp per ant rebuilds them
+// (rebuild_tour) and their lengths.  Every other warp reads one word and
+// exits (~µs per launch).  Shared: leaves, then per warp its visited bit map
+// and leaf sums.
+constexpr int kRebuildWarps = 4;
+
+__global__ void __launch_bounds__(kRebuildWarps * 32) k_rebuild_stalled(const __grid_constant__ SortedArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ant = blockIdx.x * kRebuildWarps + warp;
+  const bool mine = ant < a.m_local && a.tours[(size_t)ant * a.n + (a.n - 1)] == -1 &&
+                    !chain_stopped_update(a.status);
+  if (!__syncthreads_or(mine)) return;
+  const size_t lb = ((size_t)8 * a.n_leaves + 15) & ~(size_t)15;
+  const int nwords = (a.n + 31) / 32;
+  const size_t per_warp = ((((size_t)4 * nwords + 15) & ~(size_t)15) + lb);
+  int2 *leaves = reinterpret_cast<int2 *>(smem);
+  uint32_t *vis = reinterpret_cast<uint32_t *>(smem + lb + per_warp * warp);
+  double *leaf_sum = reinterpret_cast<double *>(smem + lb + per_warp * warp + (((size_t)4 * nwords + 15) & ~(size_t)15));
+  if (threadIdx.x == 0) pw_leaves(a.n, leaves);
+  __syncthreads();
+  if (!mine) return;
+  const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
+  const uint32_t gant = (uint32_t)(a.ant_offset + ant);
+  int32_t *trow = a.tours + (size_t)ant * a.n;
+  if (!rebuild_tour(a.sw, a.si, a.ld, (uint32_t)a.n, &a.fb, &a.ks, a.state, it, gant, vis, 0, 1, 0, nwords, trow,
+                    lane)) {
+    if (lane == 0) record_status(a.status, TACO_NO_CANDIDATE, (int)gant);
+    return;
+  }
+  if (a.costs != nullptr) {
+    const double c = warp_tour_cost(a.n, trow, a.dist, leaves, a.n_leaves, leaf_sum, lane);
     if (lane == 0) a.costs[ant] = c;
   }
 }
@@ -825,6 +899,15 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
       TACO_SORTED_CASE(1, 0, 0) TACO_SORTED_CASE(1, 0, 1) TACO_SORTED_CASE(1, 1, 0) TACO_SORTED_CASE(1, 1, 1)
       TACO_SORTED_CASE(2, 0, 0) TACO_SORTED_CASE(2, 0, 1) TACO_SORTED_CASE(2, 1, 0) TACO_SORTED_CASE(2, 1, 1)
 #undef TACO_SORTED_CASE
+    }
+    if (rc == TACO_OK && mode == 2) {  // tours the MODE 2 kernel left to the rebuild
+      const size_t lb2 = leaves_bytes;
+      const size_t smem2 = lb2 + ((((size_t)4 * nwords + 15) & ~(size_t)15) + lb2) * kRebuildWarps;
+      if (set_smem((const void *)k_rebuild_stalled, smem2) != TACO_OK) return TACO_ERR_CUDA;
+      SortedArgs ra = a;
+      ra.costs = costs_out;
+      k_rebuild_stalled<<<(m_local + kRebuildWarps - 1) / kRebuildWarps, kRebuildWarps * 32, smem2, s>>>(ra);
+      TACO_CUDA_CHECK_LAUNCH();
     }
     if (rc == TACO_OK && costs_out != nullptr && separate_cost)
       rc = taco_tour_cost(n, m_local, tours_out, 0, dist, costs_out, stream);

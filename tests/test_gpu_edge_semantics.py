@@ -94,8 +94,11 @@ def _seed_with_starts(n, m, want_side, side, it=0):
     raise AssertionError("no seed")
 
 
-@pytest.mark.parametrize("variant", ["sorted", "dense"])
-def test_all_zero_candidates_take_city_zero_like_numpy(variant):
+@pytest.mark.parametrize("variant,env", [("sorted", {}), ("sorted", {"TACO_SORTED_KERNEL": "g8e2"}),
+                                         ("dense", {})])
+def test_all_zero_candidates_take_city_zero_like_numpy(variant, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
     inst, side = _two_clusters()
     n, m = inst.n, 3
     seed = _seed_with_starts(n, m, True, side)  # every ant starts in the far cluster
@@ -138,9 +141,25 @@ def test_solver_construction_failure_leaves_tau_where_the_reference_raised():
     assert s.best()[1] == best_before[1] and np.array_equal(s.best()[0], best_before[0])
 
 
-@pytest.mark.parametrize("variant", ["sorted", "dense"])
-def test_gamma_below_one_uses_the_f64_fallback(variant):
-    n, m, it = 400, 64, 9
+# (variant, m, env): warp kernel MODE 1 (byte / bit-map visited set), MODE 2
+# (> 32 ants per SM: rebuilt by the follow-up k_rebuild_stalled), the
+# lane-group kernels and the dense kernel
+FALLBACK_CASES = [
+    ("sorted", 64, {}),
+    ("sorted", 64, {"TACO_SORTED_VIS": "bits"}),
+    ("sorted", 6000, {"TACO_SORTED_KERNEL": "warp"}),
+    ("sorted", 6000, {"TACO_SORTED_KERNEL": "warp", "TACO_SORTED_VIS": "bits"}),
+    ("sorted", 64, {"TACO_SORTED_KERNEL": "g8e2"}),
+    ("sorted", 64, {"TACO_SORTED_KERNEL": "g4e4"}),
+    ("dense", 64, {}),
+]
+
+
+@pytest.mark.parametrize("variant,m,env", FALLBACK_CASES)
+def test_gamma_below_one_uses_the_f64_fallback(variant, m, env, monkeypatch):
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    n, it = 400, 9
     # two clusters 10^4 apart: across them P is ~1e-6 of the row's best, so
     # P^(1/gamma) ~ 1e-50 of it — zero in fp32 — and the first step out of a
     # cluster is decided by the fallback
@@ -163,10 +182,11 @@ def test_gamma_below_one_uses_the_f64_fallback(variant):
     w = t.w[:, :n].cpu().numpy()
     assert (w == 0).sum() > n  # far outside fp32's range relative to the row best
     assert np.abs(w.astype(np.float64) - fastpath.selection_table(p, gamma)).max() <= 2.0**-22
-    want = fastpath_c.build_tours(w, 21, it, np.arange(m), fallback=(p, 1.0, None), inv_gamma=1.0 / gamma)
+    ants = np.arange(m) if m <= 64 else np.unique(np.linspace(0, m - 1, 64).astype(np.int64))
+    want = fastpath_c.build_tours(w, 21, it, ants, fallback=(p, 1.0, None), inv_gamma=1.0 / gamma)
     assert fastpath_c.build_tours.last_fallbacks > 0  # the fallback really decided steps
-    assert np.array_equal(batch.tours, want)
-    assert np.array_equal(batch.costs, ref.lengths(want, inst.dist))
+    assert np.array_equal(batch.tours[ants], want)
+    assert np.array_equal(batch.costs[ants], ref.lengths(want, inst.dist))
 
 
 def test_solver_runs_gamma_below_one():
