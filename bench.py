@@ -11,10 +11,15 @@ Euclidean n=2392 cities, m=4096 ants (k=409), AdaIR, on 1 GPU.  Under
 torchrun the ants are sharded over the ranks (weak in the colony sense: the
 whole colony is fixed and split).
 
---impl reference times the reference algorithm (oracle/reference_port, the
-numpy restatement pinned against the reference's golden vectors) on the host
-cores: one sampled-and-extrapolated iteration per step, one independent colony
-per core (the reference is single-threaded numpy).
+--impl reference times the reference's own CPU implementation on the host
+cores: the UNMODIFIED antbatch package installed in baseline/_ref (git-ignored,
+it travels with the repo) through its own functions — run_experiment as-is
+for C1, and for the larger configs one sampled-and-extrapolated iteration per
+step (n-1 x the mean of sampled lockstep rounds + P, logw,
+lengths and update), one independent colony per core (the reference is
+single-threaded numpy).  Without baseline/_ref it falls back to
+oracle/reference_port, the numpy restatement pinned to the reference's golden
+vectors.
 """
 
 from __future__ import annotations
@@ -59,18 +64,29 @@ def _peaks() -> tuple[float, str]:
         return HBM_FALLBACK, "fallback"
 
 
-def _traffic(kernel: str, config: str):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu capture
-    (profiles/traffic.json, written by scripts/summarize_profiles.py), when
-    that capture was taken on this config; else (None, None)."""
+def _capture(kernel: str, config: str) -> dict | None:
+    """The committed ncu --set full summary of `kernel` captured on this config
+    (profiles/traffic.json, written by scripts/summarize_profiles.py): DRAM
+    bytes and warp instructions per launch, L2 hit rate, issue activity."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            rec = json.load(f)[kernel]
-        if rec.get("config") != config:
-            return None, None
-        return rec["dram_bytes_per_launch"], rec["capture"]
-    except (OSError, KeyError, ValueError):
-        return None, None
+            return json.load(f).get(f"{kernel}@{config}")
+    except (OSError, ValueError):
+        return None
+
+
+def _traffic(kernel: str, config: str):
+    rec = _capture(kernel, config)
+    return (rec["dram_bytes_per_launch"], rec["capture"]) if rec else (None, None)
+
+
+def _config_dict(config: str, n: int, m: int, k: int, selection: str, period: int, world: int) -> dict:
+    """The workload description, identical in both arms."""
+    return {"workload": f"{config}: n={n} cities, m={m} ants, k={k}, {selection}, alpha=1 beta=2 rho=0.1, "
+                        f"gamma 1.5->1.0 period {period}",
+            "n": n, "m": m, "k": k, "selection": selection, "gamma_period": period,
+            "instance": "U(0,2000)^2 Euclidean cities (seed 0), unrounded distances",
+            "parallelism": f"ants sharded over {world} rank(s)"}
 
 
 class _null:
@@ -370,29 +386,54 @@ def run_ours(args) -> dict | None:
     dom_ms = t_construct
     kernel = "k_construct_rw" if rw else f"k_construct_{args.construct}"
     alg = m_local * (n - 1) * (n * 8 + 2048) if rw else alg_full
-    traffic, traffic_src = _traffic(kernel, args.config)
-    roof = {"kernel": kernel, "bound": "hbm", "achieved": alg / (dom_ms * 1e-3) / 1e9, "peak": peak,
-            "unit": "GB/s", "peak_kind": peak_kind, "traffic": traffic, "traffic_source": traffic_src,
-            "ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step, "alg_bytes_per_launch": alg,
-            "alg_bytes_def": ("SURVEY 8(d): f64 P row per ant-step, m*(n-1)*(8n+2048) B" if rw
-                              else "SURVEY 8(d): full-row stream of the fp32 table, m*(n-1)*n*4 B")}
+    cap = _capture(kernel, args.config)
+    traffic = cap["dram_bytes_per_launch"] if cap else None
+    clocks = sampler.summary() if sampler else {}
+    sm_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
     if not rw and args.construct == "sorted":
-        roof["table_bytes_read_per_launch"] = alg_sorted
-        roof["table_GBps"] = alg_sorted / (dom_ms * 1e-3) / 1e9
-        roof["note"] = ("frac > 1: the pruned scan touches ~2% of the algorithmic bytes and is bound by the "
-                        "serial step chain and issue, not HBM; roofline_dense is the full-row kernel")
-    roof["frac"] = roof["achieved"] / peak
+        # The pruned scan reads ~2% of the full-row bytes (table_bytes_read,
+        # counted live), so HBM does not bound it: instruction issue and the
+        # n-1 dependent steps do.  roofline = issue: ncu's warp instructions
+        # per launch (the committed capture of this config) / the event-timed
+        # launch, against 4 issue slots per SM per cycle at the sampled clock.
+        inst = cap.get("warp_instructions_per_launch") if cap else None
+        hbm_side = {"table_bytes_read_per_launch": alg_sorted, "GBps": alg_sorted / (dom_ms * 1e-3) / 1e9,
+                    "frac_of_hbm_peak": alg_sorted / (dom_ms * 1e-3) / 1e9 / peak,
+                    "dram_bytes_per_launch_ncu": traffic,
+                    "l2_hit_rate_ncu": cap.get("l2_hit_rate") if cap else None}
+        if inst:
+            issue_peak = sms * 4 * sm_mhz * 1e6
+            roof = {"kernel": kernel, "bound": "issue", "achieved": inst / (dom_ms * 1e-3), "peak": issue_peak,
+                    "unit": "warp-instructions/s", "frac": inst / (dom_ms * 1e-3) / issue_peak,
+                    "warp_instructions_per_launch": inst,
+                    "peak_def": f"{sms} SMs x 4 issue slots x {sm_mhz:.0f} MHz (sampled SM clock)",
+                    "traffic": traffic, "traffic_source": cap["capture"], "hbm": hbm_side}
+        else:  # no capture of this config: the bytes it really reads, against HBM
+            roof = {"kernel": kernel, "bound": "hbm", "achieved": hbm_side["GBps"], "peak": peak, "unit": "GB/s",
+                    "frac": hbm_side["frac_of_hbm_peak"], "traffic": traffic,
+                    "note": "no ncu capture of this config: table bytes read (live probe) against HBM"}
+        roof.update({"ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step, "peak_kind": peak_kind,
+                     "alg_bytes_full_row": alg_full,
+                     "alg_bytes_def": "SURVEY 8(d) full-row figure m*(n-1)*n*4 B is reported under "
+                                      "roofline_dense, the kernel that streams it"})
+    else:
+        roof = {"kernel": kernel, "bound": "hbm", "achieved": alg / (dom_ms * 1e-3) / 1e9, "peak": peak,
+                "unit": "GB/s", "peak_kind": peak_kind, "traffic": traffic,
+                "traffic_source": cap["capture"] if cap else None,
+                "ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step, "alg_bytes_per_launch": alg,
+                "alg_bytes_def": ("SURVEY 8(d): f64 P row per ant-step, m*(n-1)*(8n+2048) B" if rw
+                                  else "SURVEY 8(d): full-row stream of the fp32 table, m*(n-1)*n*4 B")}
+        roof["frac"] = roof["achieved"] / peak
     line = {
         "metric": METRIC, "value": it_per_s, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32",
         "data": "synthetic: U(0,2000)^2 Euclidean cities (seed 0), unrounded distances",
-        "config": {"workload": f"{args.config}: n={n} cities, m={m} ants, k={k}, {selection}, "
-                               f"alpha=1 beta=2 rho=0.1, gamma 1.5->1.0 period {period}",
-                   "n": n, "m": m, "k": k, "selection": selection, "construct": "rw" if rw else args.construct,
-                   "parallelism": f"ants sharded over {world} GPU(s)",
-                   "l2": "back-to-back iterations; per-iteration state (tau, eta^b, dist, tables, "
-                         "tours) > 126 MB L2; value_l2_flushed scrubs 256 MB before each iteration"},
+        "config": _config_dict(args.config, n, m, k, selection, period, world),
+        "construct": "rw" if rw else args.construct,
+        "l2": ("back-to-back iterations; per-iteration state (tau, eta^b, dist, tables, tours) > 126 MB L2; "
+               "value_l2_flushed scrubs 256 MB before each iteration"),
         "selections_per_s": m * (n - 1) * it_per_s,
         "value_l2_flushed": 1000.0 / flushed_ms,
         "kernel_ms": {"construct": t_construct, "update_p": t_update,
@@ -428,14 +469,18 @@ def run_ours(args) -> dict | None:
                                   "ms_per_launch": dense_ms, "traffic": _traffic("k_construct_dense", args.config)[0],
                                   "alg_bytes_def": "full-row stream m*(n-1)*n*4 B (SURVEY 8d)"}
     if sampler:
-        line["clocks"] = sampler.summary()
+        line["clocks"] = clocks
     if world == 1 and not args.no_cpu_baseline:
         from oracle import cpu_baseline
 
-        s = cpu_baseline.sample_iteration(n, m, k, selection, seed=0, steps=args.cpu_steps, period=period)
+        ref_ok = cpu_baseline.reference_available()
+        sampler_fn = cpu_baseline.sample_iteration_reference if ref_ok else cpu_baseline.sample_iteration
+        s = sampler_fn(n, m, k, selection, seed=0, steps=args.cpu_steps, period=period)
         line["cpu_baseline"] = {
-            "value": 1.0 / s["t_iter"], "unit": "iterations/s", "cores": 1, "kind": "port",
-            "sample": (f"oracle/reference_port, 1 thread: {s['steps_sampled']} construction steps "
+            "value": 1.0 / s["t_iter"], "unit": "iterations/s", "cores": 1,
+            "kind": "reference" if ref_ok else "port",
+            "sample": (f"{'antbatch (unmodified, baseline/_ref)' if ref_ok else 'oracle/reference_port'}, 1 thread: "
+                       f"{s['steps_sampled']} construction steps "
                        f"(mean {s['t_step'] * 1e3:.1f} ms) x (n-1) + P {s['t_p'] * 1e3:.0f} ms + logw "
                        f"{s['t_logw'] * 1e3:.0f} ms + lengths {s['t_costs'] * 1e3:.0f} ms + update "
                        f"{s['t_update'] * 1e3:.0f} ms; extrapolated"),
@@ -455,31 +500,43 @@ def run_reference(args) -> dict | None:
 
     n, m, selection = CONFIGS[args.config]
     k = max(1, m // 10)
+    period = args.warmup + args.steps  # the same gamma schedule as our arm
     host = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     cores = max(1, min(host, args.ref_procs) if args.ref_procs > 0 else host)
-    # warm-up round (untimed), then K rounds; a round = one sampled iteration
-    # on each of `cores` independent single-threaded colonies at once
+    ref_ok = cpu_baseline.reference_available()
+    # C1 is small enough for the reference's own run_experiment, whole; the
+    # larger configs take hours per iteration on one core: sampled + extrapolated
+    as_is = ref_ok and n * m <= 51 * 64
+    kind = "as-is" if as_is else ("reference" if ref_ok else "port")
+    per_job = args.steps + 1 if as_is else args.cpu_steps  # iterations (as-is) or sampled rounds
+    # warm-up round (untimed), then K rounds; a round = one iteration on each
+    # of `cores` independent single-threaded colonies at once
     if args.warmup:
-        cpu_baseline.parallel_samples(n, m, k, selection, cores, cores, steps=2)
+        cpu_baseline.parallel_samples(n, m, k, selection, cores, cores, steps=2, period=period, kind=kind)
     t0 = time.perf_counter()
-    times = cpu_baseline.parallel_samples(n, m, k, selection, args.steps * cores, cores, steps=args.cpu_steps)
+    rounds = 1 if as_is else args.steps
+    times = cpu_baseline.parallel_samples(n, m, k, selection, rounds * cores, cores, steps=per_job, period=period,
+                                          kind=kind)
     wall = time.perf_counter() - t0
     per_colony = 1.0 / float(np.mean(times))
     value = per_colony * cores
+    what = ("antbatch (the unmodified reference, baseline/_ref)" if ref_ok else
+            "oracle/reference_port (numpy restatement of antbatch, pinned to its golden vectors)")
+    how = (f"run_experiment as-is, {per_job} iterations per colony (its own clock; the warm-up iteration "
+           f"excluded, bench.py:228)" if as_is else
+           f"each step = one iteration extrapolated from {args.cpu_steps} sampled lockstep rounds "
+           f"(SURVEY 8(d))")
     return {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "impl": "reference",
+        "timing": "measured" if as_is else "extrapolated",
         "data": "synthetic: U(0,2000)^2 Euclidean cities (seed 0), unrounded distances",
-        "config": {"workload": f"{args.config}: n={n} cities, m={m} ants, k={k}, {selection}",
-                   "n": n, "m": m, "k": k, "selection": selection},
+        "config": _config_dict(args.config, n, m, k, selection, period, world),
         "cpu_baseline": {"value": value, "unit": "iterations/s", "cores": cores,
-                         "kind": "port",
-                         "sample": (f"oracle/reference_port (numpy restatement of antbatch, pinned to its "
-                                    f"golden vectors): each step = one iteration extrapolated from "
-                                    f"{args.cpu_steps} construction steps; {cores} independent "
-                                    f"single-threaded colonies in parallel; per-colony "
-                                    f"{per_colony:.3g} it/s"),
+                         "kind": "reference" if ref_ok else "port",
+                         "sample": (f"{what}: {how}; {cores} independent single-threaded colonies in parallel; "
+                                    f"per-colony {per_colony:.3g} it/s"),
                          "wall_s": wall},
         "e2e": {"value": value, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

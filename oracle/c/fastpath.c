@@ -255,3 +255,66 @@ void fpo_count_mismatches(const float *w, int n, int ldw, const double *logw, co
   out[3] = mm_ref;
   out[4] = trunc;
 }
+
+/* Scan-depth profile of the pruned sorted-table scan (k_construct_sorted's
+ * stop rule): for the given ants, follow their tours (the same
+ * rule as fpo_build_tours) over the row-sorted table (sw, si; rows descending
+ * by the W bits above bit 16) and record, per step, how many 32-entry windows
+ * the warp kernel reads before `bucket_ceiling(last W) < best`.  hist[w] (w <
+ * hist_len - 1) counts steps that read w + 1 windows; the last bin collects
+ * the rest.  Test / analysis infrastructure (sizing a head-only table). */
+static inline float bucket_ceiling(float w) {
+  uint32_t b;
+  memcpy(&b, &w, 4);
+  b |= 0xffffu;
+  float r;
+  memcpy(&r, &b, 4);
+  return r;
+}
+
+void fpo_scan_profile(const float *sw, const uint16_t *si, int n, int ld, uint64_t seed, uint32_t iteration,
+                      const int64_t *ants, int count, int64_t *hist, int hist_len) {
+  const uint32_t key = fpo_seed_hash32(seed) + iteration;
+  memset(hist, 0, sizeof(int64_t) * (size_t)hist_len);
+#pragma omp parallel
+  {
+    uint8_t *seen = (uint8_t *)malloc((size_t)n);
+    int64_t *h = (int64_t *)calloc((size_t)hist_len, sizeof(int64_t));
+#pragma omp for schedule(dynamic, 1)
+    for (int a = 0; a < count; ++a) {
+      const uint32_t ant = (uint32_t)ants[a];
+      memset(seen, 0, (size_t)n);
+      uint32_t cur = start_city(ant, key, (uint32_t)n);
+      seen[cur] = 1;
+      for (uint32_t step = 1; step < (uint32_t)n; ++step) {
+        const float *wr = sw + (size_t)cur * ld;
+        const uint16_t *ir = si + (size_t)cur * ld;
+        float best = -1.0f;
+        int bj = -1, windows = 0;
+        for (int base = 0; base < n; base += 32) {
+          ++windows;
+          float wl = 0.0f;
+          for (int e = base; e < base + 32; ++e) {
+            const float w = e < n ? wr[e] : 0.0f;
+            wl = w;
+            if (e >= n || !(w > 0.0f) || seen[ir[e]] || w < best) continue;
+            const uint32_t j = ir[e];
+            uint32_t r[2];
+            pair_words(j >> 1, step, ant, key, r);
+            const float s = w * bits_to_uniform(r[j & 1]);
+            if (s > best || (s == best && (int)j < bj)) best = s, bj = (int)j;
+          }
+          if (bucket_ceiling(wl) < best || !(wl > 0.0f)) break;
+        }
+        ++h[windows - 1 < hist_len - 1 ? windows - 1 : hist_len - 1];
+        if (bj < 0) break; /* no candidate: the profile stops this ant */
+        seen[bj] = 1;
+        cur = (uint32_t)bj;
+      }
+    }
+#pragma omp critical
+    for (int i = 0; i < hist_len; ++i) hist[i] += h[i];
+    free(h);
+    free(seen);
+  }
+}

@@ -49,6 +49,9 @@ def _load():
         lib.fpo_count_mismatches.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, ctypes.c_uint64,
                                              ctypes.c_uint32, P, ctypes.c_int, P, P]
         lib.fpo_count_mismatches.restype = None
+        lib.fpo_scan_profile.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, P,
+                                         ctypes.c_int, P, ctypes.c_int]
+        lib.fpo_scan_profile.restype = None
         lib.fpo_seed_hash32.argtypes = [ctypes.c_uint64]
         lib.fpo_seed_hash32.restype = ctypes.c_uint32
         lib.fpo_philox.argtypes = [ctypes.c_int, P, P, P]
@@ -136,3 +139,16 @@ def philox2x32_10(ctr: np.ndarray, key) -> np.ndarray:
     out = np.zeros_like(ctr)
     _load().fpo_philox(ctr.shape[0], _ptr(ctr), _ptr(key), _ptr(out))
     return out
+
+
+def scan_profile(sw: np.ndarray, si: np.ndarray, n: int, seed: int, iteration: int, ants,
+                 bins: int = 4096) -> np.ndarray:
+    """Histogram of 32-entry windows read per step by the pruned sorted scan
+    (index w: w + 1 windows; last bin: that many or more)."""
+    sw = np.ascontiguousarray(sw, dtype=np.float32)
+    si = np.ascontiguousarray(si, dtype=np.uint16)
+    ants = np.ascontiguousarray(np.asarray(ants, dtype=np.int64))
+    hist = np.zeros(bins, dtype=np.int64)
+    _load().fpo_scan_profile(_ptr(sw), _ptr(si), int(n), sw.shape[1], int(seed) & 0xFFFFFFFFFFFFFFFF,
+                             int(iteration) & 0xFFFFFFFF, _ptr(ants), ants.size, _ptr(hist), bins)
+    return hist

@@ -22,6 +22,7 @@
 //          median step stops after 3 entries.
 // The tour length, in numpy's pairwise order (bit-exact with batch_costs), is
 // either accumulated on the fly or computed by k_tour_cost afterwards.
+#include <algorithm>
 #include <cstdlib>
 
 #include "construct_common.cuh"
@@ -56,7 +57,19 @@ struct SortedArgs {
 };
 
 constexpr int kSortedMaxWarps = 28;      // fused tour length: 72 registers per thread
-constexpr int kSortedMaxWarpsLean = 32;  // separate tour length: <= 32 registers, 2 CTAs per SM
+// MODE 1 (one CTA per SM) holds up to 28 ants per SM at 72 registers (32
+// warps at 64 registers rematerialized constants in the step loop; C2 -1%,
+// C3 equal); more ants per SM run MODE 2: two CTAs per SM of
+// ceil(ants per SM / 2) warps each (balanced: at C4, 55 ants per SM, 2 x 28
+// warps instead of 2 x 32 on 108 SMs and 1 x 32 on 40: 15.4 -> 14.1 ms)
+#ifndef TACO_MODE1_WARPS
+#define TACO_MODE1_WARPS 28
+#endif
+#ifndef TACO_MODE2_WARPS
+#define TACO_MODE2_WARPS 32
+#endif
+constexpr int kMode1Warps = TACO_MODE1_WARPS;
+constexpr int kMode2Warps = TACO_MODE2_WARPS;  // 2 CTAs per SM: 65536 / (64 x this) registers
 
 #ifdef TACO_STEP_PROFILE
 // per-step latency phases of ant 0 (-, windows, bookkeeping;
@@ -119,11 +132,15 @@ __device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t
 // known, ahead of the step's bookkeeping (visited bit, tour and length
 // buffers), so that L2 round trip overlaps it.  COST: the tour length is
 // accumulated on the fly (else taco_construct runs k_tour_cost afterwards).
-// MODE 0: fused tour length (COST); 1: separate length, one CTA per SM (up
-// to 64 registers); 2: separate length, two 32-warp CTAs per SM (<= 32
-// registers: the compiler rematerializes more, so only for > 32 ants/SM).
+// MODE 0: fused tour length (COST); 1: separate length, one CTA of <= 28
+// warps per SM (72 registers); 3: the same with 29-32 warps (64 registers);
+// 2: separate length, two CTAs of ceil(ants per SM / 2) <= 32 warps per SM
+// (<= 32 registers: the compiler rematerializes more, so only for > 32
+// ants per SM).
 template <bool PROBE, bool VIS8, int MODE, bool COST = (MODE == 0)>
-__global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32 : kSortedMaxWarpsLean * 32, MODE == 2 ? 2 : 1)
+__global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
+                                       : (MODE == 1 ? kMode1Warps : (MODE == 3 ? 32 : kMode2Warps)) * 32,
+                                  MODE == 2 ? 2 : 1)
     k_construct_sorted(const __grid_constant__ SortedArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
@@ -858,14 +875,20 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     // 17.2 / 17.7.  TACO_SORTED_COST=fused|separate|epilogue (tuning knob).
     bool fused_cost = false;
     if (const char *ev = getenv("TACO_SORTED_COST")) fused_cost = costs_out != nullptr && ev[0] == 'f';
-    const int max_warps = fused_cost ? kSortedMaxWarps : kSortedMaxWarpsLean;
+    const int max_warps = fused_cost ? kSortedMaxWarps : kMode1Warps;  // beyond: MODE 2, 2 x 32 warps
     // warps per CTA: all ants of an SM in one CTA when they fit (one wave);
     // larger colonies run 32-warp CTAs, two per SM.  TACO_SORTED_WARPS
     // overrides (tuning knob).
     const int ants_per_sm = (m_local + sm_count() - 1) / sm_count();
+    // MODE 3: 29-32 ants per SM, one 32-warp CTA at 64 registers (MODE 2's
+    // 32 registers cost 21% at n = 2392, m = 4400)
+    const bool wide = !fused_cost && ants_per_sm > max_warps && ants_per_sm <= 32;
+    const bool two_ctas = !fused_cost && ants_per_sm > 32;  // MODE 2
     int warps = ants_per_sm < 1 ? 1 : (ants_per_sm > max_warps ? max_warps : ants_per_sm);
+    if (wide) warps = ants_per_sm;
+    if (two_ctas) warps = std::min(kMode2Warps, (ants_per_sm + 1) / 2);
     if (const char *ev = getenv("TACO_SORTED_WARPS")) warps = atoi(ev);
-    if (warps < 1 || warps > max_warps) return TACO_ERR_ARG;
+    if (warps < 1 || warps > (two_ctas ? kMode2Warps : (wide ? 32 : max_warps))) return TACO_ERR_ARG;
     // (separate: tour lengths by a k_tour_cost launch after the kernel instead
     // of the epilogue; TACO_SORTED_COST=separate, tuning knob)
     const bool separate_cost = !fused_cost && getenv("TACO_SORTED_COST") && getenv("TACO_SORTED_COST")[0] == 's';
@@ -876,7 +899,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     // visited set: a byte per city when the SM's ants fit with it (VIS8),
     // else the bit map; TACO_SORTED_VIS=bits forces the bit map (tuning knob)
     const int nwords8 = (n + 3) / 4;
-    const int resident = ants_per_sm < 2 * max_warps ? ants_per_sm : 2 * max_warps;
+    const int resident = two_ctas ? 2 * warps : warps;
     bool vis8 = lb + scratch(nwords8) * (resident > warps ? resident : warps) <= 200 * 1024;
     if (const char *ev = getenv("TACO_SORTED_VIS")) vis8 = vis8 && ev[0] != 'b';
     // (Measured and removed: a shared-memory cache of the first T entries of
@@ -889,7 +912,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     SortedArgs a{n, m_local, ant_offset, vis8 ? nwords8 : nwords, n_leaves, ldw, sw, si, dist, iteration, state,
                  tours_out, separate_cost ? nullptr : costs_out, status, scan_count, ks, fb};
     const int grid = (m_local + warps - 1) / warps;
-    const int mode = fused_cost ? 0 : (ants_per_sm > max_warps ? 2 : 1);
+    const int mode = fused_cost ? 0 : (two_ctas ? 2 : (wide ? 3 : 1));
     const int code = mode * 4 + (vis8 ? 2 : 0) + (scan_count ? 1 : 0);
     int rc = TACO_ERR_ARG;
     switch (code) {
@@ -898,6 +921,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
       TACO_SORTED_CASE(0, 0, 0) TACO_SORTED_CASE(0, 0, 1) TACO_SORTED_CASE(0, 1, 0) TACO_SORTED_CASE(0, 1, 1)
       TACO_SORTED_CASE(1, 0, 0) TACO_SORTED_CASE(1, 0, 1) TACO_SORTED_CASE(1, 1, 0) TACO_SORTED_CASE(1, 1, 1)
       TACO_SORTED_CASE(2, 0, 0) TACO_SORTED_CASE(2, 0, 1) TACO_SORTED_CASE(2, 1, 0) TACO_SORTED_CASE(2, 1, 1)
+      TACO_SORTED_CASE(3, 0, 0) TACO_SORTED_CASE(3, 0, 1) TACO_SORTED_CASE(3, 1, 0) TACO_SORTED_CASE(3, 1, 1)
 #undef TACO_SORTED_CASE
     }
     if (rc == TACO_OK && mode == 2) {  // tours the MODE 2 kernel left to the rebuild

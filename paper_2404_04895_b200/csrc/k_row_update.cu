@@ -71,7 +71,9 @@ __host__ __device__ inline RowLayout row_layout(int n, int L, size_t sort_bytes)
 }
 
 template <int BLOCK>
-__global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay) {
+// 1024 threads per SM in flight at <= 64 registers (at 89 registers the 512-thread
+// variant ran one CTA per SM: C4 update 2.19 -> 3.25 ms)
+__global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_row_update(RowParams a, RowLayout lay) {
   extern __shared__ __align__(16) unsigned char smem[];
   double *row = reinterpret_cast<double *>(smem);
   const int L = a.n_leaves > 0 ? a.n_leaves : 1;
@@ -169,6 +171,7 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
             // group's additions (no shared-memory round trip per element)
             const bool leader = col >= 0 && lane == __ffs(peers) - 1;
             if (__any_sync(0xffffffffu, __popc(peers) > 1)) {
+#ifdef TACO_DEPOSIT_FIXED32
               double acc = leader ? row[col] : 0.0;
 #pragma unroll
               for (int t = 0; t < 32; ++t) {
@@ -176,6 +179,21 @@ __global__ void __launch_bounds__(BLOCK) k_row_update(RowParams a, RowLayout lay
                 if ((peers >> t) & 1u) acc = __dadd_rn(acc, x);
               }
               if (leader) row[col] = acc;
+#else
+              // leaders walk their group's lanes in increasing (= rank) order;
+              // as many rounds as the largest group (not 32)
+              unsigned rem = leader ? peers : 0u;
+              const int rounds = __reduce_max_sync(0xffffffffu, __popc(rem));
+              double acc = leader ? row[col] : 0.0;
+#pragma unroll 4
+              for (int t = 0; t < rounds; ++t) {
+                const int src = rem ? __ffs(rem) - 1 : lane;
+                const double x = __shfl_sync(0xffffffffu, v, src);
+                if (rem) acc = __dadd_rn(acc, x);
+                rem &= rem - 1u;
+              }
+              if (leader) row[col] = acc;
+#endif
             } else if (leader) {  // no shared column in this window
               row[col] = __dadd_rn(row[col], v);
             }

@@ -52,5 +52,21 @@ taco.batch_costs(batch.tours, host_inst)
 taco.scaled_log_weights(prob.p, 1.3)
 big = taco.AcoParams(m=17000, k=5, selection="ir", seed=3)  # CUB elite sort path (m > 16384)
 taco.Solver(inst, big, graph=False).run(1)
+# gamma < 1: stalled tours rebuilt in-kernel (MODE 1, lane groups, dense) and
+# by k_rebuild_stalled (MODE 2, > 32 ants per SM)
+pts = g.uniform(0.0, 10.0, (n, 2))
+pts[n // 2:] += 1e4
+far = taco.device_euclidean_instance(pts)
+for mm, knob in ((m, None), (m, "g8e2"), (5000, "warp")):
+    if knob:
+        os.environ["TACO_SORTED_KERNEL"] = knob
+    greedy = taco.AcoParams(m=mm, k=3, selection="adair", seed=2, gamma_schedule=taco.GammaSchedule(1.0, 0.1, 4))
+    for construct in ("sorted", "dense"):
+        taco.Solver(far, greedy, construct=construct, graph=False).run(3)
+    os.environ.pop("TACO_SORTED_KERNEL", None)
+# argmax_select_block drop-in
+logw = np.log(g.uniform(0.0, 1.0, (n, n)))
+taco.argmax_select_block(logw, g.integers(0, n, m), g.standard_exponential((m, n)), g.uniform(size=(m, n)) < 0.3,
+                         np.empty((m, n)))
 torch.cuda.synchronize()
 print("kernel smoke: ok")

@@ -7,7 +7,8 @@
 set -u
 TAG=${1:-r01}
 WHAT=${2:-launches}
-CMD="python bench.py --steps 2 --warmup 1 --no-cpu-baseline"
+CONFIG=${CONFIG:-c3}
+CMD="python bench.py --config $CONFIG --steps 2 --warmup 1 --no-cpu-baseline"
 RWCMD="python bench.py --config c3rw --steps 1 --warmup 3 --no-cpu-baseline"
 mkdir -p gpurun_out
 if [ "$WHAT" = rw ]; then RUN=$RWCMD; else RUN=$CMD; fi

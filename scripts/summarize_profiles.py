@@ -1,7 +1,9 @@
 """Summarize an ncu round into profiles/ (tracked): launch-list shares and the
 key counters of each full capture.
 
-usage: python scripts/summarize_profiles.py <tag> [gpurun_out dir]
+usage: python scripts/summarize_profiles.py <tag> [gpurun_out dir] [config]
+(config: the bench.py --config the captures ran, default c3; c3rw for the
+roulette capture)
 writes profiles/<tag>_launches.csv, profiles/<tag>_kernels.csv,
 profiles/<tag>_hotlines.txt
 """
@@ -15,12 +17,14 @@ import sys
 
 tag = sys.argv[1]
 src = sys.argv[2] if len(sys.argv) > 2 else "gpurun_out"
+config = sys.argv[3] if len(sys.argv) > 3 else "c3"
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 out_dir = os.path.join(root, "profiles")
 os.makedirs(out_dir, exist_ok=True)
 
 # ---- launch list -------------------------------------------------------------
-rows = list(csv.reader(open(os.path.join(src, f"launches_{tag}.csv"))))
+launch_path = os.path.join(src, f"launches_{tag}.csv")
+rows = list(csv.reader(open(launch_path))) if os.path.exists(launch_path) else [["Kernel Name", "Metric Value"]]
 hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
 h = rows[hi]
 ki, vi = h.index("Kernel Name"), h.index("Metric Value")
@@ -29,7 +33,7 @@ for r in rows[hi + 1:]:
     name = r[ki].split("(")[0].replace("void ", "")
     agg[name] = agg.get(name, 0.0) + float(r[vi].replace(",", "")) / 1e3
     cnt[name] += 1
-total = sum(agg.values())
+total = sum(agg.values()) or 1.0
 with open(os.path.join(out_dir, f"{tag}_launches.csv"), "w", newline="") as f:
     w = csv.writer(f)
     w.writerow(["kernel", "launches", "total_us", "mean_us", "share"])
@@ -90,8 +94,12 @@ for rec in kern_rows:
     rd, wr = _bytes(rec.get("dram__bytes_read.sum")), _bytes(rec.get("dram__bytes_write.sum"))
     if rd is None or wr is None:
         continue
-    traffic[base] = {"config": "c3rw" if base == "k_construct_rw" else "c3",  # scripts/profile_round.sh
+    cfg = "c3rw" if base == "k_construct_rw" else config  # scripts/profile_round.sh
+    inst = rec.get("smsp__inst_executed.sum")
+    traffic[f"{base}@{cfg}"] = {"config": cfg,
                      "dram_bytes_per_launch": rd + wr, "dram_read_bytes": rd, "dram_write_bytes": wr,
+                     "warp_instructions_per_launch": float(inst.split()[0].replace(",", "")) if inst else None,
+                     "issue_active_pct": rec.get("smsp__issue_active.avg.pct_of_peak_sustained_active"),
                      "duration": rec.get("gpu__time_duration.sum"), "l2_hit_rate": rec.get("lts__t_sector_hit_rate.pct"),
                      "capture": f"profiles/{tag}_kernels.csv ({rec['report']}, ncu --set full)"}
 with open(traffic_path, "w") as f:

@@ -5,7 +5,7 @@ For each config the Solver (device-built instance, the bench's parameters)
 runs ITERS iterations; then, on its selection table for the next iteration:
 
 * every production instantiation of the construction kernels — warp-per-ant
-  MODE 1 / MODE 2 x byte / bit-map visited set, the fused-length MODE 0, the
+  MODE 1 / 2 / 3 x byte / bit-map visited set, the fused-length MODE 0, the
   lane-group kernels g4e2 / g4e4 / g8e2 / g8e4 / g16e2, and the dense
   full-row kernel — is forced (the TACO_SORTED_* knobs) and its tours of a
   spread sample of global ant ids must equal the C oracle's full-scan
@@ -42,6 +42,7 @@ CONFIGS = {
     "c2": (1000, 1024, "adair", 64),
     "c2_m8192": (1000, 8192, "adair", 64),  # > 32 ants/SM with the byte visited set (warp MODE 2 + VIS8)
     "c3": (2392, 4096, "adair", 64),
+    "c3_m4400": (2392, 4400, "adair", 32),  # 29.7 ants/SM: one 32-warp CTA per SM (warp MODE 3)
     "c4": (10000, 8192, "ir", 24),
     "c5_65536": (5000, 65536, "ir", 48),
 }
