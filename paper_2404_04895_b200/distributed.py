@@ -15,7 +15,7 @@ with one SUM all-reduce of a k x n buffer in which each rank filled the rows
 it owns (taco_shard_elites) — k·n·4 bytes instead of m·n·4 (10x less at
 k = m/10).  ``gather_colony`` (all tours) remains for ``last_batch()``.
 
-Row-partitioned update (the default when sharded): the deposit is identical
+Row-partitioned update (optional; replicated is the default): the deposit is identical
 on every rank, and the row update is independent per row (colony.py:27-60,
 evaporation + row normalization), so rank r updates only rows
 [r·nr, (r+1)·nr) of tau, P and the selection table (``row_partition``) and

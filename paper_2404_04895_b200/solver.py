@@ -98,9 +98,10 @@ class Solver:
     pheromone, best lengths) — the parity mode, one GPU only.
     group: torch.distributed group to shard ants over (default: the world
     group when initialized with more than one rank).
-    update: "replicated" (every rank updates all rows) or "partitioned" (each
-    rank updates its n/R rows of tau / P / the selection table and the table
-    rows are all-gathered; default when sharded).
+    update: "replicated" (default: every rank updates all rows of its own
+    replica, no n^2 collective) or "partitioned" (each rank updates its n/R
+    rows of tau / P / the selection table and the table rows are
+    all-gathered: 6n^2 B per iteration).
     graph: replay a captured CUDA graph per iteration (default: on for a
     single-GPU device-stream colony with n*m < 2^16, where launch
     overhead matters; the sharded and replay modes always run eagerly).
@@ -150,7 +151,10 @@ class Solver:
             raise ValueError("the reference-stream replay runs on one GPU")
 
         if update is None:
-            update = "partitioned" if world > 1 else "replicated"
+            # replicated (north_star: every rank applies the identical deposit,
+            # no n^2 collective); "partitioned" trades an n^2 all-gather of
+            # the selection table for 1/R of the update
+            update = "replicated"
         if update not in ("replicated", "partitioned"):
             raise ValueError(f"update must be 'replicated' or 'partitioned', got {update!r}")
         # (rows past the fused row kernel's shared memory take the replicated
