@@ -11,6 +11,8 @@
 // write the sorted table 6n, read the row's k elite (prev, next) pairs 8k
 // (contiguous: the edge map is city-major).  The row lives in shared memory
 // between the phases so tau / unnorm are touched once.
+#include <cstdlib>
+
 #include <cub/block/block_radix_sort.cuh>
 
 #include "taco_common.cuh"
@@ -45,7 +47,10 @@ struct RowParams {
   int row_begin, row_end;  // rows [row_begin, row_end) of the n x n matrices (row-partitioned update)
 };
 
-constexpr int kDepositChunk = 512;  // elites staged in shared memory per pass
+#ifndef TACO_DEPOSIT_CHUNK
+#define TACO_DEPOSIT_CHUNK 512
+#endif
+constexpr int kDepositChunk = TACO_DEPOSIT_CHUNK;  // elites staged in shared memory per pass
 constexpr int kBatch = 4;           // tau / eta^b loads in flight per thread
 
 // Shared-memory layout (bytes, all regions 16-B aligned):
@@ -327,6 +332,12 @@ static int launch_row(const RowParams &a, cudaStream_t stream) {
   // CTA width by row length (scripts/row_update_probe.py): 256 threads are
   // best up to n ~ 5000 (n = 2392: 153 us vs 154 / 211 for 128 / 512 with the
   // k = 409 deposit); long rows want 512 (n = 10000: 1565 vs 1832 us)
+  if (const char *ev = getenv("TACO_ROW_BLOCK")) {  // tuning knob
+    const int b = atoi(ev);
+    if (b == 128) return launch_row_t<128>(a, lay, stream);
+    if (b == 256) return launch_row_t<256>(a, lay, stream);
+    if (b == 512) return launch_row_t<512>(a, lay, stream);
+  }
   if (a.n > 7000) return launch_row_t<512>(a, lay, stream);
   return launch_row_t<256>(a, lay, stream);
 }
