@@ -391,17 +391,28 @@ def run_ours(args) -> dict | None:
     clocks = sampler.summary() if sampler else {}
     sm_mhz = clocks.get("sm_mhz") or clocks.get("sm_max_mhz") or 1965.0
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    if not rw and args.construct == "sorted":
+    inst = cap.get("warp_instructions_per_launch") if cap else None
+    if rw or args.construct == "sorted":
         # The pruned scan reads ~2% of the full-row bytes (table_bytes_read,
-        # counted live), so HBM does not bound it: instruction issue and the
-        # n-1 dependent steps do.  roofline = issue: ncu's warp instructions
-        # per launch (the committed capture of this config) / the event-timed
-        # launch, against 4 issue slots per SM per cycle at the sampled clock.
-        inst = cap.get("warp_instructions_per_launch") if cap else None
-        hbm_side = {"table_bytes_read_per_launch": alg_sorted, "GBps": alg_sorted / (dom_ms * 1e-3) / 1e9,
-                    "frac_of_hbm_peak": alg_sorted / (dom_ms * 1e-3) / 1e9 / peak,
-                    "dram_bytes_per_launch_ncu": traffic,
-                    "l2_hit_rate_ncu": cap.get("l2_hit_rate") if cap else None}
+        # counted live) and the roulette kernel's f64 rows are L2-resident, so
+        # HBM does not bound either: instruction issue and the n-1 dependent
+        # steps do.  roofline = issue: ncu's warp instructions per launch (the
+        # committed capture of this config) / the event-timed launch, against
+        # 4 issue slots per SM per cycle at the sampled clock.
+        if rw:
+            hbm_side = {"alg_bytes_per_launch": alg, "dram_bytes_per_launch_ncu": traffic,
+                        "l2_hit_rate_ncu": cap.get("l2_hit_rate") if cap else None,
+                        "alg_bytes_def": "SURVEY 8(d): f64 P row per ant-step, m*(n-1)*(8n+2048) B"}
+            bytes_live = traffic / (dom_ms * 1e-3) / 1e9 if traffic else None
+        else:
+            hbm_side = {"table_bytes_read_per_launch": alg_sorted, "GBps": alg_sorted / (dom_ms * 1e-3) / 1e9,
+                        "frac_of_hbm_peak": alg_sorted / (dom_ms * 1e-3) / 1e9 / peak,
+                        "dram_bytes_per_launch_ncu": traffic,
+                        "l2_hit_rate_ncu": cap.get("l2_hit_rate") if cap else None,
+                        "alg_bytes_full_row": alg_full,
+                        "alg_bytes_def": "SURVEY 8(d) full-row figure m*(n-1)*n*4 B is reported under "
+                                         "roofline_dense, the kernel that streams it"}
+            bytes_live = hbm_side["GBps"]
         if inst:
             issue_peak = sms * 4 * sm_mhz * 1e6
             roof = {"kernel": kernel, "bound": "issue", "achieved": inst / (dom_ms * 1e-3), "peak": issue_peak,
@@ -409,21 +420,17 @@ def run_ours(args) -> dict | None:
                     "warp_instructions_per_launch": inst,
                     "peak_def": f"{sms} SMs x 4 issue slots x {sm_mhz:.0f} MHz (sampled SM clock)",
                     "traffic": traffic, "traffic_source": cap["capture"], "hbm": hbm_side}
-        else:  # no capture of this config: the bytes it really reads, against HBM
-            roof = {"kernel": kernel, "bound": "hbm", "achieved": hbm_side["GBps"], "peak": peak, "unit": "GB/s",
-                    "frac": hbm_side["frac_of_hbm_peak"], "traffic": traffic,
-                    "note": "no ncu capture of this config: table bytes read (live probe) against HBM"}
-        roof.update({"ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step, "peak_kind": peak_kind,
-                     "alg_bytes_full_row": alg_full,
-                     "alg_bytes_def": "SURVEY 8(d) full-row figure m*(n-1)*n*4 B is reported under "
-                                      "roofline_dense, the kernel that streams it"})
+        else:  # no capture of this config: the bytes it really moves, against HBM
+            roof = {"kernel": kernel, "bound": "hbm", "achieved": bytes_live, "peak": peak, "unit": "GB/s",
+                    "frac": bytes_live / peak if bytes_live else None, "traffic": traffic, "hbm": hbm_side,
+                    "note": "no ncu capture of this config: the bytes it reads (live probe) against HBM"}
+        roof.update({"ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step, "peak_kind": peak_kind})
     else:
         roof = {"kernel": kernel, "bound": "hbm", "achieved": alg / (dom_ms * 1e-3) / 1e9, "peak": peak,
                 "unit": "GB/s", "peak_kind": peak_kind, "traffic": traffic,
                 "traffic_source": cap["capture"] if cap else None,
                 "ms_per_launch": dom_ms, "share_of_step": dom_ms / ms_per_step, "alg_bytes_per_launch": alg,
-                "alg_bytes_def": ("SURVEY 8(d): f64 P row per ant-step, m*(n-1)*(8n+2048) B" if rw
-                                  else "SURVEY 8(d): full-row stream of the fp32 table, m*(n-1)*n*4 B")}
+                "alg_bytes_def": "SURVEY 8(d): full-row stream of the fp32 table, m*(n-1)*n*4 B"}
         roof["frac"] = roof["achieved"] / peak
     line = {
         "metric": METRIC, "value": it_per_s, "unit": "iterations/s", "n_gpus": world,
