@@ -9,12 +9,16 @@
  * argmax_j(log P[cur, j] / gamma - E[a, j]) over unvisited j, first of ties,
  * selection.py:143-155 / colony.py:126-152 of /root/reference/pkg/src/antbatch):
  *   - Philox2x32-10 (Random123), key = H(seed) + iteration, counter
- *     (ant, (j >> 1) | step << 16), word j & 1;  u = ((x >> 9) + 1/2) 2^-23
+ *     (ant, (s >> 1) | step << 16), word s & 1;  u = ((x >> 9) + 1/2) 2^-23;
+ *     the slot s is the city j (dense stream, fpo_build_tours) or the entry's
+ *     position in row cur of the row-sorted table (sorted stream,
+ *     fpo_build_tours_sorted)
  *   - start city: Lemire bound of word 0 of counter (ant, 0)
- *   - next = argmax_j fp32(W[cur, j] * u_j) over unvisited j with W > 0,
- *     lowest j on ties (a FULL scan: no sorted table, no pruning)
+ *   - next = argmax_j fp32(W[cur, j] * u_slot(j)) over unvisited j with W > 0,
+ *     lowest j on ties (a FULL scan: no pruning)
  *   - no W > 0 candidate left: the f64 fallback, argmax over unvisited j with
- *     v_j > 0 of log(v_j) * inv_gamma + log(u_j), v = A[cur, j]^alpha (* B[cur, j]);
+ *     v_j > 0 of log(v_j) * inv_gamma + log(u_j), v = A[cur, j]^alpha (* B[cur, j]),
+ *     u_j keyed by the city in both streams;
  *     none either: city 0 when it is unvisited (numpy's argmax of an all -inf
  *     row, selection.py:152-155), else the "selector chose a visited city"
  *     failure (colony.py:149)
@@ -90,31 +94,33 @@ static inline double fb_value(const double *a, double alpha, const double *b, si
 
 /* One ant's tour.  Returns 0, or 2 when the selector is left without a city
  * (the reference's assertion).  scratch: n bytes. */
-static int one_tour(const float *w, int n, int ldw, uint32_t key, uint32_t ant, const double *fb_a,
-                    double fb_alpha, const double *fb_b, double inv_gamma, int32_t *tour, uint8_t *seen,
-                    int64_t *fallbacks) {
+static int one_tour(const float *w, const uint16_t *idx, int n, int ldw, uint32_t key, uint32_t ant,
+                    const double *fb_a, double fb_alpha, const double *fb_b, double inv_gamma, int32_t *tour,
+                    uint8_t *seen, int64_t *fallbacks) {
   memset(seen, 0, (size_t)n);
   uint32_t cur = start_city(ant, key, (uint32_t)n);
   seen[cur] = 1;
   tour[0] = (int32_t)cur;
   for (uint32_t step = 1; step < (uint32_t)n; ++step) {
     const float *row = w + (size_t)cur * ldw;
+    const uint16_t *irow = idx ? idx + (size_t)cur * ldw : NULL;
     float best = -1.0f;
     int bj = -1;
+    /* slots s = 2q, 2q+1: cities (dense) or sorted positions (idx given) */
     for (int q = 0; 2 * q < n; ++q) {
-      const int j0 = 2 * q, j1 = 2 * q + 1;
-      const int c0 = !seen[j0] && row[j0] > 0.0f;
-      const int c1 = j1 < n && !seen[j1] && row[j1] > 0.0f;
-      if (!c0 && !c1) continue;
+      int c[2], jj[2];
+      for (int e = 0; e < 2; ++e) {
+        const int slot = 2 * q + e;
+        jj[e] = slot < n ? (irow ? (int)irow[slot] : slot) : -1;
+        c[e] = slot < n && !seen[jj[e]] && row[slot] > 0.0f;
+      }
+      if (!c[0] && !c[1]) continue;
       uint32_t r[2];
       pair_words((uint32_t)q, step, ant, key, r);
-      if (c0) {
-        const float s = row[j0] * bits_to_uniform(r[0]);
-        if (s > best) best = s, bj = j0;
-      }
-      if (c1) {
-        const float s = row[j1] * bits_to_uniform(r[1]);
-        if (s > best) best = s, bj = j1;
+      for (int e = 0; e < 2; ++e) {
+        if (!c[e]) continue;
+        const float s = row[2 * q + e] * bits_to_uniform(r[e]);
+        if (s > best || (s == best && jj[e] < bj)) best = s, bj = jj[e];
       }
     }
     if (bj < 0) { /* f64 fallback, then numpy's all -inf argmax */
@@ -145,9 +151,10 @@ static int one_tour(const float *w, int n, int ldw, uint32_t key, uint32_t ant, 
 
 /* Tours of the given global ant ids.  Returns 0, or 2 and the first failing
  * row index in *fail_row.  fb_a may be NULL (no fallback source). */
-int fpo_build_tours(const float *w, int n, int ldw, uint64_t seed, uint32_t iteration, const int64_t *ants,
-                    int count, const double *fb_a, double fb_alpha, const double *fb_b, double inv_gamma,
-                    int32_t *tours_out, int64_t *fallbacks, int *fail_row) {
+static int build_tours_impl(const float *w, const uint16_t *idx, int n, int ldw, uint64_t seed, uint32_t iteration,
+                            const int64_t *ants, int count, const double *fb_a, double fb_alpha,
+                            const double *fb_b, double inv_gamma, int32_t *tours_out, int64_t *fallbacks,
+                            int *fail_row) {
   const uint32_t key = fpo_seed_hash32(seed) + iteration;
   int rc = 0;
   int64_t fb_total = 0;
@@ -158,7 +165,7 @@ int fpo_build_tours(const float *w, int n, int ldw, uint64_t seed, uint32_t iter
 #pragma omp for schedule(dynamic, 1)
     for (int a = 0; a < count; ++a) {
       int64_t fb = 0;
-      const int r = one_tour(w, n, ldw, key, (uint32_t)ants[a], fb_a, fb_alpha, fb_b, inv_gamma,
+      const int r = one_tour(w, idx, n, ldw, key, (uint32_t)ants[a], fb_a, fb_alpha, fb_b, inv_gamma,
                              tours_out + (size_t)a * n, seen, &fb);
       fb_total += fb;
       if (r != 0) {
@@ -173,6 +180,24 @@ int fpo_build_tours(const float *w, int n, int ldw, uint64_t seed, uint32_t iter
   }
   if (fallbacks) *fallbacks = fb_total;
   return rc;
+}
+
+/* Dense stream: w is the (n, ldw) fp32 table in city order. */
+int fpo_build_tours(const float *w, int n, int ldw, uint64_t seed, uint32_t iteration, const int64_t *ants,
+                    int count, const double *fb_a, double fb_alpha, const double *fb_b, double inv_gamma,
+                    int32_t *tours_out, int64_t *fallbacks, int *fail_row) {
+  return build_tours_impl(w, NULL, n, ldw, seed, iteration, ants, count, fb_a, fb_alpha, fb_b, inv_gamma,
+                          tours_out, fallbacks, fail_row);
+}
+
+/* Sorted stream: (sw, si) is the row-sorted table (W values and their
+ * cities, each row in the kernels' order); the uniform of an entry is keyed
+ * by its position.  A full scan of every entry — no pruning. */
+int fpo_build_tours_sorted(const float *sw, const uint16_t *si, int n, int ld, uint64_t seed, uint32_t iteration,
+                           const int64_t *ants, int count, const double *fb_a, double fb_alpha, const double *fb_b,
+                           double inv_gamma, int32_t *tours_out, int64_t *fallbacks, int *fail_row) {
+  return build_tours_impl(sw, si, n, ld, seed, iteration, ants, count, fb_a, fb_alpha, fb_b, inv_gamma, tours_out,
+                          fallbacks, fail_row);
 }
 
 /* Selection-level agreement along given tours (the device's): at every step
@@ -190,9 +215,9 @@ int fpo_build_tours(const float *w, int n, int ldw, uint64_t seed, uint32_t iter
  * out[0] = selections compared, out[1..3] = mismatches of [0], [1], [2];
  * out[4] = steps of [2] where the refined winner had W below 2^-24 of the
  * recorded winner's W (the uniform floor's truncation). */
-void fpo_count_mismatches(const float *w, int n, int ldw, const double *logw, const double *logu_table,
-                          uint64_t seed, uint32_t iteration, const int64_t *ants, int count,
-                          const int32_t *tours, int64_t *out) {
+void fpo_count_mismatches(const float *w, const uint16_t *idx, int n, int ldw, const double *logw,
+                          const double *logu_table, uint64_t seed, uint32_t iteration, const int64_t *ants,
+                          int count, const int32_t *tours, int64_t *out) {
   const uint32_t key = fpo_seed_hash32(seed) + iteration;
   const uint32_t key2 = key ^ 0xA5A5A5A5u;
   int64_t sel = 0, mm_prod = 0, mm_log = 0, mm_ref = 0, trunc = 0;
@@ -208,6 +233,7 @@ void fpo_count_mismatches(const float *w, int n, int ldw, const double *logw, co
       seen[cur] = 1;
       for (uint32_t step = 1; step < (uint32_t)n; ++step) {
         const float *row = w + (size_t)cur * ldw;
+        const uint16_t *irow = idx ? idx + (size_t)cur * ldw : NULL;
         const double *lrow = logw + (size_t)cur * n;
         float pbest = -1.0f;
         int pj = -1, lj = 0, rj = 0; /* numpy: an all -inf row's argmax is 0 */
@@ -215,24 +241,30 @@ void fpo_count_mismatches(const float *w, int n, int ldw, const double *logw, co
         for (int q = 0; 2 * q < n; ++q) {
           uint32_t r[2], f[2];
           int any = 0;
-          for (int e = 0; e < 2; ++e) any |= (2 * q + e < n) && !seen[2 * q + e];
+          for (int e = 0; e < 2; ++e) {
+            const int slot = 2 * q + e;
+            any |= slot < n && !seen[irow ? irow[slot] : slot];
+          }
           if (!any) continue;
           pair_words((uint32_t)q, step, ant, key, r);
           for (int e = 0; e < 2; ++e) {
-            const int j = 2 * q + e;
-            if (j >= n || seen[j]) continue;
-            if (row[j] > 0.0f) {
-              const float s = row[j] * bits_to_uniform(r[e]);
-              if (s > pbest) pbest = s, pj = j;
+            const int slot = 2 * q + e;
+            if (slot >= n) continue;
+            const int j = irow ? (int)irow[slot] : slot;
+            if (seen[j]) continue;
+            if (row[slot] > 0.0f) {
+              const float s = row[slot] * bits_to_uniform(r[e]);
+              if (s > pbest || (s == pbest && j < pj)) pbest = s, pj = j;
             }
+            /* the log rule visits cities in slot order: first of ties = lowest j */
             const double ls = lrow[j] + logu_table[r[e] >> 9];
-            if (ls > lbest) lbest = ls, lj = j;
+            if (ls > lbest || (ls == lbest && j < lj)) lbest = ls, lj = j;
             /* refined uniform: same bin (k = x >> 9), 53-bit position inside it */
-            philox2x32_10(ant ^ 0x80000000u, (uint32_t)j | (step << 16), key2, f);
+            philox2x32_10(ant ^ 0x80000000u, (uint32_t)slot | (step << 16), key2, f);
             const uint64_t frac = (((uint64_t)f[0] << 32) | f[1]) >> 11;
             const double u53 = ((double)(r[e] >> 9) + (double)frac * 0x1p-53) * 0x1p-23;
             const double rs = lrow[j] + log(u53 > 0.0 ? u53 : 0x1p-80);
-            if (rs > rbest) rbest = rs, rj = j;
+            if (rs > rbest || (rs == rbest && j < rj)) rbest = rs, rj = j;
           }
         }
         const int got = tour[step];
@@ -241,7 +273,13 @@ void fpo_count_mismatches(const float *w, int n, int ldw, const double *logw, co
         mm_log += lj != got;
         if (rj != got) {
           ++mm_ref;
-          if (row[rj] < row[got] * 0x1p-24f) ++trunc;
+          float wr = 0.0f, wg = 0.0f; /* W of the refined winner and of the recorded one */
+          for (int slot = 0; slot < n; ++slot) {
+            const int j = irow ? (int)irow[slot] : slot;
+            if (j == rj) wr = row[slot];
+            if (j == got) wg = row[slot];
+          }
+          if (wr < wg * 0x1p-24f) ++trunc;
         }
         seen[got] = 1;
         cur = (uint32_t)got;
@@ -300,8 +338,8 @@ void fpo_scan_profile(const float *sw, const uint16_t *si, int n, int ld, uint64
             if (e >= n || !(w > 0.0f) || seen[ir[e]] || w < best) continue;
             const uint32_t j = ir[e];
             uint32_t r[2];
-            pair_words(j >> 1, step, ant, key, r);
-            const float s = w * bits_to_uniform(r[j & 1]);
+            pair_words((uint32_t)e >> 1, step, ant, key, r); /* slot = sorted position */
+            const float s = w * bits_to_uniform(r[e & 1]);
             if (s > best || (s == best && (int)j < bj)) best = s, bj = (int)j;
           }
           if (bucket_ceiling(wl) < best || !(wl > 0.0f)) break;

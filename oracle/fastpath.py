@@ -188,6 +188,56 @@ def build_tours(w: np.ndarray, seed: int, iteration: int, ants, fallback=None, i
     return tours
 
 
+def build_tours_sorted(sw: np.ndarray, si: np.ndarray, seed: int, iteration: int, ants, fallback=None,
+                       inv_gamma: float = 1.0) -> np.ndarray:
+    """The sorted stream (the kernels that scan the row-sorted table): the
+    full-scan product rule over the table entries, the uniform of an entry
+    keyed by its POSITION in the current row (slot) instead of its city.
+    sw / si: (n, >= n) sorted values and cities; fallback as build_tours
+    (its uniforms keyed by city)."""
+    n = sw.shape[0]
+    ants = np.asarray(ants, dtype=np.int64)
+    a = ants.size
+    rows = np.arange(a)
+    cur = starts(seed, iteration, ants, n)
+    seen = np.zeros((a, n), dtype=bool)
+    seen[rows, cur] = True
+    tours = np.empty((a, n), dtype=np.int64)
+    tours[:, 0] = cur
+    slots = np.arange(n, dtype=np.uint64)
+    for step in range(1, n):
+        u = uniforms(seed, iteration, step, ants[:, None], slots[None, :])  # by position
+        wr = sw[cur][:, :n]
+        jr = si[cur][:, :n].astype(np.int64)
+        score = wr * u
+        score[np.take_along_axis(seen, jr, axis=1) | (wr <= 0)] = np.float32(-1.0)
+        # argmax over entries; ties to the lowest city
+        best = score.max(axis=1)
+        jr_masked = np.where(score == best[:, None], jr, n)
+        nxt = jr_masked.min(axis=1)
+        for r in np.flatnonzero(best < 0):  # no W > 0 candidate: the city-keyed fallback
+            pick = -1
+            if fallback is not None:
+                v = _fallback_value(fallback[0][cur[r]], fallback[1],
+                                    None if fallback[2] is None else fallback[2][cur[r]])
+                ok = ~seen[r] & (v > 0)
+                if ok.any():
+                    uc = uniforms(seed, iteration, step, ants[r], np.arange(n, dtype=np.uint64))
+                    with np.errstate(divide="ignore"):
+                        sc = np.log(v) * inv_gamma + np.log(uc.astype(np.float64))
+                    sc[~ok] = -np.inf
+                    pick = int(sc.argmax())
+            if pick < 0:
+                if seen[r, 0]:
+                    raise AssertionError("selector chose a visited city")
+                pick = 0
+            nxt[r] = pick
+        seen[rows, nxt] = True
+        tours[:, step] = nxt
+        cur = nxt
+    return tours
+
+
 def log_rule_tours(p: np.ndarray, g: float, seed: int, iteration: int, ants) -> np.ndarray:
     """The reference's log-domain rule argmax(log P / g - E) (selection.py:
     143-155) driven by the DEVICE uniforms, E = -log(float64(u)).  Counting

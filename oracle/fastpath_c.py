@@ -46,7 +46,10 @@ def _load():
         lib.fpo_build_tours.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, P,
                                         ctypes.c_int, P, ctypes.c_double, P, ctypes.c_double, P, P, P]
         lib.fpo_build_tours.restype = ctypes.c_int
-        lib.fpo_count_mismatches.argtypes = [P, ctypes.c_int, ctypes.c_int, P, P, ctypes.c_uint64,
+        lib.fpo_build_tours_sorted.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32,
+                                               P, ctypes.c_int, P, ctypes.c_double, P, ctypes.c_double, P, P, P]
+        lib.fpo_build_tours_sorted.restype = ctypes.c_int
+        lib.fpo_count_mismatches.argtypes = [P, P, ctypes.c_int, ctypes.c_int, P, P, ctypes.c_uint64,
                                              ctypes.c_uint32, P, ctypes.c_int, P, P]
         lib.fpo_count_mismatches.restype = None
         lib.fpo_scan_profile.argtypes = [P, P, ctypes.c_int, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32, P,
@@ -69,14 +72,46 @@ def _table(w: np.ndarray) -> tuple[np.ndarray, int]:
     return w, w.shape[1]
 
 
+def _fallback(fallback):
+    if fallback is None:
+        return None, 1.0, None
+    fb_b = None if fallback[2] is None else np.ascontiguousarray(fallback[2], dtype=np.float64)
+    return np.ascontiguousarray(fallback[0], dtype=np.float64), float(fallback[1]), fb_b
+
+
+def build_tours_sorted(sw: np.ndarray, si: np.ndarray, seed: int, iteration: int, ants, n: int | None = None,
+                       fallback: tuple | None = None, inv_gamma: float = 1.0) -> np.ndarray:
+    """Full-scan product-rule tours of the SORTED stream (the kernels that scan
+    the row-sorted table): uniforms keyed by the entry's position in the row.
+    sw / si: (n, ld) sorted values and their cities.  Otherwise as build_tours."""
+    sw, ld = _table(sw)
+    si = np.ascontiguousarray(si, dtype=np.uint16)
+    assert si.shape == sw.shape
+    n = sw.shape[0] if n is None else int(n)
+    ants = np.ascontiguousarray(np.asarray(ants, dtype=np.int64))
+    out = np.zeros((ants.size, n), dtype=np.int32)
+    fb_a, alpha, fb_b = _fallback(fallback)
+    fbs = np.zeros(1, dtype=np.int64)
+    fail = np.zeros(1, dtype=np.int32)
+    rc = _load().fpo_build_tours_sorted(_ptr(sw), _ptr(si), n, ld, int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                        int(iteration) & 0xFFFFFFFF, _ptr(ants), ants.size, _ptr(fb_a), alpha,
+                                        _ptr(fb_b), float(inv_gamma), _ptr(out), _ptr(fbs), _ptr(fail))
+    if rc == 2:
+        raise AssertionError("selector chose a visited city")
+    build_tours.last_fallbacks = int(fbs[0])
+    return out.astype(np.int64)
+
+
 def build_tours(w: np.ndarray, seed: int, iteration: int, ants, n: int | None = None,
                 fallback: tuple | None = None, inv_gamma: float = 1.0) -> np.ndarray:
-    """Full-scan product-rule tours (int64, one row per entry of `ants`).
+    """Full-scan product-rule tours of the DENSE stream (uniforms keyed by
+    city; int64, one row per entry of `ants`).
 
     w: (n, ldw) fp32 selection table (ldw >= n; pad columns ignored).
     fallback: (A, alpha, B or None), the f64 source the kernel falls back to
     when no W > 0 candidate is left (v = A^alpha * B); None: no source (the
     all -inf rule only).  Raises AssertionError like the reference (colony.py:149).
+    Both builders set build_tours.last_fallbacks.
     """
     w, ldw = _table(w)
     n = w.shape[0] if n is None else int(n)
@@ -111,19 +146,25 @@ def logu_table() -> np.ndarray:
     return _logu
 
 
-def count_mismatches(w: np.ndarray, logw: np.ndarray, seed: int, iteration: int, ants, tours) -> dict:
+def count_mismatches(w: np.ndarray, logw: np.ndarray, seed: int, iteration: int, ants, tours,
+                     si: np.ndarray | None = None) -> dict:
     """Selection-level agreement of recorded tours (the device's) with the
     product rule, the reference's log rule on the same uniforms and the log
-    rule on refined 53-bit uniforms (see fastpath.c fpo_count_mismatches)."""
+    rule on refined 53-bit uniforms (see fastpath.c fpo_count_mismatches).
+    w: the dense table, or with `si` the row-sorted table (sorted stream)."""
     w, ldw = _table(w)
     n = w.shape[0]
+    if si is not None:
+        si = np.ascontiguousarray(si, dtype=np.uint16)
+        assert si.shape == w.shape
     logw = np.ascontiguousarray(logw, dtype=np.float64)
     assert logw.shape == (n, n)
     ants = np.ascontiguousarray(np.asarray(ants, dtype=np.int64))
     tours = np.ascontiguousarray(tours, dtype=np.int32)
     assert tours.shape == (ants.size, n)
     out = np.zeros(5, dtype=np.int64)
-    _load().fpo_count_mismatches(_ptr(w), n, ldw, _ptr(logw), _ptr(logu_table()), int(seed) & 0xFFFFFFFFFFFFFFFF,
+    _load().fpo_count_mismatches(_ptr(w), _ptr(si), n, ldw, _ptr(logw), _ptr(logu_table()),
+                                 int(seed) & 0xFFFFFFFFFFFFFFFF,
                                  int(iteration) & 0xFFFFFFFF, _ptr(ants), ants.size, _ptr(tours), _ptr(out))
     return {"selections": int(out[0]), "product_rule": int(out[1]), "log_rule_same_u": int(out[2]),
             "log_rule_u53": int(out[3]), "u53_below_uniform_floor": int(out[4])}

@@ -164,8 +164,9 @@ static __device__ __noinline__ uint32_t fallback_pick(const Fallback *f, const P
 // kernels: their step loop leaves as soon as a step has no W > 0 candidate,
 // so neither this code nor its call weighs on the loop's registers).  Each
 // step scans the ant's FULL row — the same product rule argmax_j W * u over
-// unvisited j with W > 0, lowest j on ties, so every step the fast loop did
-// decide comes out identical — and steps without a candidate go to
+// unvisited j with W > 0, lowest j on ties, with the uniform of the same slot
+// (sorted position, or city for the dense table), so every step the fast loop
+// did decide comes out identical — and steps without a candidate go to
 // fallback_pick.  vals / idx: the row-sorted table (sw, si) or, idx NULL,
 // the dense table; ld: their row pitch.  Visited set as in fallback_pick
 // (cleared here: nwords 32-bit words of this ant).  Returns false when the
@@ -202,7 +203,8 @@ static __device__ __noinline__ bool rebuild_tour(const float *vals, const uint16
       const float w = vals[row + k];
       const uint32_t j = idx != nullptr ? (uint32_t)idx[row + k] : k;
       if (!(w > 0.0f) || seen(j)) continue;
-      const uint32_t key = __float_as_uint(__fmul_rn(w, bits_to_uniform(sel_word(j, step, ak, rk)))) + 1u;
+      // slot k: the sorted position (sorted table) or the city (dense table)
+      const uint32_t key = __float_as_uint(__fmul_rn(w, bits_to_uniform(sel_word(k, step, ak, rk)))) + 1u;
       if (key > bkey || (key == bkey && j < bj)) bkey = key, bj = j;
     }
     const uint32_t mkey = __reduce_max_sync(0xffffffffu, bkey);

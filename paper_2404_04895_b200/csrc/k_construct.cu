@@ -4,10 +4,14 @@
 // argmax_select_block selection.py:143-155, start cities rng.py:65-68, tour
 // lengths model.batch_costs model.py:292-295 (fused).
 //
-// Fast-path rule: next = argmax_j { W[cur, j] * u(step, ant, j) }
+// Fast-path rule: next = argmax_j { W[cur, j] * u(step, ant, s) }
 // over unvisited j with W[cur, j] > 0, first (lowest j) of ties, where
-// W = fp32(P^(1/gamma)) and u is the keyed Philox2x32-10 uniform.  This is the
-// product form of the reference's argmax(log P / gamma - E) with E = -log u.
+// W = fp32(P^(1/gamma)) and u is the keyed Philox2x32-10 uniform of slot s.
+// The slot is the entry's position in row cur of the row-sorted table for the
+// SORTED kernels (so a window's uniforms need no table data and are formed a
+// step ahead), and the city j for the DENSE kernel: two streams, each an
+// exact instance of the rule.  This is the product form of the reference's
+// argmax(log P / gamma - E) with E = -log u.
 //
 // Two variants compute the identical argmax:
 //   DENSE  streams the whole fp32 row W[cur, :] with 16-byte loads and draws
@@ -16,10 +20,10 @@
 //   SORTED scans the row's descending (W, j) table and stops as soon as the
 //          next table entry satisfies W < best score: since u < 1, no later
 //          entry can reach the running best, so the result is bit-identical to
-//          the full scan while touching only the head of the row.  Because the
-//          uniforms are counter-addressed by city, visiting candidates in
-//          sorted order draws exactly the values the full scan would.  The
-//          median step stops after 3 entries.
+//          the full scan of the table while touching only its head.  Because
+//          the uniforms are counter-addressed (by sorted position), visiting
+//          candidates in window order draws exactly the values the full scan
+//          would.  The median step stops after 3 entries.
 // The tour length, in numpy's pairwise order (bit-exact with batch_costs), is
 // either accumulated on the fly or computed by k_tour_cost afterwards.
 #include <algorithm>
@@ -122,10 +126,11 @@ __device__ __forceinline__ void score_window_u(float w, uint32_t j, const uint32
   }
 }
 
+// uniforms of the sorted-table stream are keyed by sorted position `pos`
 template <bool VIS8>
-__device__ __forceinline__ void score_window(float w, uint32_t j, const uint32_t *vis, uint32_t step,
+__device__ __forceinline__ void score_window(float w, uint32_t j, uint32_t pos, const uint32_t *vis, uint32_t step,
                                              const AntKey &ak, const RoundKeys &rk, float &best, uint32_t &bestj) {
-  score_window_u<VIS8>(w, j, vis, best, bestj, [&] { return sel_word(j, step, ak, rk); });
+  score_window_u<VIS8>(w, j, vis, best, bestj, [&] { return sel_word(pos, step, ak, rk); });
 }
 
 // The first window of the next row is issued as soon as the step's winner is
@@ -196,6 +201,10 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
     wg = __ldg(sw + (cur * (uint32_t)a.ld + lane));
     jg = __ldg(si + (cur * (uint32_t)a.ld + lane));
   }
+  // the first window's uniforms depend only on (step, sorted position =
+  // lane): each step's are formed in the previous step's shadow, while its
+  // window is in flight (C3 -5%, one ant per SM -10%)
+  uint32_t xnext = sel_word((uint32_t)lane, 1u, ak, rk);
   // the step's bookkeeping once its city is known: the next row's first
   // window is issued before it, so that L2 round trip overlaps it
   auto advance = [&](uint32_t bj, uint32_t stp) {
@@ -206,6 +215,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
       wg = __ldg(sw + (bj * (uint32_t)a.ld + e));
       jg = __ldg(si + (bj * (uint32_t)a.ld + e));
     }
+    xnext = sel_word(e, stp + 1, ak, rk);
     if (lane == 0) mark_visited<VIS8>(vis, bj);
     if (COST) {
       if (stp > 1) lc.push();  // edge stp-2, loaded one step ago
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
         const uint32_t sink = consume(wg) ^ jg;
         const long long pb = clock64();
         const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
-        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(sel_word(jg, step, ak, rk)))) + 1u : 0u;
+        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(sel_word((uint32_t)lane, step, ak, rk)))) + 1u : 0u;
         const uint32_t k2 = consume(__uint_as_float(key));
         const long long pc = clock64();
         const uint32_t mkey = __reduce_max_sync(kFull, k2);
@@ -252,9 +262,9 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
       }
 #endif
       if (base == 0) {
-        // first window: Philox issued ahead of the visited lookup and the vote;
-        // best is still -1, so no running-best test and the window's best wins
-        uint32_t x = sel_word(jg, step, ak, rk);
+        // first window: its uniforms were formed a step ahead (xnext); best
+        // is still -1, so no running-best test and the window's best wins
+        uint32_t x = xnext;
         asm volatile("" : "+r"(x));
         const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
         if (__any_sync(kFull, cand)) {
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
           best = __uint_as_float(mkey - 1u);
         }
       } else {
-        score_window<VIS8>(wg, jg, vis, step, ak, rk, best, bestj);
+        score_window<VIS8>(wg, jg, base + (uint32_t)lane, vis, step, ak, rk, best, bestj);
       }
       if (PROBE) ++windows;
       // entries after this window have W <= bucket_ceiling(window's last W)
@@ -426,7 +436,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
     uint32_t x[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      x[e] = sel_word(j[e], step, ak, rk);
+      x[e] = sel_word(chunk + (uint32_t)(gl * E + e), step, ak, rk);  // sorted position
       asm volatile("" : "+r"(x[e]));
     }
     bool cand[E];

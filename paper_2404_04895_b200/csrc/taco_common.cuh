@@ -16,9 +16,12 @@ namespace taco {
 //   key(seed, it) = H(seed) + it (mod 2^32), H = xor-fold of the MurmurHash3
 //                   64-bit finalizer of the seed: distinct iterations of a run
 //                   never share a key
-//   selection u(step >= 1, ant, city j):
-//                   counter (ant, (j >> 1) | step << 16), word j & 1
-//                   (n <= 65535: j >> 1 <= 0x7fff, step <= 0xfffe)
+//   selection u(step >= 1, ant, slot s):
+//                   counter (ant, (s >> 1) | step << 16), word s & 1
+//                   (n <= 65535: s >> 1 <= 0x7fff, step <= 0xfffe); the slot
+//                   is the entry's position in the current row of the
+//                   row-sorted table (sorted kernels) or the city (dense
+//                   kernel, and the fallback of steps without a W > 0 city)
 //   start city:     counter (ant, 0) (step 0 never selects), word 0, Lemire
 //   RW threshold:   counter (ant, 0xffff | step << 16), 53 bits of both words
 // Counter word 0 is the ant, so round 1's product is one per ant (AntKey) and
@@ -136,7 +139,7 @@ __device__ __forceinline__ uint32_t select_u32(uint32_t pred, uint32_t a, uint32
   return r;
 }
 
-// the selection uniform's raw word for city j at (step, ant)
+// the selection uniform's raw word for slot j (sorted position or city) at (step, ant)
 __device__ __forceinline__ uint32_t sel_word(uint32_t j, uint32_t step, const AntKey &ak, const RoundKeys &rk) {
   const uint2 r = philox_ant(sel_counter(j, step), ak, rk);
   return select_u32(j & 1u, r.y, r.x);

@@ -133,7 +133,7 @@ def convergence_generation(best_trace: list[float]) -> int:
 
 
 def run_experiment(config: ExperimentConfig, inst=None, clock=time.perf_counter,
-                   construct: str = "sorted") -> tuple[list[IterationRecord], list[RunSummary]]:
+                   construct: str = "auto") -> tuple[list[IterationRecord], list[RunSummary]]:
     """construct -> elite -> deposit -> evaporate -> P per iteration on the
     device, `repetitions` runs with seeds base..base+r-1."""
     if inst is None:

@@ -9,7 +9,9 @@ runs ITERS iterations; then, on its selection table for the next iteration:
   lane-group kernels g4e2 / g4e4 / g8e2 / g8e4 / g16e2, and the dense
   full-row kernel — is forced (the TACO_SORTED_* knobs) and its tours of a
   spread sample of global ant ids must equal the C oracle's full-scan
-  product rule (oracle/c/fastpath.c) bit for bit.  Ants are independent and
+  product rule (oracle/c/fastpath.c) bit for bit: the sorted stream
+  (uniforms keyed by sorted position) for the sorted-table kernels, the dense
+  stream (keyed by city) for the dense kernel.  Ants are independent and
   keyed by their global id, so restating a sample is exact.
 * the Solver's own next iteration (production kernel choice) must give the
   same sampled tours, their lengths bit-exact (numpy's pairwise order over
@@ -138,8 +140,12 @@ def test_construction_kernels_match_oracle_at_config(solvers, name):
     it, seed = s.iteration, s.params.seed
     ants = _sample(m, count)
     w = s.tables.w[:, :n].cpu().numpy()
-    want = fastpath_c.build_tours(w, seed, it, ants)
+    wants = {"sorted": fastpath_c.build_tours_sorted(s.tables.sw.cpu().numpy(), s.tables.si.cpu().numpy(), seed,
+                                                     it, ants, n=n)}
     assert fastpath_c.build_tours.last_fallbacks == 0
+    if name != "c5_65536":
+        wants["dense"] = fastpath_c.build_tours(w, seed, it, ants)
+        assert fastpath_c.build_tours.last_fallbacks == 0
     dev = s.dev
     tours = torch.zeros((m, n), dtype=torch.int32, device=dev)
     costs = torch.zeros(m, dtype=torch.float64, device=dev)
@@ -162,6 +168,7 @@ def test_construction_kernels_match_oracle_at_config(solvers, name):
             assert "unsupported" in str(e).lower(), (label, e)
             continue
         assert _device.read_status(status)[0] == 0, label
+        want = wants[variant]
         got = tours[torch.from_numpy(ants).to(dev)].cpu().numpy()
         assert np.array_equal(got, want), f"{name}/{label}: tours differ from the oracle"
         assert np.array_equal(costs[torch.from_numpy(ants).to(dev)].cpu().numpy(),
@@ -180,8 +187,7 @@ def test_solver_iteration_matches_reference_at_config(solvers, name):
     s = _solver(solvers, name)
     it, seed, p = s.iteration, s.params.seed, s.params
     ants = _sample(m, count)
-    w = s.tables.w[:, :n].cpu().numpy()
-    want = fastpath_c.build_tours(w, seed, it, ants)
+    want = fastpath_c.build_tours_sorted(s.tables.sw.cpu().numpy(), s.tables.si.cpu().numpy(), seed, it, ants, n=n)
     g = np.random.default_rng(it)
     rows = np.unique(np.concatenate([g.integers(0, n, 40), [0, n - 1]]))
     rows_t = torch.from_numpy(rows).to(s.dev)
@@ -232,11 +238,15 @@ def test_selection_mismatch_count_against_log_rule(solvers, name):
     gamma = taco.colony.construction_gamma(s.params, it)
     assert gamma != 1.0 or CONFIGS[name][2] == "ir"
     ants = _sample(m, 4 * count)
-    w = s.tables.w[:, :n].cpu().numpy()
+    sw, si = s.tables.sw.cpu().numpy(), s.tables.si.cpu().numpy()
     pmat = s.probability().p
     logw = ref.log_table(pmat, gamma)
-    tours = fastpath_c.build_tours(w, seed, it, ants).astype(np.int32)
-    c = fastpath_c.count_mismatches(w, logw, seed, it, ants, tours)
+    # the production (sorted-stream) choices, checked against the device first
+    tours = fastpath_c.build_tours_sorted(sw, si, seed, it, ants, n=n).astype(np.int32)
+    dev_tours = torch.zeros((m, n), dtype=torch.int32, device=s.dev)
+    _device.construct(n, m, 0, _lib.CONSTRUCT_SORTED, s.tables, seed, it, dev_tours, _device.new_status(s.dev))
+    assert np.array_equal(dev_tours[torch.from_numpy(ants).to(s.dev)].cpu().numpy(), tours)
+    c = fastpath_c.count_mismatches(sw, logw, seed, it, ants, tours, si=si)
     assert c["selections"] == ants.size * (n - 1)
     assert c["product_rule"] == 0
     rate = c["log_rule_same_u"] / c["selections"]

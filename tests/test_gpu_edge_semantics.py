@@ -110,8 +110,15 @@ def test_all_zero_candidates_take_city_zero_like_numpy(variant, env, monkeypatch
     half = n // 2
     assert side[batch.tours[:, :half]].all()
     assert (batch.tours[:, half] == 0).all()
-    w = fastpath.selection_table(p.p, 1.0)
-    assert np.array_equal(batch.tours, fastpath_c.build_tours(w, seed, 0, np.arange(m), fallback=(p.p, 1.0, None)))
+    dev = _device.device()
+    t = _device.SelectionTables(n, dev, dense=True, sorted_=True)
+    _device.selection_table_from_p(_device.upload(p.p, dev), 1.0, t)
+    if variant == "sorted":
+        want = fastpath_c.build_tours_sorted(t.sw.cpu().numpy(), t.si.cpu().numpy(), seed, 0, np.arange(m), n=n,
+                                             fallback=(p.p, 1.0, None))
+    else:
+        want = fastpath_c.build_tours(t.w.cpu().numpy(), seed, 0, np.arange(m), n=n, fallback=(p.p, 1.0, None))
+    assert np.array_equal(batch.tours, want)
     # the reference's own rule and streams agree on the semantics
     ref_tours = ref.build_tours(p.p, m, seed, 0, 1.0) if side[ref.start_block(seed, 0, m, n)].all() else None
     if ref_tours is not None:
@@ -177,13 +184,17 @@ def test_gamma_below_one_uses_the_f64_fallback(variant, m, env, monkeypatch):
     assert (np.sort(batch.tours, axis=1) == np.arange(n)).all()
     # the device table (fp32, row-scaled, zero below 2^-126 of the row's best)
     dev = _device.device()
-    t = _device.SelectionTables(n, dev, dense=True, sorted_=False)
+    t = _device.SelectionTables(n, dev, dense=True, sorted_=True)
     _device.selection_table_from_p(_device.upload(p, dev), 1.0 / gamma, t)
     w = t.w[:, :n].cpu().numpy()
     assert (w == 0).sum() > n  # far outside fp32's range relative to the row best
     assert np.abs(w.astype(np.float64) - fastpath.selection_table(p, gamma)).max() <= 2.0**-22
     ants = np.arange(m) if m <= 64 else np.unique(np.linspace(0, m - 1, 64).astype(np.int64))
-    want = fastpath_c.build_tours(w, 21, it, ants, fallback=(p, 1.0, None), inv_gamma=1.0 / gamma)
+    fb = dict(fallback=(p, 1.0, None), inv_gamma=1.0 / gamma)
+    if variant == "sorted":
+        want = fastpath_c.build_tours_sorted(t.sw.cpu().numpy(), t.si.cpu().numpy(), 21, it, ants, n=n, **fb)
+    else:
+        want = fastpath_c.build_tours(t.w.cpu().numpy(), 21, it, ants, n=n, **fb)
     assert fastpath_c.build_tours.last_fallbacks > 0  # the fallback really decided steps
     assert np.array_equal(batch.tours[ants], want)
     assert np.array_equal(batch.costs[ants], ref.lengths(want, inst.dist))
@@ -220,11 +231,14 @@ def test_row_scaled_table_keeps_tours_of_the_unscaled_rule():
                                 gamma_schedule=taco.GammaSchedule(gamma, gamma, 10))
         batch = taco.construct_tours(taco.ProbabilityMatrix(p), inst, params, 2)
         dev = _device.device()
-        t = _device.SelectionTables(n, dev, dense=True, sorted_=False)
+        t = _device.SelectionTables(n, dev, dense=True, sorted_=True)
         _device.selection_table_from_p(_device.upload(p, dev), 1.0 / gamma, t)
         w = t.w[:, :n].cpu().numpy()
         rowmax = w.max(axis=1)
         assert ((rowmax >= 1.0) & (rowmax <= 2.0)).all()
         scale = np.ldexp(1.0, np.frexp(p.max(axis=1) ** (1.0 / gamma))[1] - 1)
-        unscaled = (w.astype(np.float64) * scale[:, None]).astype(np.float32)  # exact: powers of two
-        assert np.array_equal(batch.tours, fastpath_c.build_tours(unscaled, 8, 2, np.arange(m)))
+        # exact: powers of two (and the sorted order, a function of the W bits
+        # above bit 16, is unchanged by them)
+        unscaled = (t.sw.cpu().numpy().astype(np.float64) * scale[:, None]).astype(np.float32)
+        assert np.array_equal(batch.tours, fastpath_c.build_tours_sorted(unscaled, t.si.cpu().numpy(), 8, 2,
+                                                                         np.arange(m), n=n))

@@ -169,9 +169,12 @@ def test_fast_construction_matches_restatement(n, m, gamma):
     assert (np.diff(si, axis=1)[same] > 0).all()
     assert (np.sort(si, axis=1) == np.arange(n)).all()
     seed, it = 11, 5
-    want = fastpath.build_tours(w, seed, it, np.arange(m))
+    # two streams: uniforms keyed by sorted position (sorted kernels) or by city (dense)
+    wants = {_lib.CONSTRUCT_SORTED: fastpath.build_tours_sorted(sw, si, seed, it, np.arange(m)),
+             _lib.CONSTRUCT_DENSE: fastpath.build_tours(w, seed, it, np.arange(m))}
     dist = _device.upload(inst.dist, t.w.device)
     for variant in (_lib.CONSTRUCT_SORTED, _lib.CONSTRUCT_DENSE):
+        want = wants[variant]
         tours = torch.zeros((m, n), dtype=torch.int32, device=t.w.device)
         costs = torch.zeros(m, dtype=torch.float64, device=t.w.device)
         status = _device.new_status(t.w.device)
@@ -188,22 +191,33 @@ def test_fast_rule_agrees_with_reference_log_rule():
     inst = euclid(5, n)
     p = ref.transition(ref.initial_tau(n, 1.0), inst.eta, 1.0, 2.0)
     params = taco.AcoParams(m=m, k=1, selection="ir", seed=4)
-    got = taco.construct_tours(taco.ProbabilityMatrix(p), inst, params, 2).tours
+    # the dense (city-keyed) stream; the sorted stream's count is in test_gpu_config_parity
+    got = taco.construct_tours(taco.ProbabilityMatrix(p), inst, params, 2, variant="dense").tours
     want = fastpath.log_rule_tours(p, 1.0, 4, 2, np.arange(m))
     mismatches = int((got != want).any(axis=1).sum())
     assert mismatches == 0
 
 
-def test_dense_and_sorted_agree_at_scale():
+def test_dense_and_sorted_match_their_oracles_at_scale():
+    from oracle import fastpath_c
+
     n, m = 1000, 256
     inst = euclid(1, n)
     params = taco.AcoParams(m=m, k=25, selection="adair", seed=3)
     p = taco.compute_probability_matrix(taco.PheromoneState.initial(n, 1.0), inst, params)
     a = taco.construct_tours(p, inst, params, 0, variant="sorted")
     b = taco.construct_tours(p, inst, params, 0, variant="dense")
-    assert np.array_equal(a.tours, b.tours)
-    assert np.array_equal(np.sort(a.tours, axis=1), np.broadcast_to(np.arange(n), (m, n)))
-    assert np.array_equal(a.costs, ref.lengths(a.tours, inst.dist))
+    t = _device_tables(p.p, taco.gamma_at(0, params.gamma_schedule))
+    ants = np.arange(m)
+    assert np.array_equal(a.tours, fastpath_c.build_tours_sorted(t.sw.cpu().numpy(), t.si.cpu().numpy(), 3, 0,
+                                                                 ants, n=n))
+    assert np.array_equal(b.tours, fastpath_c.build_tours(t.w.cpu().numpy(), 3, 0, ants, n=n))
+    for x in (a, b):
+        assert np.array_equal(np.sort(x.tours, axis=1), np.broadcast_to(np.arange(n), (m, n)))
+        assert np.array_equal(x.costs, ref.lengths(x.tours, inst.dist))
+    # two streams of the same rule: same tour-length distribution (KS)
+    from scipy import stats
+    assert stats.ks_2samp(a.costs, b.costs).pvalue > 1e-3
 
 
 # ---------------------------------------------------------------------------

@@ -251,6 +251,24 @@ def test_c_oracle_equals_numpy_restatement():
                     fastpath_c.build_tours(padded, 77, 3, ants, n=n, fallback=fb, inv_gamma=0.25)
                 continue
             assert np.array_equal(fastpath_c.build_tours(padded, 77, 3, ants, n=n, fallback=fb, inv_gamma=0.25), want)
+    # the sorted stream: uniforms keyed by the entry's position in the sorted row
+    for n in (5, 40, 201):
+        w = g.uniform(0.0, 1.0, (n, n)).astype(np.float32)
+        np.fill_diagonal(w, 0.0)
+        w[g.uniform(size=(n, n)) < 0.1] = 0.0
+        key = (w.view(np.uint32) >> 16).astype(np.int64)
+        si = np.argsort(-key, axis=1, kind="stable").astype(np.uint16)  # the kernels' row order
+        sw = np.take_along_axis(w, si.astype(np.int64), axis=1)
+        src = g.uniform(0.0, 1.0, (n, n))
+        for fb in (None, (src, 1.0, None)):
+            try:
+                want = fastpath.build_tours_sorted(sw, si, 5, 2, np.arange(9), fallback=fb, inv_gamma=0.5)
+            except AssertionError:
+                with pytest.raises(AssertionError):
+                    fastpath_c.build_tours_sorted(sw, si, 5, 2, np.arange(9), fallback=fb, inv_gamma=0.5)
+                continue
+            assert np.array_equal(fastpath_c.build_tours_sorted(sw, si, 5, 2, np.arange(9), fallback=fb,
+                                                                inv_gamma=0.5), want)
     # Philox and the key schedule
     ctr = np.array([[0, 0], [0xFFFFFFFF, 0xFFFFFFFF], [0x243F6A88, 0x85A308D3]], dtype=np.uint64)
     key = np.array([0, 0xFFFFFFFF, 0x13198A2E], dtype=np.uint64)
