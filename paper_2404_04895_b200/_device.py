@@ -7,6 +7,7 @@ without libtaco.so the calls raise.
 
 from __future__ import annotations
 
+import threading
 import warnings
 import weakref
 
@@ -30,8 +31,28 @@ def device() -> torch.device:
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_PINNED_STREAM = threading.local()
+
+
 def stream_handle() -> int:
-    return torch.cuda.current_stream().cuda_stream
+    """The current CUDA stream as a raw handle (a Solver pins it for the
+    launches of one iteration: torch's current_stream() lookup costs
+    microseconds per call, several per iteration)."""
+    h = getattr(_PINNED_STREAM, "handle", None)
+    return h if h is not None else torch.cuda.current_stream().cuda_stream
+
+
+class pinned_stream:
+    """Context: stream_handle() returns the stream current at entry."""
+
+    def __enter__(self):
+        self._prev = getattr(_PINNED_STREAM, "handle", None)
+        _PINNED_STREAM.handle = torch.cuda.current_stream().cuda_stream
+        return self
+
+    def __exit__(self, *exc):
+        _PINNED_STREAM.handle = self._prev
+        return False
 
 
 def new_status(dev) -> torch.Tensor:

@@ -361,6 +361,10 @@ class Solver:
 
     def _enqueue(self, timers: dict | None, scan_count: torch.Tensor | None) -> None:
         """Launch one iteration (eagerly, or into a graph being captured)."""
+        with _device.pinned_stream():
+            self._enqueue_launches(timers, scan_count)
+
+    def _enqueue_launches(self, timers: dict | None, scan_count: torch.Tensor | None) -> None:
         p, sh, it = self.params, self.shard, self.iteration
         st = self.state if self.graph else None
         lib = _lib.load()
