@@ -236,6 +236,8 @@ def run_ours(args) -> dict | None:
     from paper_2404_04895_b200 import _device, _lib
 
     n, m, selection = CONFIGS[args.config]
+    if args.weak:  # population scaling: the colony grows with the GPUs (m per GPU fixed)
+        m *= int(os.environ.get("WORLD_SIZE", "1"))
     if args.construct == "auto":  # the Solver's own choice (full-row kernel for tiny rows)
         args.construct = "dense" if n < taco.Solver.DENSE_MAX_N else "sorted"
     k = max(1, m // 10)
@@ -435,7 +437,7 @@ def run_ours(args) -> dict | None:
     line = {
         "metric": METRIC, "value": it_per_s, "unit": "iterations/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64+f32",
+        "higher_is_better": True, "scaling": "weak" if args.weak else "strong", "vs_baseline": None, "dtype": "f64+f32",
         "data": "synthetic: U(0,2000)^2 Euclidean cities (seed 0), unrounded distances",
         "config": _config_dict(args.config, n, m, k, selection, period, world),
         "construct": "rw" if rw else args.construct,
@@ -506,6 +508,8 @@ def run_reference(args) -> dict | None:
     from oracle import cpu_baseline
 
     n, m, selection = CONFIGS[args.config]
+    if args.weak:
+        m *= world
     k = max(1, m // 10)
     period = args.warmup + args.steps  # the same gamma schedule as our arm
     host = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
@@ -535,7 +539,7 @@ def run_reference(args) -> dict | None:
            f"(SURVEY 8(d))")
     return {
         "metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "strong",
+        "warmup": args.warmup, "ms_per_step": 1000.0 / value, "higher_is_better": True, "scaling": "weak" if args.weak else "strong",
         "vs_baseline": None, "dtype": "f64", "impl": "reference",
         "timing": "measured" if as_is else "extrapolated",
         "data": "synthetic: U(0,2000)^2 Euclidean cities (seed 0), unrounded distances",
@@ -560,6 +564,9 @@ def main() -> None:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-steps", type=int, default=6)
     ap.add_argument("--ref-procs", type=int, default=0, help="reference arm processes (0: all host cores)")
+    ap.add_argument("--weak", action="store_true",
+                    help="weak (population) scaling: the config's m ants per GPU, m x N in total; default strong "
+                         "(the config's colony split over the GPUs)")
     args = ap.parse_args()
     if args.warmup < 0 or args.steps < 1:
         ap.error("need --steps >= 1 and --warmup >= 0")
