@@ -58,6 +58,7 @@ struct LeafCost {
   // lane 0 starts loading the length of edge (a, b); it is parked one step later
   __device__ __forceinline__ void load(uint32_t a, uint32_t b) {
     // 32-bit index: n <= 65535, so a * n + b < 2^32 (one IMAD instead of 64-bit math)
+    TACO_DCHECK(!active || (a < (uint32_t)n && b < (uint32_t)n));
     if (active && lane == 0) pending = __ldg(dist + (a * (uint32_t)n + b));
   }
   __device__ __forceinline__ void push() {
@@ -91,6 +92,7 @@ __device__ __forceinline__ double warp_tour_cost(int n, const int32_t *trow, con
     ls[L] = pw_leaf_sum(lf.y, [&](int q) {
       const int s = lf.x + q;
       const int s1 = (s + 1 == n) ? 0 : s + 1;
+      TACO_DCHECK((uint32_t)trow[s] < (uint32_t)n && (uint32_t)trow[s1] < (uint32_t)n);
       return __ldg(dist + ((uint32_t)trow[s] * (uint32_t)n + (uint32_t)trow[s1]));
     });
   }
@@ -215,6 +217,7 @@ static __device__ __noinline__ bool rebuild_tour(const float *vals, const uint16
       nxt = fallback_pick(f, ks, state, it, gant, n, cur, step, 32, lane, 1, vis, vis8, stride, offset);
       if (nxt == 0xffffffffu) return false;
     }
+    TACO_DCHECK(nxt < n && !seen(nxt));
     if (lane == 0) {
       mark(nxt);
       trow[step] = (int32_t)nxt;

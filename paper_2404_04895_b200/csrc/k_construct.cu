@@ -298,6 +298,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
       stalled = true;
       break;
     }
+    TACO_DCHECK(bestj < un && !(lane == 0 && visited_at<VIS8>(vis, bestj)));
     advance(bestj, step);
 #ifdef TACO_STEP_PROFILE
     const long long t3 = clock64();
@@ -482,6 +483,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
         stalled = true;
         alive = false;
       } else {
+        TACO_DCHECK(bestj < un && !((vis[(bestj >> 5) * A + g] >> (bestj & 31)) & 1u));
         if (gl == 0) {
           vis[(bestj >> 5) * A + g] |= 1u << (bestj & 31);
           trow[step] = (int32_t)bestj;
@@ -621,6 +623,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
       break;
     }
     const uint32_t bestj = __reduce_min_sync(kFull, lkey == mkey ? lj : 0xffffffffu);
+    TACO_DCHECK(bestj < (uint32_t)n && !is_visited(vis, bestj));
     if (lane == 0) vis[bestj >> 5] |= 1u << (bestj & 31);
     if (step > 1) lc.push();
     lc.load(cur, bestj);

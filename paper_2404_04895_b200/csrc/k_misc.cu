@@ -90,6 +90,9 @@ __global__ void k_elite_neighbors(int n, int k, const TourT *__restrict__ tours,
   const int city = (int)t[s];
   const int prev = (int)t[s == 0 ? n - 1 : s - 1];
   const int next = (int)t[s + 1 == n ? 0 : s + 1];
+  // a failed construction leaves partial rows (the iteration's update is then
+  // skipped through status[3]): never index with them
+  if ((unsigned)city >= (unsigned)n || (unsigned)prev >= (unsigned)n || (unsigned)next >= (unsigned)n) return;
   nbr[(size_t)city * k + r] = make_int2(prev, next);  // city-major: row i reads k contiguous pairs
   if (s == 0) inc[r] = __ddiv_rn(1.0, costs[a]);  // pheromone.py:66 inc = 1.0 / cost
 }

@@ -169,6 +169,7 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_row_update(RowParams a,
               const int2 nb = nb_stage[e >> 1];
               col = (e & 1) ? nb.y : nb.x;
               v = inc_stage[e >> 1];
+              TACO_DCHECK((unsigned)col < (unsigned)n && col != i);
             }
             const unsigned peers = __match_any_sync(0xffffffffu, col);
             // every lane folds its column group in lane (= rank) order; the

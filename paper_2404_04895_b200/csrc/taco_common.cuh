@@ -4,8 +4,28 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 
 #include "../../include/taco.h"
+
+// Device-side index checks of the debug build (-DTACO_DEBUG_CHECKS,
+// scripts/debug_checks.sh): compute-sanitizer is closed on this GPU pool, so
+// the GPU suite runs once against a library that traps on any out-of-range
+// city / column index the kernels are about to use.  Compiled out otherwise.
+#ifdef TACO_DEBUG_CHECKS
+#define TACO_DCHECK(cond)                                                                        \
+  do {                                                                                          \
+    if (!(cond)) {                                                                              \
+      printf("TACO_DCHECK failed: %s at %s:%d (block %d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)threadIdx.x);                                                \
+      __trap();                                                                                 \
+    }                                                                                           \
+  } while (0)
+#else
+#define TACO_DCHECK(cond) \
+  do {                    \
+  } while (0)
+#endif
 
 namespace taco {
 
