@@ -376,6 +376,10 @@ def run_ours(args) -> dict | None:
     peak, peak_kind = _peaks()
     sharded = solver.shard.world > 1
     launches_per_iter = 5 + (0 if rw else 1) + (1 if solver.graph else 0) + (1 if sharded else 0)
+    sms_ = torch.cuda.get_device_properties(dev).multi_processor_count
+    # > 32 ants per SM on the warp kernel (MODE 2): + the k_rebuild_stalled follow-up
+    mode2 = (not rw and args.construct == "sorted" and 32 * sms_ < solver.shard.count <= 64 * sms_)
+    launches_per_iter += 1 if mode2 else 0
     m_local = solver.shard.count
     # roofline.achieved = ALGORITHMIC bytes per launch / launch time, with the
     # per-unit figure of SURVEY §8(d): each ant streams its current row of the
@@ -463,7 +467,8 @@ def run_ours(args) -> dict | None:
                      "what": "as e2e, with K blocking Solver.step() calls (host waits for every iteration)"},
         "gpu_launches": args.steps * launches_per_iter,
         "gpu_launches_note": (f"{launches_per_iter} libtaco kernels per iteration: k_construct_"
-                              f"{'rw' if rw else args.construct} (or the lane-group variant), k_elite_rank, "
+                              f"{'rw' if rw else args.construct} (or the lane-group variant)"
+                              f"{' + k_rebuild_stalled' if mode2 else ''}, k_elite_rank, "
                               "k_track_best, k_elite_neighbors, k_row_update"
                               f"{'' if rw else ', k_row_sort'}{', k_iter_advance' if solver.graph else ''}"
                               f"{', k_shard_elites (+ NCCL collectives)' if sharded else ''}"
