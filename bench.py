@@ -380,6 +380,7 @@ def run_ours(args) -> dict | None:
     # > 32 ants per SM on the warp kernel (MODE 2): + the k_rebuild_stalled follow-up
     mode2 = (not rw and args.construct == "sorted" and 32 * sms_ < solver.shard.count <= 64 * sms_)
     launches_per_iter += 1 if mode2 else 0
+    launches_per_iter += 2 if solver._split_update else 0  # deposit + evaporation + normalization
     m_local = solver.shard.count
     # roofline.achieved = ALGORITHMIC bytes per launch / launch time, with the
     # per-unit figure of SURVEY §8(d): each ant streams its current row of the
@@ -469,7 +470,8 @@ def run_ours(args) -> dict | None:
         "gpu_launches_note": (f"{launches_per_iter} libtaco kernels per iteration: k_construct_"
                               f"{'rw' if rw else args.construct} (or the lane-group variant)"
                               f"{' + k_rebuild_stalled' if mode2 else ''}, k_elite_rank, "
-                              "k_track_best, k_elite_neighbors, k_row_update"
+                              "k_track_best, k_elite_neighbors, "
+                              f"{'k_deposit_rows, k_evap_unnorm, k_row_normalize' if solver._split_update else 'k_row_update'}"
                               f"{'' if rw else ', k_row_sort'}{', k_iter_advance' if solver.graph else ''}"
                               f"{', k_shard_elites (+ NCCL collectives)' if sharded else ''}"
                               f"{' (+ CUB radix-sort kernels: m > 16384)' if m > 16384 else ''}; "
