@@ -836,11 +836,14 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     // g8e2 | g16e2 overrides (tuning knob)
     int G = 0, E = 0;
     // Measured on B200 at n = 2392 (scripts/sweep_kernel_choice.sh): the warp
-    // kernel wins up to ~64 ants per SM (m = 8192: 4.38 vs 4.79 ms); beyond
-    // that the SIMT sharing of the lane-group kernel wins (m = 12288: 6.03 vs
-    // 6.52 ms).
-    if (m_local > 64 * sm_count()) G = 8, E = 2;
-    if (m_local > 200 * sm_count()) G = 4, E = 4;  // n = 5000, m = 65536: 44.9 vs 51.1 ms
+    // kernel wins up to ~64 ants per SM (m = 8192: 2.93 vs 3.04 ms for g4e4);
+    // beyond that the SIMT sharing of the lane-group kernel wins.
+    // With position-keyed uniforms (independent of the table loads) four
+    // entries per lane win everywhere above 64 ants per SM (round 2, ms, g4e4
+    // vs g8e2): n = 5000 m = 12288 8.06 vs 12.02, m = 16384 10.16 vs 12.46,
+    // m = 32768 16.39 vs 21.50; n = 2392 m = 16384 4.53 vs 5.70; n = 1000
+    // m = 32768 2.95 vs 3.80
+    if (m_local > 64 * sm_count()) G = 4, E = 4;
     if (const char *ev = getenv("TACO_SORTED_KERNEL")) {
       G = 0;
       if (ev[0] == 'g') {
