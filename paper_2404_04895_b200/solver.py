@@ -160,6 +160,12 @@ class Solver:
         # (rows past the fused row kernel's shared memory take the replicated
         # split update)
         self.partitioned = update == "partitioned" and world > 1 and n <= self.FUSED_MAX_N
+        if self.partitioned and Selection(p.selection) is Selection.ADAIR and p.gamma_schedule.gamma_min < 1.0:
+            # steps left without a W > 0 city are decided from the row's
+            # tau^alpha eta^beta (include/taco.h), which a row-partitioned rank
+            # holds only for its own rows
+            raise ValueError("update='partitioned' needs gamma >= 1 (gamma_min < 1 can leave steps to the f64 "
+                             "fallback, which reads every row of tau); use update='replicated'")
         # row partition: this rank updates rows [begin, end); the row buffers
         # carry world * chunk rows so the table all-gather has equal chunks
         self._part = row_partition(n, rank, world) if self.partitioned else row_partition(n, 0, 1)
