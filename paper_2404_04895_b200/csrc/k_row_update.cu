@@ -52,26 +52,35 @@ struct RowParams {
 #endif
 constexpr int kDepositChunk = TACO_DEPOSIT_CHUNK;  // elites staged in shared memory per pass
 constexpr int kBatch = 4;           // tau / eta^b loads in flight per thread
+#ifndef TACO_COLUMNS_MAX
+#define TACO_COLUMNS_MAX 256
+#endif
+constexpr int kColumnsMax = TACO_COLUMNS_MAX;  // column-parallel deposit up to this many distinct columns
 
 // Shared-memory layout (bytes, all regions 16-B aligned):
 //   row      double[n]        delta, then unnorm (also the CUB sort workspace)
 //   plan     leaves int2[L], left/right/order u16[L], level_start int[42],
 //            leaf_sum double[L], ival double[L], hgt u8[L]
 //   stage    int2[kDepositChunk], double[kDepositChunk]
+//   deposit  column bit map u32[ceil(n/32)], distinct columns int[dcap]
 struct RowLayout {
-  size_t row_bytes, plan_off, stage_off, total;
+  size_t row_bytes, plan_off, stage_off, bm_off, cols_off, total;
+  int dcap;
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 
-__host__ __device__ inline RowLayout row_layout(int n, int L, size_t sort_bytes) {
+__host__ __device__ inline RowLayout row_layout(int n, int L, size_t sort_bytes, int dcap = 0) {
   RowLayout l;
   l.row_bytes = align16((size_t)8 * n > sort_bytes ? (size_t)8 * n : sort_bytes);
   l.plan_off = l.row_bytes;
   const size_t plan = align16((size_t)8 * L) + 3 * align16((size_t)2 * L) + align16(4 * (kMaxPlanHeight + 2)) +
                       2 * align16((size_t)8 * L) + align16((size_t)L);
   l.stage_off = l.plan_off + plan;
-  l.total = l.stage_off + (size_t)16 * kDepositChunk;
+  l.bm_off = l.stage_off + (size_t)16 * kDepositChunk;
+  l.cols_off = l.bm_off + (dcap > 0 ? align16((size_t)4 * ((n + 31) / 32)) : 0);
+  l.dcap = dcap;
+  l.total = l.cols_off + align16((size_t)4 * dcap);
   return l;
 }
 
@@ -101,6 +110,9 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_row_update(RowParams a,
   uint8_t *hgt = pp;
   int2 *nb_stage = reinterpret_cast<int2 *>(smem + lay.stage_off);
   double *inc_stage = reinterpret_cast<double *>(nb_stage + kDepositChunk);
+  uint32_t *dep_bm = reinterpret_cast<uint32_t *>(smem + lay.bm_off);
+  int *dep_cols = reinterpret_cast<int *>(smem + lay.cols_off);
+  __shared__ int s_ndist;
   __shared__ int s_meta[4];  // n_leaves, n_internal, height of the plan; fail-stop flag
   __shared__ double s_wmax[BLOCK / 32];  // per-warp row maxima (selection-table scale)
 
@@ -144,7 +156,69 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_row_update(RowParams a,
     load_batch(tid);
 
     // ---- delta row ---------------------------------------------------------
-    if (a.nbr != nullptr) {
+    // Column-parallel form (lay.dcap > 0): the row's distinct deposit
+    // columns (prev / next of city i in the k elites) are collected first,
+    // then each thread owns one of them and walks all k elites in rank
+    // order, adding inc_r where the column matches: per column the same
+    // sequence ((0 + inc_a) + inc_b) + ... as the reference's per-elite fancy
+    // += (pheromone.py:62-67; one cell is hit at most once per elite), with
+    // the columns in parallel instead of warp 0 folding 2k entries while the
+    // CTA waits (the deposit was 34% of the C3 update, 40% at C4; now half
+    // that).  Real colonies have few distinct columns per row (median 42 at
+    // C3 from the first iterations, 55 at C4); rows with more than
+    // kColumnsMax (random elites) keep the warp fold, which suits them.
+    bool dep_done = false;
+    if (a.nbr != nullptr && lay.dcap > 0) {
+      const int nw = (n + 31) >> 5;
+      for (int w = tid; w < nw; w += BLOCK) dep_bm[w] = 0u;
+      for (int j = tid; j < n; j += BLOCK) row[j] = 0.0;
+      if (tid == 0) s_ndist = 0;
+      __syncthreads();
+      const int2 *nbi = a.nbr + (size_t)i * a.k;
+      for (int r = tid; r < a.k; r += BLOCK) {
+        const int2 p = nbi[r];
+        TACO_DCHECK((unsigned)p.x < (unsigned)n && (unsigned)p.y < (unsigned)n && p.x != i && p.y != i);
+        atomicOr(&dep_bm[p.x >> 5], 1u << (p.x & 31));
+        atomicOr(&dep_bm[p.y >> 5], 1u << (p.y & 31));
+      }
+      __syncthreads();
+      for (int w = tid; w < nw; w += BLOCK) {
+        uint32_t bits = dep_bm[w];
+        if (bits) {
+          int at = atomicAdd(&s_ndist, __popc(bits));
+          while (bits) {
+            const int b = __ffs(bits) - 1;
+            if (at < lay.dcap) dep_cols[at] = (w << 5) + b;
+            ++at;
+            bits &= bits - 1u;
+          }
+        }
+      }
+      __syncthreads();
+      const int nd = s_ndist;
+      if (nd <= lay.dcap && nd <= kColumnsMax && nd <= BLOCK) {  // else the warp fold below
+        dep_done = true;
+        const int c = tid < nd ? dep_cols[tid] : -2;
+        double acc = 0.0;
+        for (int rbase = 0; rbase < a.k; rbase += kDepositChunk) {
+          const int rcount = min(kDepositChunk, a.k - rbase);
+          __syncthreads();
+          for (int r = tid; r < rcount; r += BLOCK) {
+            nb_stage[r] = nbi[rbase + r];
+            inc_stage[r] = a.inc[rbase + r];
+          }
+          __syncthreads();
+          if (tid < nd) {
+            for (int r = 0; r < rcount; ++r) {
+              const int2 p = nb_stage[r];
+              if (p.x == c || p.y == c) acc = __dadd_rn(acc, inc_stage[r]);
+            }
+          }
+        }
+        if (c >= 0) row[c] = acc;
+      }
+    }
+    if (a.nbr != nullptr && !dep_done) {
       for (int j = tid; j < n; j += BLOCK) row[j] = 0.0;
       for (int rbase = 0; rbase < a.k; rbase += kDepositChunk) {
         const int rcount = min(kDepositChunk, a.k - rbase);
@@ -327,8 +401,19 @@ static int launch_row_t(const RowParams &a, const RowLayout &lay, cudaStream_t s
   return TACO_OK;
 }
 
+#ifndef TACO_DEPOSIT_WARP
+#define TACO_DEPOSIT_COLUMNS 1
+#endif
+
 static int launch_row(const RowParams &a, cudaStream_t stream) {
-  const RowLayout lay = row_layout(a.n, a.n_leaves > 0 ? a.n_leaves : 1, 0);
+  int dcap = 0;  // the column-parallel deposit (0: the warp fold)
+#ifdef TACO_DEPOSIT_COLUMNS
+  if (a.nbr != nullptr && a.k > 0) {
+    dcap = 2 * a.k < a.n - 1 ? 2 * a.k : a.n - 1;
+    if (dcap > kColumnsMax) dcap = kColumnsMax;  // more distinct columns: the warp fold
+  }
+#endif
+  const RowLayout lay = row_layout(a.n, a.n_leaves > 0 ? a.n_leaves : 1, 0, dcap);
   if (lay.total > 227 * 1024) return TACO_ERR_UNSUPPORTED;
   // CTA width by row length (scripts/row_update_probe.py): 256 threads are
   // best up to n ~ 5000 (n = 2392: 153 us vs 154 / 211 for 128 / 512 with the
