@@ -251,15 +251,6 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_row_update(RowParams a,
             // group's additions (no shared-memory round trip per element)
             const bool leader = col >= 0 && lane == __ffs(peers) - 1;
             if (__any_sync(0xffffffffu, __popc(peers) > 1)) {
-#ifdef TACO_DEPOSIT_FIXED32
-              double acc = leader ? row[col] : 0.0;
-#pragma unroll
-              for (int t = 0; t < 32; ++t) {
-                const double x = __shfl_sync(0xffffffffu, v, t);
-                if ((peers >> t) & 1u) acc = __dadd_rn(acc, x);
-              }
-              if (leader) row[col] = acc;
-#else
               // leaders walk their group's lanes in increasing (= rank) order;
               // as many rounds as the largest group (not 32)
               unsigned rem = leader ? peers : 0u;
@@ -273,7 +264,6 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_row_update(RowParams a,
                 rem &= rem - 1u;
               }
               if (leader) row[col] = acc;
-#endif
             } else if (leader) {  // no shared column in this window
               row[col] = __dadd_rn(row[col], v);
             }
