@@ -103,8 +103,9 @@ class Solver:
     rows of tau / P / the selection table and the table rows are
     all-gathered: 6n^2 B per iteration).
     graph: replay a captured CUDA graph per iteration (default: on for a
-    single-GPU device-stream colony with n*m < 2^16, where launch
-    overhead matters; the sharded and replay modes always run eagerly).
+    single-GPU device-stream colony; the sharded and replay modes always run
+    eagerly).  Measured per iteration, eager -> graph: C1 0.192 -> 0.183 ms,
+    C2 -1.9%, C3 1.588 -> 1.578 ms, C4 15.53 -> 15.50 ms.
     graph_warmup: eager iterations before the first capture (default
     GRAPH_WARMUP = 32: a short run does not pay a capture it cannot
     amortize; 0 captures at the second iteration).
@@ -112,7 +113,6 @@ class Solver:
 
     GRAPH_BATCH = 8  # iterations per graph replay in run()
     GRAPH_WARMUP = 32  # eager iterations before the first capture
-    GRAPH_MAX_WORK = 1 << 16  # default graph mode below this many (city x ant) selections per iteration
     FUSED_MAX_N = 27000  # the fused row kernel stages a row of n doubles in shared memory
     # construct="auto": the full-row kernel below this n (no row sort; n = 51,
     # m = 64: 0.040 vs 0.044 ms per iteration; even at n = 100; sorted from 200)
@@ -249,11 +249,11 @@ class Solver:
                                        dtype=torch.float64, device=dev)
         self.state = torch.zeros(32, dtype=torch.uint8, device=dev)  # taco_iter_state
         self._write_state(0)
-        # default: graphs where launch overhead is a visible share of the
-        # iteration (small colonies: C1 9.5k -> 16.7k it/s; at C2 the gain is 3%
-        # and a capture, ~2-10 ms, costs more than it saves in short runs)
+        # default: graphs on one GPU (small colonies: 9.5k -> 16.7k it/s; the
+        # launch gaps still cost 0.6% at C3); GRAPH_WARMUP keeps the capture,
+        # ~2-10 ms, out of runs too short to amortize it
         if graph is None:
-            use_graph = world == 1 and stream == "device" and n * p.m < self.GRAPH_MAX_WORK
+            use_graph = world == 1 and stream == "device"
         else:
             use_graph = bool(graph)
         if use_graph and (world > 1 or stream != "device"):
