@@ -8,11 +8,13 @@
  * What it restates (the reference rule it approximates is
  * argmax_j(log P[cur, j] / gamma - E[a, j]) over unvisited j, first of ties,
  * selection.py:143-155 / colony.py:126-152 of /root/reference/pkg/src/antbatch):
- *   - Philox2x32-10 (Random123), key = H(seed) + iteration, counter
- *     (ant, (s >> 1) | step << 16), word s & 1;  u = ((x >> 9) + 1/2) 2^-23;
- *     the slot s is the city j (dense stream, fpo_build_tours) or the entry's
- *     position in row cur of the row-sorted table (sorted stream,
- *     fpo_build_tours_sorted)
+ *   - Philox2x32-10 (Random123), key = H(seed) + iteration;
+ *     u = ((x >> 9) + 1/2) 2^-23 of the word x of
+ *       dense stream (fpo_build_tours; slot s = the city j):
+ *         counter (ant, (s >> 1) | step << 16), word s & 1
+ *       sorted stream (fpo_build_tours_sorted; slot p = the entry's position
+ *       in row cur of the row-sorted table):
+ *         counter (ant, p | ((step + 1) >> 1) << 16), word (step + 1) & 1
  *   - start city: Lemire bound of word 0 of counter (ant, 0)
  *   - next = argmax_j fp32(W[cur, j] * u_slot(j)) over unvisited j with W > 0,
  *     lowest j on ties (a FULL scan: no pruning)
@@ -75,6 +77,23 @@ static inline void pair_words(uint32_t q, uint32_t step, uint32_t ant, uint32_t 
   philox2x32_10(ant, q | (step << 16), key, r);
 }
 
+/* the sorted stream's word of position p at (step, ant) */
+static inline uint32_t pos_word(uint32_t p, uint32_t step, uint32_t ant, uint32_t key) {
+  uint32_t r[2];
+  philox2x32_10(ant, p | (((step + 1u) >> 1) << 16), key, r);
+  return r[(step + 1u) & 1u];
+}
+
+/* the words of slots 2q, 2q+1 of either stream */
+static inline void slot_words(int sorted, uint32_t q, uint32_t step, uint32_t ant, uint32_t key, uint32_t r[2]) {
+  if (sorted) {
+    r[0] = pos_word(2 * q, step, ant, key);
+    r[1] = pos_word(2 * q + 1, step, ant, key);
+  } else {
+    pair_words(q, step, ant, key, r);
+  }
+}
+
 static inline double fb_value(const double *a, double alpha, const double *b, size_t off) {
   /* numpy's scalar-power dispatch for the exponents the engine uses */
   const double x = a[off];
@@ -116,7 +135,7 @@ static int one_tour(const float *w, const uint16_t *idx, int n, int ldw, uint32_
       }
       if (!c[0] && !c[1]) continue;
       uint32_t r[2];
-      pair_words((uint32_t)q, step, ant, key, r);
+      slot_words(irow != NULL, (uint32_t)q, step, ant, key, r);
       for (int e = 0; e < 2; ++e) {
         if (!c[e]) continue;
         const float s = row[2 * q + e] * bits_to_uniform(r[e]);
@@ -246,7 +265,7 @@ void fpo_count_mismatches(const float *w, const uint16_t *idx, int n, int ldw, c
             any |= slot < n && !seen[irow ? irow[slot] : slot];
           }
           if (!any) continue;
-          pair_words((uint32_t)q, step, ant, key, r);
+          slot_words(irow != NULL, (uint32_t)q, step, ant, key, r);
           for (int e = 0; e < 2; ++e) {
             const int slot = 2 * q + e;
             if (slot >= n) continue;
@@ -337,9 +356,7 @@ void fpo_scan_profile(const float *sw, const uint16_t *si, int n, int ld, uint64
             wl = w;
             if (e >= n || !(w > 0.0f) || seen[ir[e]] || w < best) continue;
             const uint32_t j = ir[e];
-            uint32_t r[2];
-            pair_words((uint32_t)e >> 1, step, ant, key, r); /* slot = sorted position */
-            const float s = w * bits_to_uniform(r[e & 1]);
+            const float s = w * bits_to_uniform(pos_word((uint32_t)e, step, ant, key)); /* sorted position */
             if (s > best || (s == best && (int)j < bj)) best = s, bj = (int)j;
           }
           if (bucket_ceiling(wl) < best || !(wl > 0.0f)) break;

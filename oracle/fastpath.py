@@ -69,6 +69,20 @@ def uniforms(seed: int, iteration: int, step, ant, city) -> np.ndarray:
     return bits_to_uniform(pick)
 
 
+def position_uniforms(seed: int, iteration: int, step, ant, pos) -> np.ndarray:
+    """The sorted stream's u(seed, iteration, step, ant, sorted position).
+    Counter (ant, pos | ((step + 1) >> 1) << 16), word (step + 1) & 1: one
+    block serves a position at steps 2t - 1 and 2t."""
+    step, ant, pos = np.broadcast_arrays(np.asarray(step, dtype=np.uint64),
+                                         np.asarray(ant, dtype=np.uint64),
+                                         np.asarray(pos, dtype=np.uint64))
+    pair = (step + np.uint64(1)) >> np.uint64(1)
+    ctr = np.stack([ant, (pos | (pair << np.uint64(16))) & np.uint64(MASK32)], axis=-1)
+    words = philox2x32_10(ctr, stream_key(seed, iteration))
+    pick = np.where((step & np.uint64(1)) == 1, words[..., 0], words[..., 1])
+    return bits_to_uniform(pick)
+
+
 def starts(seed: int, iteration: int, ants, n: int) -> np.ndarray:
     """Device start cities: Lemire bound of word 0 of counter (ant, 0)."""
     ants = np.asarray(ants, dtype=np.uint64)
@@ -206,7 +220,7 @@ def build_tours_sorted(sw: np.ndarray, si: np.ndarray, seed: int, iteration: int
     tours[:, 0] = cur
     slots = np.arange(n, dtype=np.uint64)
     for step in range(1, n):
-        u = uniforms(seed, iteration, step, ants[:, None], slots[None, :])  # by position
+        u = position_uniforms(seed, iteration, step, ants[:, None], slots[None, :])
         wr = sw[cur][:, :n]
         jr = si[cur][:, :n].astype(np.int64)
         score = wr * u

@@ -206,7 +206,8 @@ static __device__ __noinline__ bool rebuild_tour(const float *vals, const uint16
       const uint32_t j = idx != nullptr ? (uint32_t)idx[row + k] : k;
       if (!(w > 0.0f) || seen(j)) continue;
       // slot k: the sorted position (sorted table) or the city (dense table)
-      const uint32_t key = __float_as_uint(__fmul_rn(w, bits_to_uniform(sel_word(k, step, ak, rk)))) + 1u;
+      const uint32_t x = idx != nullptr ? pos_word(k, step, ak, rk) : sel_word(k, step, ak, rk);
+      const uint32_t key = __float_as_uint(__fmul_rn(w, bits_to_uniform(x))) + 1u;
       if (key > bkey || (key == bkey && j < bj)) bkey = key, bj = j;
     }
     const uint32_t mkey = __reduce_max_sync(0xffffffffu, bkey);

@@ -9,14 +9,15 @@
 // W = fp32(P^(1/gamma)) and u is the keyed Philox2x32-10 uniform of slot s.
 // The slot is the entry's position in row cur of the row-sorted table for the
 // SORTED kernels (so a window's uniforms need no table data and are formed a
-// step ahead), and the city j for the DENSE kernel: two streams, each an
+// step ahead; one block serves a position at two consecutive steps), and the
+// city j for the DENSE kernel: two streams, each an
 // exact instance of the rule.  This is the product form of the reference's
 // argmax(log P / gamma - E) with E = -log u.
 //
 // Two variants compute the identical argmax:
 //   DENSE  streams the whole fp32 row W[cur, :] with 16-byte loads and draws
-//          four uniforms per Philox block (the north-star "row streaming"
-//          kernel; ALU bound on Philox).
+//          four uniforms per two Philox blocks (the north-star "row
+//          streaming" kernel; ALU bound on Philox).
 //   SORTED scans the row's descending (W, j) table and stops as soon as the
 //          next table entry satisfies W < best score: since u < 1, no later
 //          entry can reach the running best, so the result is bit-identical to
@@ -130,7 +131,7 @@ __device__ __forceinline__ void score_window_u(float w, uint32_t j, const uint32
 template <bool VIS8>
 __device__ __forceinline__ void score_window(float w, uint32_t j, uint32_t pos, const uint32_t *vis, uint32_t step,
                                              const AntKey &ak, const RoundKeys &rk, float &best, uint32_t &bestj) {
-  score_window_u<VIS8>(w, j, vis, best, bestj, [&] { return sel_word(pos, step, ak, rk); });
+  score_window_u<VIS8>(w, j, vis, best, bestj, [&] { return pos_word(pos, step, ak, rk); });
 }
 
 // The first window of the next row is issued as soon as the step's winner is
@@ -204,7 +205,12 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
   // the first window's uniforms depend only on (step, sorted position =
   // lane): each step's are formed in the previous step's shadow, while its
   // window is in flight (C3 -5%, one ant per SM -10%)
-  uint32_t xnext = sel_word((uint32_t)lane, 1u, ak, rk);
+  uint32_t xnext, xstash;  // step s's word; word 1 of the block of odd step s - 1
+  {
+    const uint2 b = pos_block((uint32_t)lane, 1u, ak, rk);
+    xnext = b.x;
+    xstash = b.y;
+  }
   // the step's bookkeeping once its city is known: the next row's first
   // window is issued before it, so that L2 round trip overlaps it
   auto advance = [&](uint32_t bj, uint32_t stp) {
@@ -215,7 +221,13 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
       wg = __ldg(sw + (bj * (uint32_t)a.ld + e));
       jg = __ldg(si + (bj * (uint32_t)a.ld + e));
     }
-    xnext = sel_word(e, stp + 1, ak, rk);
+    if (stp & 1u) {  // step stp + 1 is even: word 1 of the block formed at stp
+      xnext = xstash;
+    } else {
+      const uint2 b = pos_block(e, stp + 1, ak, rk);
+      xnext = b.x;
+      xstash = b.y;
+    }
     if (lane == 0) mark_visited<VIS8>(vis, bj);
     if (COST) {
       if (stp > 1) lc.push();  // edge stp-2, loaded one step ago
@@ -247,7 +259,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
         const uint32_t sink = consume(wg) ^ jg;
         const long long pb = clock64();
         const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
-        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(sel_word((uint32_t)lane, step, ak, rk)))) + 1u : 0u;
+        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(pos_word((uint32_t)lane, step, ak, rk)))) + 1u : 0u;
         const uint32_t k2 = consume(__uint_as_float(key));
         const long long pc = clock64();
         const uint32_t mkey = __reduce_max_sync(kFull, k2);
@@ -437,7 +449,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
     uint32_t x[E];
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      x[e] = sel_word(chunk + (uint32_t)(gl * E + e), step, ak, rk);  // sorted position
+      x[e] = pos_word(chunk + (uint32_t)(gl * E + e), step, ak, rk);  // sorted position
       asm volatile("" : "+r"(x[e]));
     }
     bool cand[E];

@@ -37,11 +37,14 @@ namespace taco {
 //                   64-bit finalizer of the seed: distinct iterations of a run
 //                   never share a key
 //   selection u(step >= 1, ant, slot s):
+//                   dense stream, slot s = the city (dense kernel, and the
+//                   fallback of steps without a W > 0 city):
 //                   counter (ant, (s >> 1) | step << 16), word s & 1
-//                   (n <= 65535: s >> 1 <= 0x7fff, step <= 0xfffe); the slot
-//                   is the entry's position in the current row of the
-//                   row-sorted table (sorted kernels) or the city (dense
-//                   kernel, and the fallback of steps without a W > 0 city)
+//                   (n <= 65535: s >> 1 <= 0x7fff, step <= 0xfffe);
+//                   sorted stream, slot p = the entry's position in the
+//                   current row of the row-sorted table (sorted kernels):
+//                   counter (ant, p | ((step + 1) >> 1) << 16), word
+//                   (step + 1) & 1 (pos_block / pos_word)
 //   start city:     counter (ant, 0) (step 0 never selects), word 0, Lemire
 //   RW threshold:   counter (ant, 0xffff | step << 16), 53 bits of both words
 // Counter word 0 is the ant, so round 1's product is one per ant (AntKey) and
@@ -163,6 +166,19 @@ __device__ __forceinline__ uint32_t select_u32(uint32_t pred, uint32_t a, uint32
 __device__ __forceinline__ uint32_t sel_word(uint32_t j, uint32_t step, const AntKey &ak, const RoundKeys &rk) {
   const uint2 r = philox_ant(sel_counter(j, step), ak, rk);
   return select_u32(j & 1u, r.y, r.x);
+}
+
+// the sorted stream's uniforms (slot = sorted position p): counter
+// (ant, p | ((step + 1) >> 1) << 16), word (step + 1) & 1 -- one block serves
+// position p at steps 2t - 1 (word 0) and 2t (word 1), so the sorted kernels'
+// first-window uniforms cost one block per lane every second step
+__device__ __forceinline__ uint2 pos_block(uint32_t p, uint32_t step, const AntKey &ak, const RoundKeys &rk) {
+  return philox_ant(p | (((step + 1u) >> 1) << 16), ak, rk);
+}
+
+__device__ __forceinline__ uint32_t pos_word(uint32_t p, uint32_t step, const AntKey &ak, const RoundKeys &rk) {
+  const uint2 r = pos_block(p, step, ak, rk);
+  return select_u32(step & 1u, r.x, r.y);
 }
 
 __device__ __forceinline__ uint32_t start_city(uint32_t n, const AntKey &ak, const RoundKeys &rk) {

@@ -142,6 +142,13 @@ def test_stream_keys_and_counters():
     w = fastpath.philox2x32_10(np.array([[0, 2 | 1 << 16], [0, 2 | 2 << 16]], dtype=np.uint64),
                                fastpath.stream_key(9, 2))
     assert np.array_equal(u, fastpath.bits_to_uniform(np.array([w[0, 0], w[0, 1], w[1, 0]])))
+    # sorted stream: position p at steps 2t - 1 and 2t shares counter
+    # (ant, p | t << 16), words 0 and 1; t >= 1, so never the start counter
+    # (ant, 0), and p <= 65534 never reaches RW_LOW
+    u = fastpath.position_uniforms(9, 2, np.array([1, 2, 3, 4]), np.array([7, 7, 7, 7]), np.array([5, 5, 5, 5]))
+    w = fastpath.philox2x32_10(np.array([[7, 5 | 1 << 16], [7, 5 | 2 << 16]], dtype=np.uint64),
+                               fastpath.stream_key(9, 2))
+    assert np.array_equal(u, fastpath.bits_to_uniform(np.array([w[0, 0], w[0, 1], w[1, 0], w[1, 1]])))
 
 
 def test_uniform_conversion_is_exact_and_open():
