@@ -273,6 +273,9 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
         }
       }
 #endif
+      // entries after this window have W <= bucket_ceiling(window's last W);
+      // the shuffle is issued first so that it overlaps the scoring
+      const float wl = __shfl_sync(kFull, wg, 31);
       if (base == 0) {
         // first window: its uniforms were formed a step ahead (xnext); best
         // is still -1, so no running-best test and the window's best wins
@@ -289,8 +292,6 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
         score_window<VIS8>(wg, jg, base + (uint32_t)lane, vis, step, ak, rk, best, bestj);
       }
       if (PROBE) ++windows;
-      // entries after this window have W <= bucket_ceiling(window's last W)
-      const float wl = __shfl_sync(kFull, wg, 31);
       base += 32;
       done = (bucket_ceiling(wl) < best) || (wl <= 0.0f) || (base >= un);
       if (!done) {
