@@ -12,6 +12,7 @@
 // (contiguous: the edge map is city-major).  The row lives in shared memory
 // between the phases so tau / unnorm are touched once.
 #include <cstdlib>
+#include <string>
 
 #include <cub/block/block_radix_sort.cuh>
 
@@ -45,6 +46,7 @@ struct RowParams {
   int32_t *status;
   int n_leaves;
   int row_begin, row_end;  // rows [row_begin, row_end) of the n x n matrices (row-partitioned update)
+  const unsigned char *plan_image;  // nullable: the pairwise plan prebuilt for n (plan_image_bytes)
 };
 
 #ifndef TACO_DEPOSIT_CHUNK
@@ -69,6 +71,14 @@ struct RowLayout {
 };
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// the plan's tables (leaves, left, right, order, level_start) as laid out at
+// the start of the plan region, followed by int meta[4] (n_leaves,
+// n_internal, height): prebuilt once per n (k_plan_image) and copied by each
+// CTA instead of built by one thread (a ~10 us serial prologue per launch)
+__host__ __device__ inline size_t plan_tables_bytes(int L) {
+  return align16((size_t)8 * L) + 3 * align16((size_t)2 * L) + align16(4 * (kMaxPlanHeight + 2));
+}
 
 __host__ __device__ inline RowLayout row_layout(int n, int L, size_t sort_bytes, int dcap = 0) {
   RowLayout l;
@@ -123,8 +133,15 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_row_update(RowParams a,
   const double inv_gamma = a.state != nullptr ? a.state->inv_gamma : a.inv_gamma;
   const bool have_delta = (a.nbr != nullptr) || (a.delta_in != nullptr);
 
-  // the pairwise tree depends only on n: build it once per CTA
-  if (need_sum && tid == 0) {
+  // the pairwise tree depends only on n: copied from its prebuilt image, or
+  // built once per CTA
+  if (need_sum && a.plan_image != nullptr) {
+    const int words = (int)(plan_tables_bytes(L) / 16);
+    const int4 *src = reinterpret_cast<const int4 *>(a.plan_image);
+    int4 *dst = reinterpret_cast<int4 *>(smem + lay.plan_off);
+    for (int q = tid; q < words; q += BLOCK) dst[q] = src[q];
+    if (tid < 3) s_meta[tid] = reinterpret_cast<const int *>(a.plan_image + plan_tables_bytes(L))[tid];
+  } else if (need_sum && tid == 0) {
     pw_plan_build(n, plan, hgt);
     s_meta[0] = plan.n_leaves;
     s_meta[1] = plan.n_internal;
@@ -357,6 +374,53 @@ __global__ void __launch_bounds__(BLOCK, 1024 / BLOCK) k_row_update(RowParams a,
 
 static int sm_count_row() { return device_sm_count(); }
 
+__global__ void k_plan_image(int n, int L, unsigned char *img) {
+  PwPlan p;
+  unsigned char *q = img;
+  p.leaves = reinterpret_cast<int2 *>(q);
+  q += align16((size_t)8 * L);
+  p.left = reinterpret_cast<uint16_t *>(q);
+  q += align16((size_t)2 * L);
+  p.right = reinterpret_cast<uint16_t *>(q);
+  q += align16((size_t)2 * L);
+  p.order = reinterpret_cast<uint16_t *>(q);
+  q += align16((size_t)2 * L);
+  p.level_start = reinterpret_cast<int *>(q);
+  int *meta = reinterpret_cast<int *>(img + plan_tables_bytes(L));
+  pw_plan_build(n, p, reinterpret_cast<uint8_t *>(meta + 4));
+  meta[0] = p.n_leaves;
+  meta[1] = p.n_internal;
+  meta[2] = p.height;
+}
+
+// the plan image for n on the current device (built on `stream` at first
+// use; never freed: a few KB per distinct n).  Null while the stream is being
+// captured and no image exists yet (the kernel then builds the plan itself).
+static const unsigned char *plan_image(int n, int L, cudaStream_t stream) {
+  constexpr int kSlots = 8;
+  static int ns[kMaxDevices][kSlots] = {};
+  static unsigned char *imgs[kMaxDevices][kSlots] = {};
+  const int dev = current_device();
+  for (int q = 0; q < kSlots; ++q)
+    if (ns[dev][q] == n && imgs[dev][q] != nullptr) return imgs[dev][q];
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return nullptr;
+  int slot = -1;
+  for (int q = 0; q < kSlots && slot < 0; ++q)
+    if (imgs[dev][q] == nullptr) slot = q;
+  if (slot < 0) return nullptr;  // many distinct n in one process: build in the kernel
+  unsigned char *img = nullptr;
+  if (cudaMalloc(&img, plan_tables_bytes(L) + 16 + align16((size_t)L)) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return nullptr;
+  }
+  k_plan_image<<<1, 1, 0, stream>>>(n, L, img);
+  if (cudaGetLastError() != cudaSuccess) return nullptr;
+  ns[dev][slot] = n;
+  imgs[dev][slot] = img;
+  return img;
+}
+
 template <int BLOCK>
 static int launch_row_t(const RowParams &a, const RowLayout &lay, cudaStream_t stream) {
   // per device: the shared-memory attribute and the occupancy query
@@ -395,7 +459,11 @@ static int launch_row_t(const RowParams &a, const RowLayout &lay, cudaStream_t s
 #define TACO_DEPOSIT_COLUMNS 1
 #endif
 
-static int launch_row(const RowParams &a, cudaStream_t stream) {
+static int launch_row(RowParams a, cudaStream_t stream) {
+  a.plan_image = nullptr;
+#ifndef TACO_NO_PLAN_IMAGE
+  if (a.want_p && !a.p_given && a.n_leaves > 0) a.plan_image = plan_image(a.n, a.n_leaves, stream);
+#endif
   int dcap = 0;  // the column-parallel deposit (0: the warp fold)
 #ifdef TACO_DEPOSIT_COLUMNS
   if (a.nbr != nullptr && a.k > 0) {
@@ -429,8 +497,8 @@ static int launch_row(const RowParams &a, cudaStream_t stream) {
 #define TACO_SORT_RADIX_BITS 5  // 5-bit digits: -2% at n = 2392, -5% at n = 10000 vs 4 (6: slower; 8: no shared memory)
 #endif
 
-template <int BLOCK, int ITEMS>
-__global__ void __launch_bounds__(BLOCK) k_row_sort(int n, int row_begin, int row_end, int ldw,
+template <int BLOCK, int ITEMS, int MINB = 0>
+__global__ void __launch_bounds__(BLOCK, MINB) k_row_sort(int n, int row_begin, int row_end, int ldw,
                                                     const float *__restrict__ w, float *__restrict__ sw,
                                                     uint16_t *__restrict__ si) {
   using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, cub::NullType, TACO_SORT_RADIX_BITS>;
@@ -461,7 +529,7 @@ __global__ void __launch_bounds__(BLOCK) k_row_sort(int n, int row_begin, int ro
   }
 }
 
-template <int BLOCK, int ITEMS>
+template <int BLOCK, int ITEMS, int MINB = 0>
 static int launch_sort_t(int n, int r0, int r1, int ldw, const float *w, float *sw, uint16_t *si,
                          cudaStream_t stream) {
   using Sort = cub::BlockRadixSort<uint32_t, BLOCK, ITEMS, cub::NullType, TACO_SORT_RADIX_BITS>;
@@ -475,13 +543,13 @@ static int launch_sort_t(int n, int r0, int r1, int ldw, const float *w, float *
   if (configured != smem) {
     if (smem > 48 * 1024) {
       const cudaError_t e =
-          cudaFuncSetAttribute(k_row_sort<BLOCK, ITEMS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+          cudaFuncSetAttribute(k_row_sort<BLOCK, ITEMS, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) {
         note_cuda_error(e);
         return TACO_ERR_CUDA;
       }
     }
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_row_sort<BLOCK, ITEMS>, BLOCK, smem) !=
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, k_row_sort<BLOCK, ITEMS, MINB>, BLOCK, smem) !=
             cudaSuccess ||
         blocks_per_sm < 1)
       blocks_per_sm = 1;
@@ -491,12 +559,21 @@ static int launch_sort_t(int n, int r0, int r1, int ldw, const float *w, float *
   const int rows = r1 - r0;
   if (rows <= 0) return TACO_OK;
   const int grid = rows < sms * blocks_per_sm ? rows : sms * blocks_per_sm;
-  k_row_sort<BLOCK, ITEMS><<<grid, BLOCK, smem, stream>>>(n, r0, r1, ldw, w, sw, si);
+  k_row_sort<BLOCK, ITEMS, MINB><<<grid, BLOCK, smem, stream>>>(n, r0, r1, ldw, w, sw, si);
   TACO_CUDA_CHECK_LAUNCH();
   return TACO_OK;
 }
 
 static int launch_sort(int n, int r0, int r1, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t s) {
+  if (const char *ev = getenv("TACO_SORT_CFG")) {  // tuning knob: BLOCKxITEMS[xMINB]
+    const std::string c(ev);
+    if (c == "256x20" && n <= 5120) return launch_sort_t<256, 20>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "512x20x2" && n <= 10240) return launch_sort_t<512, 20, 2>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "1024x10" && n <= 10240) return launch_sort_t<1024, 10>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "256x10x4" && n <= 2560) return launch_sort_t<256, 10, 4>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "128x20" && n <= 2560) return launch_sort_t<128, 20>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "512x5" && n <= 2560) return launch_sort_t<512, 5>(n, r0, r1, ldw, w, sw, si, s);
+  }
   if (n <= 1024) return launch_sort_t<128, 8>(n, r0, r1, ldw, w, sw, si, s);
   if (n <= 2560) return launch_sort_t<256, 10>(n, r0, r1, ldw, w, sw, si, s);
   if (n <= 5120) return launch_sort_t<512, 10>(n, r0, r1, ldw, w, sw, si, s);
