@@ -1,3 +1,10 @@
+"""Row-update launch timing by row count (taco_row_update_rows, rows [0, R)):
+separates the per-launch fixed cost (R = 148: one row per CTA) from the
+per-row cost.  A sleep kernel ahead of each timed launch hides the host's
+launch latency.  Random elites (the warp-fold deposit) or none.
+
+    python scripts/row_range_probe.py <n> <k>
+"""
 import ctypes, os, sys
 import numpy as np, torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
