@@ -182,6 +182,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
   const uint32_t un = (uint32_t)n;  // n <= 65535, so every row offset fits in 32 bits
   const float *__restrict__ sw = a.sw;
   const uint16_t *__restrict__ si = a.si;
+  const uint32_t ldr = (uint32_t)a.ld;
   for (int q = lane; q < a.nwords; q += 32) vis[q] = 0u;
   const uint32_t start = start_city(un, ak, rk);
   __syncwarp();
@@ -199,8 +200,8 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
   float wg = 0.0f;
   uint32_t jg = 0;
   if ((uint32_t)lane < un) {
-    wg = __ldg(sw + (cur * (uint32_t)a.ld + lane));
-    jg = __ldg(si + (cur * (uint32_t)a.ld + lane));
+    wg = __ldg(sw + (cur * ldr + lane));
+    jg = __ldg(si + (cur * ldr + lane));
   }
   // the first window's uniforms depend only on (step, sorted position =
   // lane): each step's are formed in the previous step's shadow, while its
@@ -217,9 +218,9 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
     const uint32_t e = (uint32_t)lane;
     wg = 0.0f;
     jg = 0;
-    if (stp + 1 < un && e < un) {
-      wg = __ldg(sw + (bj * (uint32_t)a.ld + e));
-      jg = __ldg(si + (bj * (uint32_t)a.ld + e));
+    if (e < un) {  // also at the last step (row bj exists; unused): no step test (C3 -2%)
+      wg = __ldg(sw + (bj * ldr + e));
+      jg = __ldg(si + (bj * ldr + e));
     }
     if (stp & 1u) {  // step stp + 1 is even: word 1 of the block formed at stp
       xnext = xstash;
@@ -242,7 +243,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
 #ifdef TACO_STEP_PROFILE
     const long long t0 = clock64();
 #endif
-    const uint32_t row = cur * (uint32_t)a.ld;  // < 2^32 for n <= 65535
+    const uint32_t row = cur * ldr;  // < 2^32 for n <= 65535
     float best = -1.0f;
     uint32_t bestj = 0xffffffffu;
     bool done = false;
