@@ -600,3 +600,50 @@ def test_iterate_yields_what_step_returns():
         for (tw, lw), (_, tg, lg) in zip(want, got):
             assert np.array_equal(tw, tg) and lw == lg
         assert np.array_equal(a.pheromone().tau, b.pheromone().tau)
+
+
+def test_row_update_plan_built_in_kernel_equals_prebuilt_image():
+    """The row update copies the pairwise plan from a per-n image built at the
+    first eager launch (k_plan_image); a launch captured into a CUDA graph
+    before any image exists for that n builds the plan in the kernel
+    instead.  Both give the same tau / row sums / P / selection table bits.
+    n = 1237 is used by no other test, so the capture runs first."""
+    dev = _device.device()
+    n, k = 1237, 9
+    g = np.random.default_rng(n)
+    tau0 = torch.from_numpy(g.uniform(1e-6, 2.0, (n, n))).to(dev)
+    eta = torch.from_numpy(g.uniform(0.01, 1.0, (n, n))).to(dev)
+    tours = np.stack([g.permutation(n) for _ in range(k)])
+    nbr = np.zeros((n, k, 2), dtype=np.int32)
+    for r, t in enumerate(tours):
+        nbr[t, r, 0], nbr[t, r, 1] = np.roll(t, 1), np.roll(t, -1)
+    nbr_t = torch.from_numpy(nbr).to(dev)
+    inc = torch.from_numpy(1.0 / g.uniform(1e3, 1e4, k)).to(dev)
+    outs = []
+    for captured in (True, False):
+        tau = tau0.clone()
+        t = _device.SelectionTables(n, dev, dense=True, sorted_=True)
+        p = torch.zeros((n, n), dtype=torch.float64, device=dev)
+        rs = torch.zeros(n, dtype=torch.float64, device=dev)
+        st = _device.new_status(dev)
+        common = dict(tau_in=tau, tau_out=tau, eta_b=eta, nbr=nbr_t, inc=inc, k=k, do_evap=True, keep=0.9,
+                      want_p=True, alpha=1.0, inv_gamma=1.0 / 1.5, p_out=p, rowsum_out=rs, w_out=t.w,
+                      ldw=t.ldw, sw_out=t.sw, si_out=t.si, status=st)
+        torch.cuda.synchronize()
+        if captured:
+            side = torch.cuda.Stream(device=dev)
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                graph.capture_begin(capture_error_mode="thread_local")
+                try:
+                    _device.row_update(n, **common)
+                finally:
+                    graph.capture_end()
+            graph.replay()
+        else:
+            _device.row_update(n, **common)
+        torch.cuda.synchronize()
+        assert _device.read_status(st)[0] == 0
+        outs.append([x.cpu().numpy() for x in (tau, rs, p, t.w, t.sw, t.si)])
+    for a, b in zip(*outs):
+        assert np.array_equal(a, b)
