@@ -9,6 +9,20 @@ namespace taco {
 
 constexpr unsigned kFull = 0xffffffffu;
 
+// The pairwise-tree leaves of length n, prebuilt once per n and device (the
+// head of k_row_update.cu's plan image); null while the stream is being
+// captured before that image exists.  Kernels copy them instead of having
+// thread 0 walk the tree (a serial, local-memory prologue per CTA).
+const int2 *leaves_image(int n, cudaStream_t stream);
+
+__device__ __forceinline__ void load_leaves(int n, int L, int2 *leaves, const int2 *img) {
+  if (img != nullptr) {
+    for (int q = threadIdx.x; q < L; q += blockDim.x) leaves[q] = img[q];
+  } else if (threadIdx.x == 0) {
+    pw_leaves(n, leaves);
+  }
+}
+
 struct TourWriter {
   // lane (step & 31) buffers the choice of `step`; every 32 steps the warp
   // writes one coalesced 128-byte segment of the tour row.

@@ -59,6 +59,7 @@ struct SortedArgs {
   unsigned long long *scan_count;
   PhiloxKeys ks;
   Fallback fb;  // no W > 0 candidate left (construct_common.cuh)
+  const int2 *leaves_img;  // nullable (construct_common.cuh leaves_image)
 };
 
 constexpr int kSortedMaxWarps = 28;      // fused tour length: 72 registers per thread
@@ -177,7 +178,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
     vis = reinterpret_cast<uint32_t *>(mine + ls_bytes);
   }
 
-  if (a.costs != nullptr && threadIdx.x == 0) pw_leaves(n, leaves);
+  if (a.costs != nullptr) load_leaves(n, a.n_leaves, leaves, a.leaves_img);
   __syncthreads();
 
   const int ant = blockIdx.x * warps + warp;
@@ -387,6 +388,7 @@ struct GroupArgs {
   unsigned long long *scan_count;  // optional traffic probe (32-entry windows)
   PhiloxKeys ks;
   Fallback fb;
+  const int2 *leaves_img;  // nullable (construct_common.cuh leaves_image)
 };
 
 
@@ -406,7 +408,7 @@ __global__ void __launch_bounds__(kGroupWarps * 32) k_construct_group(const __gr
   unsigned char *wp = smem + off + per_warp * warp;
   uint32_t *vis = reinterpret_cast<uint32_t *>(wp);  // [nwords][A]: conflict-free per ant
   double *leaf_sum = reinterpret_cast<double *>(wp + (((size_t)4 * a.nwords * A + 15) & ~(size_t)15));
-  if (threadIdx.x == 0) pw_leaves(n, leaves);
+  load_leaves(n, L, leaves, a.leaves_img);
   for (int q = lane; q < a.nwords * A; q += 32) vis[q] = 0u;
   __syncthreads();
 
@@ -562,6 +564,7 @@ struct DenseArgs {
   int32_t *status;
   PhiloxKeys ks;
   Fallback fb;
+  const int2 *leaves_img;  // nullable (construct_common.cuh leaves_image)
 };
 
 // Shared memory: int2 leaves[n_leaves]; per ant: double leaf_buf[kPwBlock],
@@ -578,7 +581,7 @@ __global__ void __launch_bounds__(WARPS * 32) k_construct_dense(const __grid_con
   double *leaf_buf = reinterpret_cast<double *>(mine);
   double *leaf_sum = leaf_buf + kPwBlock;
   uint32_t *vis = reinterpret_cast<uint32_t *>(leaf_sum + a.n_leaves);
-  if (threadIdx.x == 0) pw_leaves(n, leaves);
+  load_leaves(n, a.n_leaves, leaves, a.leaves_img);
   __syncthreads();
   const int ant = blockIdx.x * WARPS + warp;
   if (ant >= a.m_local) return;
@@ -695,7 +698,7 @@ __global__ void __launch_bounds__(kRebuildWarps * 32) k_rebuild_stalled(const __
   int2 *leaves = reinterpret_cast<int2 *>(smem);
   uint32_t *vis = reinterpret_cast<uint32_t *>(smem + lb + per_warp * warp);
   double *leaf_sum = reinterpret_cast<double *>(smem + lb + per_warp * warp + (((size_t)4 * nwords + 15) & ~(size_t)15));
-  if (threadIdx.x == 0) pw_leaves(a.n, leaves);
+  load_leaves(a.n, a.n_leaves, leaves, a.leaves_img);
   __syncthreads();
   if (!mine) return;
   const uint32_t it = a.state != nullptr ? a.state->iteration : a.iteration;
@@ -881,7 +884,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
       const size_t smem = leaves_bytes + per_warp * kGroupWarps;
       if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
       GroupArgs ga{n, m_local, ant_offset, nwords, n_leaves, ldw, sw, si, dist, iteration, state,
-                   tours_out, costs_out, status, scan_count, ks, fb};
+                   tours_out, costs_out, status, scan_count, ks, fb, leaves_image(n, s)};
       const int ants_per_cta = (int)A * kGroupWarps;
       const int grid = (m_local + ants_per_cta - 1) / ants_per_cta;
 #define TACO_GROUP_CASE(GG, EE)                                                                         \
@@ -948,7 +951,8 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     const size_t smem = lb + scratch(vis8 ? nwords8 : nwords) * warps;
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
     SortedArgs a{n, m_local, ant_offset, vis8 ? nwords8 : nwords, n_leaves, ldw, sw, si, dist, iteration, state,
-                 tours_out, separate_cost ? nullptr : costs_out, status, scan_count, ks, fb};
+                 tours_out, separate_cost ? nullptr : costs_out, status, scan_count, ks, fb,
+                 costs_out != nullptr ? leaves_image(n, s) : nullptr};
     const int grid = (m_local + warps - 1) / warps;
     const int mode = fused_cost ? 0 : (two_ctas ? 2 : (wide ? 3 : 1));
     const int code = mode * 4 + (vis8 ? 2 : 0) + (scan_count ? 1 : 0);
@@ -982,7 +986,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
     if (smem > 227 * 1024) return TACO_ERR_UNSUPPORTED;
     if (set_smem((const void *)k_construct_dense<WARPS>, smem) != TACO_OK) return TACO_ERR_CUDA;
     DenseArgs a{n, m_local, ant_offset, ldw, nwords, n_leaves, w, dist, iteration, state, tours_out, costs_out,
-                status, ks, fb};
+                status, ks, fb, leaves_image(n, s)};
     k_construct_dense<WARPS><<<(m_local + WARPS - 1) / WARPS, WARPS * 32, smem, s>>>(a);
   } else {
     return TACO_ERR_ARG;

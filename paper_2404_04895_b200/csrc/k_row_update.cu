@@ -459,6 +459,10 @@ static int launch_row_t(const RowParams &a, const RowLayout &lay, cudaStream_t s
 #define TACO_DEPOSIT_COLUMNS 1
 #endif
 
+const int2 *leaves_image(int n, cudaStream_t stream) {
+  return reinterpret_cast<const int2 *>(plan_image(n, pw_num_leaves(n), stream));
+}
+
 static int launch_row(RowParams a, cudaStream_t stream) {
   a.plan_image = nullptr;
 #ifndef TACO_NO_PLAN_IMAGE
