@@ -292,18 +292,25 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
         uint32_t x = xnext;
         asm volatile("" : "+r"(x));
         const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
+        base = 32;
         if (__any_sync(kFull, cand)) {
           const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(x))) + 1u : 0u;
           const uint32_t mkey = __reduce_max_sync(kFull, key);
-          bestj = __reduce_min_sync(kFull, key == mkey ? jg : 0xffffffffu);
+          const uint32_t jsel = key == mkey ? jg : 0xffffffffu;
           best = __uint_as_float(mkey - 1u);
+          // the stop test needs only the max: it runs while the min reduction
+          // is in flight (C3 -1%, one ant per SM -3%)
+          done = (bucket_ceiling(wl) < best) || (wl <= 0.0f) || (base >= un);
+          bestj = __reduce_min_sync(kFull, jsel);
+        } else {
+          done = (wl <= 0.0f) || (base >= un);
         }
       } else {
         score_window<VIS8>(wg, jg, base + (uint32_t)lane, vis, step, ak, rk, best, bestj);
+        base += 32;
+        done = (bucket_ceiling(wl) < best) || (wl <= 0.0f) || (base >= un);
       }
       if (PROBE) ++windows;
-      base += 32;
-      done = (bucket_ceiling(wl) < best) || (wl <= 0.0f) || (base >= un);
       if (!done) {
         const uint32_t e = base + lane;
         wg = 0.0f;
