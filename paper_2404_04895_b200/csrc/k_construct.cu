@@ -75,6 +75,10 @@ constexpr int kSortedMaxWarps = 28;      // fused tour length: 72 registers per 
 #define TACO_MODE2_WARPS 32
 #endif
 constexpr int kMode1Warps = TACO_MODE1_WARPS;
+#ifndef TACO_LATENCY_ANTS
+#define TACO_LATENCY_ANTS 24
+#endif
+constexpr int kLatencyAnts = TACO_LATENCY_ANTS;  // MODE 4 up to this many ants per SM
 constexpr int kMode2Warps = TACO_MODE2_WARPS;  // 2 CTAs per SM: 65536 / (64 x this) registers
 
 #ifdef TACO_STEP_PROFILE
@@ -151,12 +155,19 @@ __device__ __forceinline__ void score_window(float w, uint32_t j, uint32_t pos, 
 // warps per SM (72 registers); 3: the same with 29-32 warps (64 registers);
 // 2: separate length, two CTAs of ceil(ants per SM / 2) <= 32 warps per SM
 // (<= 32 registers: the compiler rematerializes more, so only for > 32
-// ants per SM).
+// ants per SM); 4: MODE 1 for few ants per SM, latency-bound rather than
+// issue-bound, with the next row's window issued ahead of the stall test.
 template <bool PROBE, bool VIS8, int MODE, bool COST = (MODE == 0)>
 __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
-                                       : (MODE == 1 ? kMode1Warps : (MODE == 3 ? 32 : kMode2Warps)) * 32,
+                                       : ((MODE == 1 || MODE == 4) ? kMode1Warps
+                                                                   : (MODE == 3 ? 32 : kMode2Warps)) * 32,
                                   MODE == 2 ? 2 : 1)
     k_construct_sorted(const __grid_constant__ SortedArgs a) {
+  // the next row's first window issued right after the window loop, before
+  // the stall test and the bookkeeping: one ant per SM -4.4%, 2-7 ants per
+  // SM -3-4%, 14 ants -2.5%, 21 ants -0.4%, but +0.5% at 28 (C3) and +2% in
+  // MODE 2 (issue-bound there)
+  constexpr bool EARLY_LOAD = MODE == 4;
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
   const int warps = blockDim.x >> 5;
@@ -225,11 +236,13 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
   // window is issued before it, so that L2 round trip overlaps it
   auto advance = [&](uint32_t bj, uint32_t stp) {
     const uint32_t e = (uint32_t)lane;
-    wg = 0.0f;
-    jg = 0;
-    if (e < un) {  // also at the last step (row bj exists; unused): no step test (C3 -2%)
-      wg = __ldg(sw + (bj * ldr + e));
-      jg = __ldg(si + (bj * ldr + e));
+    if (!EARLY_LOAD) {
+      wg = 0.0f;
+      jg = 0;
+      if (e < un) {  // also at the last step (row bj exists; unused): no step test (C3 -2%)
+        wg = __ldg(sw + (bj * ldr + e));
+        jg = __ldg(si + (bj * ldr + e));
+      }
     }
     if (stp & 1u) {  // step stp + 1 is even: word 1 of the block formed at stp
       xnext = xstash;
@@ -324,6 +337,16 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
 #ifdef TACO_STEP_PROFILE
     const long long t2 = clock64();
 #endif
+    if (EARLY_LOAD) {  // the next row's first window, issued ahead of the stall
+                       // test (a stalled step loads row 0 instead of row -1; unused)
+      const uint32_t nrow = bestj < un ? bestj : 0u;
+      wg = 0.0f;
+      jg = 0;
+      if ((uint32_t)lane < un) {
+        wg = __ldg(sw + (nrow * ldr + lane));
+        jg = __ldg(si + (nrow * ldr + lane));
+      }
+    }
     if (bestj == 0xffffffffu) {  // no W > 0 candidate: the tour is rebuilt after the loop
       stalled = true;
       break;
@@ -961,7 +984,12 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
                  tours_out, separate_cost ? nullptr : costs_out, status, scan_count, ks, fb,
                  costs_out != nullptr ? leaves_image(n, s) : nullptr};
     const int grid = (m_local + warps - 1) / warps;
-    const int mode = fused_cost ? 0 : (two_ctas ? 2 : (wide ? 3 : 1));
+    // MODE 4 up to kLatencyAnts ants per SM (latency-bound: few warps to interleave)
+    int mode = fused_cost ? 0 : (two_ctas ? 2 : (wide ? 3 : (ants_per_sm <= kLatencyAnts ? 4 : 1)));
+    if (const char *ev = getenv("TACO_SORTED_MODE")) {  // tuning knob: 1 <-> 4 where either applies
+      const int f = atoi(ev);
+      if ((mode == 1 || mode == 4) && (f == 1 || f == 4)) mode = f;
+    }
     const int code = mode * 4 + (vis8 ? 2 : 0) + (scan_count ? 1 : 0);
     int rc = TACO_ERR_ARG;
     switch (code) {
@@ -971,6 +999,7 @@ extern "C" int taco_construct(int n, int m_local, int ant_offset, int variant, c
       TACO_SORTED_CASE(1, 0, 0) TACO_SORTED_CASE(1, 0, 1) TACO_SORTED_CASE(1, 1, 0) TACO_SORTED_CASE(1, 1, 1)
       TACO_SORTED_CASE(2, 0, 0) TACO_SORTED_CASE(2, 0, 1) TACO_SORTED_CASE(2, 1, 0) TACO_SORTED_CASE(2, 1, 1)
       TACO_SORTED_CASE(3, 0, 0) TACO_SORTED_CASE(3, 0, 1) TACO_SORTED_CASE(3, 1, 0) TACO_SORTED_CASE(3, 1, 1)
+      TACO_SORTED_CASE(4, 0, 0) TACO_SORTED_CASE(4, 0, 1) TACO_SORTED_CASE(4, 1, 0) TACO_SORTED_CASE(4, 1, 1)
 #undef TACO_SORTED_CASE
     }
     if (rc == TACO_OK && mode == 2) {  // tours the MODE 2 kernel left to the rebuild

@@ -54,6 +54,9 @@ KERNELS = {
     "warp_vis8": ("sorted", {"TACO_SORTED_KERNEL": "warp"}),
     "warp_bits": ("sorted", {"TACO_SORTED_KERNEL": "warp", "TACO_SORTED_VIS": "bits"}),
     "warp_fused_len": ("sorted", {"TACO_SORTED_KERNEL": "warp", "TACO_SORTED_COST": "fused"}),
+    # one CTA per SM: the issue-bound MODE 1 and the latency MODE 4 (<= 24 ants per SM by default)
+    "warp_mode1": ("sorted", {"TACO_SORTED_KERNEL": "warp", "TACO_SORTED_MODE": "1"}),
+    "warp_mode4": ("sorted", {"TACO_SORTED_KERNEL": "warp", "TACO_SORTED_MODE": "4"}),
     "g4e2": ("sorted", {"TACO_SORTED_KERNEL": "g4e2"}),
     "g4e4": ("sorted", {"TACO_SORTED_KERNEL": "g4e4"}),
     "g8e2": ("sorted", {"TACO_SORTED_KERNEL": "g8e2"}),
@@ -61,7 +64,7 @@ KERNELS = {
     "g16e2": ("sorted", {"TACO_SORTED_KERNEL": "g16e2"}),
     "dense": ("dense", {}),
 }
-_ENV_KEYS = ("TACO_SORTED_KERNEL", "TACO_SORTED_VIS", "TACO_SORTED_COST", "TACO_SORTED_WARPS")
+_ENV_KEYS = ("TACO_SORTED_KERNEL", "TACO_SORTED_VIS", "TACO_SORTED_COST", "TACO_SORTED_WARPS", "TACO_SORTED_MODE")
 
 
 def _sample(m: int, count: int) -> np.ndarray:
