@@ -571,7 +571,7 @@ static int launch_sort_t(int n, int r0, int r1, int ldw, const float *w, float *
 static int launch_sort(int n, int r0, int r1, int ldw, const float *w, float *sw, uint16_t *si, cudaStream_t s) {
   if (const char *ev = getenv("TACO_SORT_CFG")) {  // tuning knob: BLOCKxITEMS[xMINB]
     const std::string c(ev);
-    if (c == "256x20" && n <= 5120) return launch_sort_t<256, 20>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "512x10" && n <= 5120) return launch_sort_t<512, 10>(n, r0, r1, ldw, w, sw, si, s);
     if (c == "512x20x2" && n <= 10240) return launch_sort_t<512, 20, 2>(n, r0, r1, ldw, w, sw, si, s);
     if (c == "1024x10" && n <= 10240) return launch_sort_t<1024, 10>(n, r0, r1, ldw, w, sw, si, s);
     if (c == "256x10x4" && n <= 2560) return launch_sort_t<256, 10, 4>(n, r0, r1, ldw, w, sw, si, s);
@@ -580,7 +580,7 @@ static int launch_sort(int n, int r0, int r1, int ldw, const float *w, float *sw
   }
   if (n <= 1024) return launch_sort_t<128, 8>(n, r0, r1, ldw, w, sw, si, s);
   if (n <= 2560) return launch_sort_t<128, 20>(n, r0, r1, ldw, w, sw, si, s);  // vs 256x10: n = 2392 0.187 vs 0.194 ms (row + sort)
-  if (n <= 5120) return launch_sort_t<512, 10>(n, r0, r1, ldw, w, sw, si, s);
+  if (n <= 5120) return launch_sort_t<256, 20>(n, r0, r1, ldw, w, sw, si, s);  // vs 512x10: n = 5000 0.464 vs 0.484 ms (row + sort)
   if (n <= 10240) return launch_sort_t<512, 20>(n, r0, r1, ldw, w, sw, si, s);
   if (n <= 20480) return launch_sort_t<1024, 20>(n, r0, r1, ldw, w, sw, si, s);
   return TACO_ERR_UNSUPPORTED;
