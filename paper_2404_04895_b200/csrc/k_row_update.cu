@@ -486,8 +486,12 @@ static int launch_row(RowParams a, cudaStream_t stream) {
     if (b == 256) return launch_row_t<256>(a, lay, stream);
     if (b == 512) return launch_row_t<512>(a, lay, stream);
   }
+  // re-measured with the prebuilt plan (no per-CTA build): 128 threads at 8
+  // CTAs per SM up to n ~ 3000 (n = 2392: 0.157 vs 0.167 ms with the sort,
+  // n = 1000: 0.050 vs 0.056; n = 3500: 0.298 vs 0.284)
   if (a.n > 7000) return launch_row_t<512>(a, lay, stream);
-  return launch_row_t<256>(a, lay, stream);
+  if (a.n > 2800) return launch_row_t<256>(a, lay, stream);
+  return launch_row_t<128>(a, lay, stream);
 }
 
 // ---------------------------------------------------------------------------
