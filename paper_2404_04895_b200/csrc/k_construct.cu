@@ -168,6 +168,10 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
   // SM -3-4%, 14 ants -2.5%, 21 ants -0.4%, but +0.5% at 28 (C3) and +2% in
   // MODE 2 (issue-bound there)
   constexpr bool EARLY_LOAD = MODE == 4;
+  // the tour row stored by lane 0 every step instead of buffered in lanes and
+  // written 128 B at a time: fewer instructions per step (C3 -0.6%), but
+  // +2.6% in the 32-register MODE 2
+  constexpr bool TOUR_STG = MODE != 2;
   extern __shared__ __align__(16) unsigned char smem[];
   const int n = a.n;
   const int warps = blockDim.x >> 5;
@@ -210,7 +214,11 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
   __syncwarp();
 
   TourWriter tw{a.tours + (size_t)ant * n, n, lane, 0};
-  tw.put(0, (int32_t)start);
+  if (TOUR_STG) {
+    if (lane == 0) tw.row[0] = (int32_t)start;
+  } else {
+    tw.put(0, (int32_t)start);
+  }
   LeafCost lc;
   lc.init(COST && a.costs != nullptr ? a.dist : nullptr, leaves, leaf_buf, leaf_sum, n, lane);
   uint32_t cur = start;
@@ -257,7 +265,11 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
       lc.load(cur, bj);        // edge stp-1
     }
     __syncwarp();
-    tw.put((int)stp, (int32_t)bj);
+    if (TOUR_STG) {
+      if (lane == 0) tw.row[stp] = (int32_t)bj;
+    } else {
+      tw.put((int)stp, (int32_t)bj);
+    }
     cur = bj;
   };
   bool stalled = false;  // a step without a W > 0 candidate (rebuilt below)
@@ -273,66 +285,45 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
     const long long t1 = clock64();
     int nwin = 0;
 #endif
-    uint32_t base = 0;
-    while (!done) {
-#ifdef TACO_STEP_PROFILE
-      ++nwin;
-      if (nwin == 1) {  // phase probe of the first window (same arithmetic, results discarded)
-        const long long pa = clock64();
-        const uint32_t sink = consume(wg) ^ jg;
-        const long long pb = clock64();
-        const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
-        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(pos_word((uint32_t)lane, step, ak, rk)))) + 1u : 0u;
-        const uint32_t k2 = consume(__uint_as_float(key));
-        const long long pc = clock64();
-        const uint32_t mkey = __reduce_max_sync(kFull, k2);
-        const uint32_t jmin = __reduce_min_sync(kFull, k2 == mkey ? jg : 0xffffffffu);
-        const uint32_t j2 = consume(__uint_as_float(jmin));
-        const long long pd = clock64();
-        if (ant == 0 && lane == 0 && (sink ^ j2) != 0xdeadbeefu) {
-          g_step_prof[5] += pb - pa;
-          g_step_prof[6] += pc - pb;
-          g_step_prof[7] += pd - pc;
-        }
-      }
-#endif
+    // the first window, peeled out of the window loop (its uniforms were
+    // formed a step ahead; best is still -1, so no running-best test and the
+    // window's best entry wins): a straight-line common path (94% of steps
+    // end here), C3 -8%, C4 -4.7%
+    uint32_t base = 32;
+    {
       // entries after this window have W <= bucket_ceiling(window's last W);
       // the shuffle is issued first so that it overlaps the scoring
       const float wl = __shfl_sync(kFull, wg, 31);
-      if (base == 0) {
-        // first window: its uniforms were formed a step ahead (xnext); best
-        // is still -1, so no running-best test and the window's best wins
-        uint32_t x = xnext;
-        asm volatile("" : "+r"(x));
-        const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
-        base = 32;
-        if (__any_sync(kFull, cand)) {
-          const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(x))) + 1u : 0u;
-          const uint32_t mkey = __reduce_max_sync(kFull, key);
-          const uint32_t jsel = key == mkey ? jg : 0xffffffffu;
-          best = __uint_as_float(mkey - 1u);
-          // the stop test needs only the max: it runs while the min reduction
-          // is in flight (C3 -1%, one ant per SM -3%)
-          done = (bucket_ceiling(wl) < best) || (wl <= 0.0f) || (base >= un);
-          bestj = __reduce_min_sync(kFull, jsel);
-        } else {
-          done = (wl <= 0.0f) || (base >= un);
-        }
-      } else {
-        score_window<VIS8>(wg, jg, base + (uint32_t)lane, vis, step, ak, rk, best, bestj);
-        base += 32;
+      uint32_t x = xnext;
+      asm volatile("" : "+r"(x));
+      const bool cand = (wg > 0.0f) && !visited_at<VIS8>(vis, jg);
+      if (__any_sync(kFull, cand)) {
+        const uint32_t key = cand ? __float_as_uint(__fmul_rn(wg, bits_to_uniform(x))) + 1u : 0u;
+        const uint32_t mkey = __reduce_max_sync(kFull, key);
+        const uint32_t jsel = key == mkey ? jg : 0xffffffffu;
+        best = __uint_as_float(mkey - 1u);
+        // the stop test needs only the max: it runs while the min reduction
+        // is in flight (C3 -1%, one ant per SM -3%)
         done = (bucket_ceiling(wl) < best) || (wl <= 0.0f) || (base >= un);
+        bestj = __reduce_min_sync(kFull, jsel);
+      } else {
+        done = (wl <= 0.0f) || (base >= un);
       }
       if (PROBE) ++windows;
-      if (!done) {
-        const uint32_t e = base + lane;
-        wg = 0.0f;
-        jg = 0;
-        if (e < un) {
-          wg = __ldg(sw + (row + e));
-          jg = __ldg(si + (row + e));
-        }
+    }
+    while (!done) {  // later windows (6% of steps)
+      const uint32_t e = base + lane;
+      wg = 0.0f;
+      jg = 0;
+      if (e < un) {
+        wg = __ldg(sw + (row + e));
+        jg = __ldg(si + (row + e));
       }
+      const float wl = __shfl_sync(kFull, wg, 31);
+      score_window<VIS8>(wg, jg, e, vis, step, ak, rk, best, bestj);
+      base += 32;
+      done = (bucket_ceiling(wl) < best) || (wl <= 0.0f) || (base >= un);
+      if (PROBE) ++windows;
     }
 #ifdef TACO_STEP_PROFILE
     const long long t2 = clock64();
@@ -360,7 +351,7 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
       g_step_prof[1] += t2 - t1;
       g_step_prof[2] += t3 - t2;
       g_step_prof[3] += 1;
-      g_step_prof[4] += nwin;
+      g_step_prof[4] += (base >> 5);
     }
 #endif
   }
@@ -379,7 +370,8 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
     }
     return;
   }
-  tw.flush();
+  if (!TOUR_STG) tw.flush();
+  __syncwarp();
   if (COST && lc.active) {
     lc.push();  // edge n-2
     lc.load(cur, start);
