@@ -76,7 +76,7 @@ constexpr int kSortedMaxWarps = 28;      // fused tour length: 72 registers per 
 #endif
 constexpr int kMode1Warps = TACO_MODE1_WARPS;
 #ifndef TACO_LATENCY_ANTS
-#define TACO_LATENCY_ANTS 24
+#define TACO_LATENCY_ANTS 16
 #endif
 constexpr int kLatencyAnts = TACO_LATENCY_ANTS;  // MODE 4 up to this many ants per SM
 constexpr int kMode2Warps = TACO_MODE2_WARPS;  // 2 CTAs per SM: 65536 / (64 x this) registers
@@ -164,9 +164,9 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
                                   MODE == 2 ? 2 : 1)
     k_construct_sorted(const __grid_constant__ SortedArgs a) {
   // the next row's first window issued right after the window loop, before
-  // the stall test and the bookkeeping: one ant per SM -4.4%, 2-7 ants per
-  // SM -3-4%, 14 ants -2.5%, 21 ants -0.4%, but +0.5% at 28 (C3) and +2% in
-  // MODE 2 (issue-bound there)
+  // the stall test and the bookkeeping (with the peeled first window): one ant
+  // per SM -2.7%, 7 ants per SM -2%, 10-14 ants -1.5-2.5%, but +1% at 21,
+  // +2% at 28 (C3) and in MODE 2 (issue-bound there)
   constexpr bool EARLY_LOAD = MODE == 4;
   // the tour row stored by lane 0 every step instead of buffered in lanes and
   // written 128 B at a time: fewer instructions per step (C3 -0.6%), but
