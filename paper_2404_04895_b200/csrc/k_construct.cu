@@ -275,7 +275,10 @@ __global__ void __launch_bounds__(COST ? kSortedMaxWarps * 32
   bool stalled = false;  // a step without a W > 0 candidate (rebuilt below)
   // two steps per loop iteration (the step-pair Philox parity resolves at
   // compile time): C3 -2.5%, C4 -1.3%; not in the latency MODE 4 (+1.2%)
-  constexpr int kStepUnroll = MODE == 4 ? 1 : 2;
+#ifndef TACO_STEP_UNROLL
+#define TACO_STEP_UNROLL 2
+#endif
+  constexpr int kStepUnroll = MODE == 4 ? 1 : TACO_STEP_UNROLL;
 #pragma unroll kStepUnroll
   for (uint32_t step = 1; step < un; ++step) {
 #ifdef TACO_STEP_PROFILE
