@@ -12,6 +12,7 @@
 // (contiguous: the edge map is city-major).  The row lives in shared memory
 // between the phases so tau / unnorm are touched once.
 #include <cstdlib>
+#include <mutex>
 #include <string>
 
 #include <cub/block/block_radix_sort.cuh>
@@ -400,6 +401,8 @@ static const unsigned char *plan_image(int n, int L, cudaStream_t stream) {
   constexpr int kSlots = 8;
   static int ns[kMaxDevices][kSlots] = {};
   static unsigned char *imgs[kMaxDevices][kSlots] = {};
+  static std::mutex mu;  // host threads may launch concurrently (one stream each)
+  std::lock_guard<std::mutex> lock(mu);
   const int dev = current_device();
   for (int q = 0; q < kSlots; ++q)
     if (ns[dev][q] == n && imgs[dev][q] != nullptr) return imgs[dev][q];
@@ -415,7 +418,8 @@ static const unsigned char *plan_image(int n, int L, cudaStream_t stream) {
     return nullptr;
   }
   k_plan_image<<<1, 1, 0, stream>>>(n, L, img);
-  if (cudaGetLastError() != cudaSuccess) return nullptr;
+  // once per n and device: complete before any stream can pick the image up
+  if (cudaGetLastError() != cudaSuccess || cudaStreamSynchronize(stream) != cudaSuccess) return nullptr;
   ns[dev][slot] = n;
   imgs[dev][slot] = img;
   return img;
