@@ -148,12 +148,15 @@ def test_solver_construction_failure_leaves_tau_where_the_reference_raised():
     assert s.best()[1] == best_before[1] and np.array_equal(s.best()[0], best_before[0])
 
 
-# (variant, m, env): warp kernel MODE 1 (byte / bit-map visited set), MODE 2
-# (> 32 ants per SM: rebuilt by the follow-up k_rebuild_stalled), the
-# lane-group kernels and the dense kernel
+# (variant, m, env): warp kernel MODE 4 (<= 16 ants per SM, the default at
+# m = 64) and MODE 1, each with the byte / bit-map visited set, MODE 2 (> 32
+# ants per SM: rebuilt by the follow-up k_rebuild_stalled), the lane-group
+# kernels and the dense kernel
 FALLBACK_CASES = [
     ("sorted", 64, {}),
     ("sorted", 64, {"TACO_SORTED_VIS": "bits"}),
+    ("sorted", 64, {"TACO_SORTED_MODE": "1"}),
+    ("sorted", 64, {"TACO_SORTED_MODE": "1", "TACO_SORTED_VIS": "bits"}),
     ("sorted", 6000, {"TACO_SORTED_KERNEL": "warp"}),
     ("sorted", 6000, {"TACO_SORTED_KERNEL": "warp", "TACO_SORTED_VIS": "bits"}),
     ("sorted", 64, {"TACO_SORTED_KERNEL": "g8e2"}),
