@@ -586,13 +586,16 @@ static int launch_sort(int n, int r0, int r1, int ldw, const float *w, float *sw
     if (c == "256x10" && n <= 2560) return launch_sort_t<256, 10>(n, r0, r1, ldw, w, sw, si, s);
     if (c == "512x5" && n <= 2560) return launch_sort_t<512, 5>(n, r0, r1, ldw, w, sw, si, s);
     if (c == "128x20" && n <= 2560) return launch_sort_t<128, 20>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "128x8" && n <= 1024) return launch_sort_t<128, 8>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "256x20" && n <= 5120) return launch_sort_t<256, 20>(n, r0, r1, ldw, w, sw, si, s);
+    if (c == "512x20" && n <= 10240) return launch_sort_t<512, 20>(n, r0, r1, ldw, w, sw, si, s);
   }
-  if (n <= 1024) return launch_sort_t<128, 8>(n, r0, r1, ldw, w, sw, si, s);
+  if (n <= 1024) return launch_sort_t<96, 11>(n, r0, r1, ldw, w, sw, si, s);  // vs 128x8: n = 1000 0.046 vs 0.050 ms
   // vs 256x10 and 128x20 at n = 2392: 0.194 / 0.158 / 0.153 ms (row + sort)
   if (n <= 2400) return launch_sort_t<96, 25>(n, r0, r1, ldw, w, sw, si, s);
   if (n <= 2560) return launch_sort_t<128, 20>(n, r0, r1, ldw, w, sw, si, s);
-  if (n <= 5120) return launch_sort_t<256, 20>(n, r0, r1, ldw, w, sw, si, s);  // vs 512x10: n = 5000 0.464 vs 0.484 ms (row + sort)
-  if (n <= 10240) return launch_sort_t<512, 20>(n, r0, r1, ldw, w, sw, si, s);
+  if (n <= 5120) return launch_sort_t<192, 27>(n, r0, r1, ldw, w, sw, si, s);  // vs 512x10 / 256x20: n = 5000 0.484 / 0.464 / 0.456 ms
+  if (n <= 10240) return launch_sort_t<384, 27>(n, r0, r1, ldw, w, sw, si, s);  // vs 512x20: n = 10000 1.96 vs 2.01 ms
   if (n <= 20480) return launch_sort_t<1024, 20>(n, r0, r1, ldw, w, sw, si, s);
   return TACO_ERR_UNSUPPORTED;
 }
