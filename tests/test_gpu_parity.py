@@ -647,3 +647,27 @@ def test_row_update_plan_built_in_kernel_equals_prebuilt_image():
         outs.append([x.cpu().numpy() for x in (tau, rs, p, t.w, t.sw, t.si)])
     for a, b in zip(*outs):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("n", [97, 1000, 1024, 1025, 2392, 2400, 2401, 2560, 2561, 5000, 5120, 5121, 10000, 10240])
+def test_row_sort_order_at_every_cta_shape(n):
+    """The sorted table is row i of W in descending order of the W bits above
+    bit 16, stable in the column (the order the pruned scan and the sorted
+    stream's positions are defined on), for every row-sort CTA shape and at
+    both ends of each one's n range (k_row_sort: 96x11 up to 1024, 96x25 up
+    to 2400, 128x20 up to 2560, 192x27 up to 5120, 384x27 up to 10240)."""
+    dev = _device.device()
+    g = np.random.default_rng(n)
+    rows = np.unique(np.concatenate([[0, n - 1], g.integers(0, n, 6)]))
+    p = g.uniform(0.0, 1.0, (n, n)) ** 8  # wide exponent range: many equal 16-bit prefixes
+    p[g.uniform(size=(n, n)) < 0.05] = 0.0
+    np.fill_diagonal(p, 0.0)
+    p /= p.sum(axis=1, keepdims=True)
+    t = _device.SelectionTables(n, dev, dense=True, sorted_=True)
+    _device.selection_table_from_p(_device.upload(p, dev), 1.0, t)
+    torch.cuda.synchronize()
+    w = t.w.cpu().numpy()[rows, :n]
+    key = (w.view(np.uint32) >> 16).astype(np.int64)
+    want_si = np.argsort(-key, axis=1, kind="stable")
+    assert np.array_equal(t.si.cpu().numpy()[rows, :n].astype(np.int64), want_si)
+    assert np.array_equal(t.sw.cpu().numpy()[rows, :n], np.take_along_axis(w, want_si, axis=1))
