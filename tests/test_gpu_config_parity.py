@@ -46,6 +46,7 @@ CONFIGS = {
     "c3": (2392, 4096, "adair", 64),
     "c3_m4400": (2392, 4400, "adair", 32),  # 29.7 ants/SM: one 32-warp CTA per SM (warp MODE 3)
     "c4": (10000, 8192, "ir", 24),
+    "c5_256": (5000, 256, "ir", 32),  # 1.7 ants/SM: the latency MODE 4 at n = 5000
     "c5_65536": (5000, 65536, "ir", 48),
 }
 # label -> (variant, env overrides)
